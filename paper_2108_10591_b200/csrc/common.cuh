@@ -1,0 +1,136 @@
+// common.cuh — shared device-side types of libpbsafe (sm_100a).
+//
+// Floating-point contract: the whole library is compiled with -fmad=false and
+// the update/SpMV arithmetic is written with explicit __dmul_rn/__dadd_rn, so
+// every expression rounds exactly like the reference's numba loops
+// (kernels.py:95-137: a product rounded, then a sum rounded, left to right).
+// SpMV rows accumulate sequentially in ascending column order; only the dot
+// batch is reassociated (a fixed-shape tree, or the reference's own
+// PartitionPlan chains in PBS_REDUCE_PLAN mode).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/pbsafe.h"
+
+namespace pbs {
+
+constexpr int kThreads = 256;          // CTA size of every streaming kernel
+constexpr int kChunk = 2048;           // CSR products staged per smem chunk (16 KiB)
+constexpr int kNumDots = 9;            // a b c d e f g h r  (reduction.py:32)
+constexpr int kMaxStencil = 27;
+constexpr long long kNoError = 0x7fffffffffffffffLL;
+
+// dot slots in BATCH_LABELS order; _safe_batch pairs (solvers.py:467-482)
+enum Dot { DA = 0, DB, DC, DD, DE, DF, DG, DH, DR };
+
+// Host-visible mirror, written by the finalize kernel through mapped pinned
+// memory so the host can stop launching without a device sync.
+struct HostMirror {
+  volatile long long iter;
+  volatile int run_all;
+  volatile int err;
+};
+
+// Device-resident solver state.  Written by the single-CTA finalize kernel
+// (the reference's _Run bookkeeping + coefficient step) and by SpMV epilogues
+// (non-finite detection); read by every gated kernel.
+struct SolverState {
+  // configuration
+  double tol;
+  long long max_iters;
+  int record_history;
+  int spine_done;  // 1 for ssBiCGSafe2: the iteration's SpMV precedes the check
+  // carried scalars (solvers.py:631-632)
+  double alpha, beta, zeta, eta;
+  double f_prev;
+  double r0_norm;
+  double dots[kNumDots];
+  // control
+  long long iter;       // index of the next check the finalize kernel performs
+  int run_all;          // 0 once a check stopped the solve
+  int run_spine;        // the spine SpMV (As / Ar) still runs for the stop iteration
+  int status;           // -1 running, else PBS_CONVERGED...
+  int breakdown;
+  long long failure_iter;
+  long long iterations;
+  long long n_records;
+  // non-finite SpMV output (NonFiniteVectorError): first row, tag
+  unsigned long long nf_row;
+  int nf_tag;
+  int pad;
+  // history (device arrays, max_iters+1 slots)
+  double* hist_rel;
+  unsigned char* hist_flags;
+  double* hist_coef;
+  HostMirror* mirror;
+};
+
+__device__ __forceinline__ bool dev_err(const SolverState* st) {
+  return *(volatile const unsigned long long*)&st->nf_row != (unsigned long long)kNoError;
+}
+
+// kernels of the iteration body run while no check has stopped the solve
+__device__ __forceinline__ bool gate_all(const SolverState* st) {
+  return st == nullptr || (!dev_err(st) && st->run_all);
+}
+// the spine SpMV (As in p-BiCGSafe, Ar in ssBiCGSafe2) also runs on the
+// iteration whose check stops the solve (solvers.py:641-643, 530-531)
+__device__ __forceinline__ bool gate_spine(const SolverState* st) {
+  return st == nullptr || (!dev_err(st) && st->run_spine);
+}
+
+__device__ __forceinline__ void report_nonfinite(SolverState* st, int tag, long long row) {
+  if (st == nullptr) return;
+  atomicMin(&st->nf_row, (unsigned long long)row);
+  st->nf_tag = tag;
+}
+
+__device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
+
+// kernels.py:110-137 element expressions, association as written
+__device__ __forceinline__ double lc2(double sa, double a, double sb, double b) {
+  return add(mul(sa, a), mul(sb, b));
+}
+__device__ __forceinline__ double lc3(double sa, double a, double sb, double b, double sc, double c) {
+  return add(add(mul(sa, a), mul(sb, b)), mul(sc, c));
+}
+__device__ __forceinline__ double lc4(double sa, double a, double sb, double b, double sc, double c,
+                                      double sd, double d) {
+  return add(add(add(mul(sa, a), mul(sb, b)), mul(sc, c)), mul(sd, d));
+}
+__device__ __forceinline__ double lcn(double sa, double a, double sb, double b, double sc, double c) {
+  return add(mul(sa, a), mul(sb, add(b, mul(sc, c))));
+}
+__device__ __forceinline__ double asd(double base, double s, double a, double b) {
+  return add(base, mul(s, sub(a, b)));
+}
+__device__ __forceinline__ double asdd(double base, double s, double a, double w, double b) {
+  return add(base, mul(s, sub(a, mul(w, b))));
+}
+
+// Block-level reduction of 9 per-thread partials into partials[blk*9 + j];
+// fixed shape (xor-butterfly in warps, then warps in index order), so the
+// result depends only on the data-to-thread mapping, never on timing.
+__device__ __forceinline__ void block_reduce9(double (&acc)[kNumDots], double* out) {
+  __shared__ double red[kThreads / 32][kNumDots];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < kNumDots; ++j) {
+    double v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[warp][j] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kNumDots) {
+    double v = red[0][threadIdx.x];
+#pragma unroll
+    for (int w = 1; w < kThreads / 32; ++w) v = add(v, red[w][threadIdx.x]);
+    out[threadIdx.x] = v;
+  }
+}
+
+}  // namespace pbs

@@ -1,0 +1,1160 @@
+// pbsafe.cu — host side of libpbsafe: contexts, HBM operators, the solver
+// orchestration (CUDA graphs, device-side stop, no per-iteration host sync)
+// and the C-ABI declared in include/pbsafe.h.
+//
+// Per steady p-BiCGSafe iteration j (solvers.py:639-734) the device runs
+//   K1  As = A s                      (spine; also runs on the stop iteration)
+//   K2  p o u q w t z y x r updates   (one pass, o/q in registers)
+//   K3  Aw = A w -> l g s updates + the 9 dot partials of iteration j+1
+//   F   reduce partials, check j+1, coefficients (1 CTA)
+// captured once into a CUDA graph; residual-replacement iterations
+// (solvers.py:676-713) use a second graph.  The finalize kernel mirrors the
+// stop state into mapped host memory, so the host keeps a bounded number of
+// iterations in flight and stops launching once the device has stopped.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+#include <map>
+#include <thread>
+
+#include "common.cuh"
+#include "spmv.cuh"
+#include "vec.cuh"
+
+using namespace pbs;
+
+#define PBS_EXPORT extern "C" __attribute__((visibility("default")))
+
+static std::string g_last_error;
+
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  cudaEvent_t get() {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+  void reset() { used = 0; }
+  ~EventPool() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
+struct Workspace;
+
+struct pbs_ctx {
+  int device = 0;
+  int sms = 148;
+  int cc_major = 0, cc_minor = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  // kernel-table scratch (grow-only)
+  void* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  double* partials = nullptr;  // dot partials for ad-hoc reductions
+  SolverState* tmp_state = nullptr;
+  std::map<const void*, int> occ;  // kernel -> resident CTAs per SM
+  EventPool events;
+};
+
+struct pbs_mat {
+  pbs_ctx* ctx = nullptr;
+  int stencil = 0;
+  long long n_rows = 0, n_cols = 0, nnz = 0;
+  long long* rp = nullptr;
+  int* ci = nullptr;
+  double* v = nullptr;
+  StencilView sv{};
+  Workspace* ws = nullptr;
+};
+
+static int set_err(pbs_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  g_last_error = msg;
+  return code;
+}
+
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return set_err(ctx, PBS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int cap_per_sm = 8) {
+  auto it = ctx->occ.find(kernel);
+  int per_sm;
+  if (it == ctx->occ.end()) {
+    per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    ctx->occ[kernel] = per_sm;
+  } else {
+    per_sm = it->second;
+  }
+  if (per_sm > cap_per_sm) per_sm = cap_per_sm;
+  long long g = (long long)ctx->sms * per_sm;
+  if (work_blocks < g) g = work_blocks;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+constexpr int kMaxParts = 148 * 16;
+
+// ------------------------------------------------------------------ workspace
+
+struct Workspace {
+  long long n = 0;
+  size_t stride = 0;  // padded elements per vector
+  double* base = nullptr;
+  VecPtrs V{};
+  double* partials = nullptr;
+  long long* plan_bounds = nullptr;
+  int plan_workers = 0;
+  int plan_w_actual = 0;
+  SolverState* st = nullptr;
+  HostMirror* mirror_h = nullptr;
+  HostMirror* mirror_d = nullptr;
+  double* hist_rel = nullptr;
+  unsigned char* hist_flags = nullptr;
+  double* hist_coef = nullptr;
+  long long hist_cap = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  double* trace_host = nullptr;  // pinned staging for trace_hook (13 vectors)
+  // graph cache: key -> exec
+  std::map<long long, cudaGraphExec_t> graphs;
+};
+
+static void free_graphs(Workspace* ws) {
+  for (auto& kv : ws->graphs) cudaGraphExecDestroy(kv.second);
+  ws->graphs.clear();
+}
+
+static void free_ws(Workspace* ws) {
+  if (!ws) return;
+  free_graphs(ws);
+  cudaFree(ws->base);
+  cudaFree(ws->partials);
+  cudaFree(ws->plan_bounds);
+  cudaFree(ws->st);
+  if (ws->mirror_h) cudaFreeHost(ws->mirror_h);
+  cudaFree(ws->hist_rel);
+  cudaFree(ws->hist_flags);
+  cudaFree(ws->hist_coef);
+  if (ws->ev0) cudaEventDestroy(ws->ev0);
+  if (ws->ev1) cudaEventDestroy(ws->ev1);
+  if (ws->trace_host) cudaFreeHost(ws->trace_host);
+  delete ws;
+}
+
+static int ensure_ws(pbs_mat* m, long long hist_slots) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  if (!ws) {
+    ws = new Workspace();
+    m->ws = ws;
+    ws->n = m->n_rows;
+    ws->stride = ((size_t)(ws->n > 0 ? ws->n : 1) + 31) / 32 * 32;
+    CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
+    for (int k = 0; k < kNumVecs; ++k) ws->V.v[k] = ws->base + ws->stride * k;
+    CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kNumDots));
+    CK(cudaMalloc(&ws->st, sizeof(SolverState)));
+    CK(cudaHostAlloc(&ws->mirror_h, sizeof(HostMirror), cudaHostAllocMapped));
+    CK(cudaHostGetDevicePointer((void**)&ws->mirror_d, ws->mirror_h, 0));
+    CK(cudaEventCreate(&ws->ev0));
+    CK(cudaEventCreate(&ws->ev1));
+  }
+  if (hist_slots > ws->hist_cap) {
+    cudaFree(ws->hist_rel);
+    cudaFree(ws->hist_flags);
+    cudaFree(ws->hist_coef);
+    long long cap = hist_slots < 1024 ? 1024 : hist_slots;
+    CK(cudaMalloc(&ws->hist_rel, sizeof(double) * cap));
+    CK(cudaMalloc(&ws->hist_flags, cap));
+    CK(cudaMalloc(&ws->hist_coef, sizeof(double) * 4 * cap));
+    ws->hist_cap = cap;
+    free_graphs(ws);  // graphs capture the state pointer only, but keep it simple
+  }
+  return PBS_OK;
+}
+
+// PartitionPlan.balanced (reduction.py:80-87) bounds, numpy linspace semantics
+static int plan_balanced(long long n, long long workers, std::vector<long long>& b) {
+  long long cap = n > 1 ? n : 1;
+  if (workers > cap) workers = cap;
+  b.resize(workers + 1);
+  double step = (double)n / (double)workers;
+  for (long long k = 0; k < workers; ++k) {
+    double y = (step == 0.0) ? ((double)k / (double)workers) * (double)n : (double)k * step;
+    b[k] = (long long)y;
+  }
+  b[workers] = n;
+  return (int)workers;
+}
+
+static int ensure_plan(pbs_mat* m, int workers) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  if (workers < 1) return set_err(ctx, PBS_ERR_INVALID, "plan_workers must be >= 1");
+  if (ws->plan_workers == workers && ws->plan_bounds) return PBS_OK;
+  std::vector<long long> b;
+  int w = plan_balanced(ws->n, workers, b);
+  if (w > kMaxParts) return set_err(ctx, PBS_ERR_INVALID, "plan_workers too large for the device plan");
+  cudaFree(ws->plan_bounds);
+  CK(cudaMalloc(&ws->plan_bounds, sizeof(long long) * (w + 1)));
+  CK(cudaMemcpy(ws->plan_bounds, b.data(), sizeof(long long) * (w + 1), cudaMemcpyHostToDevice));
+  ws->plan_workers = workers;
+  ws->plan_w_actual = w;
+  free_graphs(ws);
+  return PBS_OK;
+}
+
+// ------------------------------------------------------------------ launching
+
+enum Kind { KK1 = 0, KK2, KK3, KF, KR, KRS, KS, KD };
+
+struct Launcher {
+  pbs_ctx* ctx;
+  pbs_mat* m;
+  cudaStream_t s;
+  bool timing = false;
+  std::vector<std::pair<int, cudaEvent_t>>* marks = nullptr;
+  long long launches = 0;
+  // trace_hook support: called by the iteration bodies where the reference
+  // calls trace_hook (after the updates, before the next check)
+  const pbs_config* trace_cfg = nullptr;
+  Workspace* trace_ws = nullptr;
+  long long iter = 0;
+  int trace_rc = 0;
+  void trace_point();
+  void done(int kind) {
+    ++launches;
+    if (timing && marks) {
+      cudaEvent_t e = ctx->events.get();
+      cudaEventRecord(e, s);
+      marks->push_back({kind, e});
+    }
+  }
+};
+
+void Launcher::trace_point() {
+  if (!trace_cfg || !trace_cfg->trace_fn || trace_rc) return;
+  Workspace* ws = trace_ws;
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    trace_rc = set_err(ctx, PBS_ERR_CUDA, "sync failed while tracing");
+    return;
+  }
+  SolverState st;
+  cudaMemcpy(&st, ws->st, sizeof(st), cudaMemcpyDeviceToHost);
+  if (!st.run_all || st.nf_row != (unsigned long long)kNoError) return;  // iteration did not run
+  const size_t n = (size_t)ws->n;
+  if (!ws->trace_host &&
+      cudaHostAlloc(&ws->trace_host, sizeof(double) * 13 * (n > 0 ? n : 1), cudaHostAllocDefault) != cudaSuccess) {
+    trace_rc = set_err(ctx, PBS_ERR_NOMEM, "cannot allocate trace staging");
+    return;
+  }
+  const int order[13] = {VX, VR, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL};
+  double* ptrs[13];
+  for (int k = 0; k < 13; ++k) {
+    ptrs[k] = ws->trace_host + k * n;
+    cudaMemcpy(ptrs[k], ws->V.v[order[k]], sizeof(double) * n, cudaMemcpyDeviceToHost);
+  }
+  trace_cfg->trace_fn(iter, ptrs, trace_cfg->trace_user);
+}
+
+template <class Epi>
+static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long long hi, int kind) {
+  pbs_mat* m = L.m;
+  long long nblk = (hi - lo + kThreads - 1) / kThreads;
+  int grid;
+  if (!m->stencil) {
+    CsrView A{m->rp, m->ci, m->v, lo, hi};
+    grid = grid_for(L.ctx, (const void*)csr_spmv_kernel<Epi>, nblk);
+    csr_spmv_kernel<Epi><<<grid, kThreads, 0, L.s>>>(A, x, epi);
+  } else {
+    StencilView S = m->sv;
+    S.row_lo = lo;
+    S.row_hi = hi;
+#define PBS_STENCIL(D, NP)                                                                 \
+  {                                                                                        \
+    grid = grid_for(L.ctx, (const void*)stencil_spmv_kernel<Epi, D, NP>, nblk);            \
+    stencil_spmv_kernel<Epi, D, NP><<<grid, kThreads, 0, L.s>>>(S, x, epi);               \
+  }
+    if (S.dim == 3 && S.npts == 7) PBS_STENCIL(3, 7)
+    else if (S.dim == 3 && S.npts == 27) PBS_STENCIL(3, 27)
+    else if (S.dim == 3) PBS_STENCIL(3, 0)
+    else if (S.dim == 2 && S.npts == 5) PBS_STENCIL(2, 5)
+    else if (S.dim == 2) PBS_STENCIL(2, 0)
+    else if (S.dim == 1 && S.npts == 3) PBS_STENCIL(1, 3)
+    else PBS_STENCIL(1, 0)
+#undef PBS_STENCIL
+  }
+  L.done(kind);
+  return grid;
+}
+
+template <class K, class... Args>
+static void vec_launch(Launcher& L, K kernel, long long n, int kind, Args... args) {
+  long long nblk = (n + kThreads - 1) / kThreads;
+  int grid = grid_for(L.ctx, (const void*)kernel, nblk);
+  kernel<<<grid, kThreads, 0, L.s>>>(args...);
+  L.done(kind);
+}
+
+struct Mode {
+  int plan = 0;  // PBS_REDUCE_PLAN
+  int store_temps = 0;
+};
+
+// batch partials over (s, y, r, r0s, t) for PLAN mode (tree mode fuses them
+// into the producing SpMV); returns nparts
+static int plan_dots(Launcher& L, Workspace* ws, int kind) {
+  dots9_plan_kernel<<<ws->plan_w_actual, 32, 0, L.s>>>(ws->plan_bounds, ws->V.v[VS], ws->V.v[VY],
+                                                      ws->V.v[VR], ws->V.v[VR0S], ws->V.v[VT],
+                                                      ws->partials, ws->st);
+  L.done(kind);
+  return ws->plan_w_actual;
+}
+
+static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int replaced) {
+  finalize_kernel<<<1, 288, 0, L.s>>>(ws->st, ws->partials, nparts, chain, replaced);
+  L.done(KF);
+}
+
+// s = A r (+ dot partials); returns nparts
+static int spmv_s_dots(Launcher& L, Workspace* ws, const Mode& md, int kind, int spine) {
+  auto& V = ws->V.v;
+  EpiDots e{V[VS], V[VY], V[VR], V[VR0S], V[VT], md.plan ? nullptr : ws->partials, ws->st,
+            PBS_TAG_AR, spine};
+  int grid = spmv_launch(L, V[VR], e, 0, ws->n, kind);
+  if (md.plan) return plan_dots(L, ws, KD);
+  return grid;
+}
+
+// setup of the pipelined methods (solvers.py:612-631) + check 0
+static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  EpiResid er{V[VB], V[VR], V[VR0S], ws->st};
+  spmv_launch(L, V[VX], er, 0, ws->n, KS);
+  int np = spmv_s_dots(L, ws, md, KS, 0);
+  finalize(L, ws, np, md.plan, 0);
+}
+
+// one steady p-BiCGSafe iteration (K1 K2 K3 F)
+static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
+  spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+  vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
+  EpiK3 e3{};
+  e3.as = V[VAS];
+  e3.l = V[VL];
+  e3.g = V[VG];
+  e3.s = V[VS];
+  e3.y = V[VY];
+  e3.r = V[VR];
+  e3.r0s = V[VR0S];
+  e3.t = V[VT];
+  e3.q_out = md.store_temps ? V[VQ] : nullptr;
+  e3.partials = md.plan ? nullptr : ws->partials;
+  e3.st = ws->st;
+  int np = spmv_launch(L, V[VW], e3, 0, ws->n, KK3);
+  if (md.plan) np = plan_dots(L, ws, KD);
+  L.trace_point();
+  finalize(L, ws, np, md.plan, 0);
+}
+
+// residual-replacement iteration (solvers.py:676-713)
+static void iter_replace(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
+  spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+  vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+  EpiStore eq{V[VQ], ws->st, PBS_TAG_AO, 0};
+  spmv_launch(L, V[VO], eq, 0, ws->n, KRS);
+  EpiStore ew{V[VW], ws->st, PBS_TAG_AU, 0};
+  spmv_launch(L, V[VU], ew, 0, ws->n, KRS);
+  vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+  EpiResid er{V[VB], V[VR], nullptr, ws->st};
+  spmv_launch(L, V[VX], er, 0, ws->n, KRS);
+  EpiStore el{V[VL], ws->st, PBS_TAG_AT, 0};
+  spmv_launch(L, V[VT], el, 0, ws->n, KRS);
+  EpiStore eg{V[VG], ws->st, PBS_TAG_AY, 0};
+  spmv_launch(L, V[VY], eg, 0, ws->n, KRS);
+  int np = spmv_s_dots(L, ws, md, KRS, 0);
+  L.trace_point();
+  finalize(L, ws, np, md.plan, 1);
+}
+
+// one ssBiCGSafe2 iteration (solvers.py:528-587): s = A r + batch, check,
+// p o u, w = A u + t z y x r
+static void iter_ss(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  int np = spmv_s_dots(L, ws, md, KK1, 1);
+  finalize(L, ws, np, md.plan, 0);
+  vec_launch(L, pou_kernel, ws->n, KK2, ws->V, ws->n, ws->st);
+  EpiSS3 e{V[VW], V[VO], V[VS], V[VU], V[VP], V[VT], V[VZ], V[VY], V[VX], V[VR], ws->st};
+  spmv_launch(L, V[VU], e, 0, ws->n, KK3);
+  L.trace_point();
+}
+
+// final record of ssBiCGSafe2 after max_iters: plan_dot(r, r) (solvers.py:589)
+static void final_ss(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  int np;
+  if (md.plan) {
+    np = plan_dots(L, ws, KD);
+  } else {
+    long long nblk = (ws->n + kThreads - 1) / kThreads;
+    np = grid_for(L.ctx, (const void*)dots9_tree_kernel, nblk);
+    dots9_tree_kernel<<<np, kThreads, 0, L.s>>>(ws->n, V[VS], V[VY], V[VR], V[VR0S], V[VT],
+                                                ws->partials, ws->st);
+    L.done(KD);
+  }
+  finalize(L, ws, np, md.plan, 0);
+}
+
+typedef void (*IterFn)(Launcher&, Workspace*, const Mode&);
+
+static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const Mode& md,
+                     cudaGraphExec_t* out) {
+  Workspace* ws = m->ws;
+  auto it = ws->graphs.find(key);
+  if (it != ws->graphs.end()) {
+    *out = it->second;
+    return PBS_OK;
+  }
+  cudaGraph_t g;
+  Launcher L{ctx, m, ctx->stream};
+  CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  fn(L, ws, md);
+  cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+  cudaGraphExec_t ge;
+  e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  ws->graphs[key] = ge;
+  *out = ge;
+  return PBS_OK;
+}
+
+// ------------------------------------------------------------------- solving
+
+static int validate_cfg(pbs_ctx* ctx, const pbs_config* cfg) {
+  if (!cfg) return set_err(ctx, PBS_ERR_INVALID, "config is NULL");
+  if (!(cfg->tol > 0.0)) return set_err(ctx, PBS_ERR_INVALID, "tol must be positive");
+  if (cfg->max_iters < 1) return set_err(ctx, PBS_ERR_INVALID, "max_iters must be >= 1");
+  if (cfg->rr_epoch < 1) return set_err(ctx, PBS_ERR_INVALID, "rr_epoch must be >= 1");
+  if (cfg->rr_cutoff > cfg->max_iters) return set_err(ctx, PBS_ERR_INVALID, "rr_cutoff must lie in [0, max_iters]");
+  if (cfg->reduce_mode != PBS_REDUCE_TREE && cfg->reduce_mode != PBS_REDUCE_PLAN)
+    return set_err(ctx, PBS_ERR_INVALID, "unknown reduce_mode");
+  return PBS_OK;
+}
+
+// Runs a solve with b / x0 already in the workspace (VB, VX).
+static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* res) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  const long long n = ws->n;
+  Mode md;
+  md.plan = cfg->reduce_mode == PBS_REDUCE_PLAN;
+  const bool tracing = cfg->trace_fn != nullptr;
+  md.store_temps = tracing ? 1 : 0;
+  if (md.plan) {
+    int rc = ensure_plan(m, cfg->plan_workers);
+    if (rc) return rc;
+  }
+  cudaStream_t s = ctx->stream;
+  // device state
+  SolverState h{};
+  h.tol = cfg->tol;
+  h.max_iters = cfg->max_iters;
+  h.record_history = cfg->record_history ? 1 : 0;
+  h.spine_done = method == PBS_METHOD_SSBICGSAFE2 ? 1 : 0;
+  h.iter = 0;
+  h.run_all = 1;
+  h.run_spine = 1;
+  h.status = -1;
+  h.failure_iter = -1;
+  h.nf_row = (unsigned long long)kNoError;
+  h.hist_rel = ws->hist_rel;
+  h.hist_flags = ws->hist_flags;
+  h.hist_coef = ws->hist_coef;
+  h.mirror = ws->mirror_d;
+  ws->mirror_h->iter = 0;
+  ws->mirror_h->run_all = 1;
+  ws->mirror_h->err = 0;
+  CK(cudaMemcpyAsync(ws->st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  // zero-initialised workspace (solvers.py:621-628)
+  const int zero_slots[] = {VP, VU, VT, VY, VZ, VG, VL, VW};
+  for (int k : zero_slots) CK(cudaMemsetAsync(ws->V.v[k], 0, sizeof(double) * n, s));
+
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  ctx->events.reset();
+  Launcher L{ctx, m, s};
+  L.timing = cfg->timing != 0 && !tracing;
+  L.marks = &marks;
+  if (tracing) {
+    L.trace_cfg = cfg;
+    L.trace_ws = ws;
+  }
+  const bool graphs = cfg->use_graphs && !L.timing && !tracing;
+  const bool pipelined = method != PBS_METHOD_SSBICGSAFE2;
+  const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
+  const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
+  const long long key_base = (long long)md.plan * 4;
+
+  CK(cudaEventRecord(ws->ev0, s));
+  if (L.timing) marks.push_back({-1, ws->ev0});
+  if (pipelined) {
+    setup_pipelined(L, ws, md);
+  } else {
+    EpiResid er{ws->V.v[VB], ws->V.v[VR], ws->V.v[VR0S], ws->st};
+    spmv_launch(L, ws->V.v[VX], er, 0, n, KS);
+  }
+  const long long lookahead = 6;
+  long long launched_graph_kernels = 0;
+  long long j = 0;
+  for (; j < cfg->max_iters; ++j) {
+    // stop once the device has stopped (the stop iteration's spine SpMV is
+    // part of iteration j = stop, so keep launching through it)
+    for (;;) {
+      const long long dev_iter = ws->mirror_h->iter;
+      if (ws->mirror_h->err) goto loop_end;
+      if (!ws->mirror_h->run_all && j >= dev_iter) goto loop_end;
+      if (j <= dev_iter + lookahead) break;
+      if (cudaStreamQuery(s) == cudaSuccess) continue;  // re-read the mirror
+      std::this_thread::yield();
+    }
+    {
+      const bool replace = rr && (j % cfg->rr_epoch == 0) && 0 < j && j < cutoff;
+      IterFn fn = !pipelined ? iter_ss : (replace ? iter_replace : iter_steady);
+      if (graphs) {
+        long long key = key_base + (!pipelined ? 2 : (replace ? 1 : 0));
+        cudaGraphExec_t ge;
+        int rc = get_graph(ctx, m, key, fn, md, &ge);
+        if (rc) return rc;
+        CK(cudaGraphLaunch(ge, s));
+        launched_graph_kernels += !pipelined ? 4 + md.plan : (replace ? 10 : 4) + md.plan;
+      } else {
+        L.iter = j;
+        fn(L, ws, md);
+        if (L.trace_rc) return L.trace_rc;
+      }
+    }
+  }
+  if (!pipelined) final_ss(L, ws, md);
+loop_end:
+  CK(cudaEventRecord(ws->ev1, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  SolverState out;
+  CK(cudaMemcpy(&out, ws->st, sizeof(out), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+  memset(res, 0, sizeof(*res));
+  res->device_ms = ms;
+  res->kernel_launches = L.launches + launched_graph_kernels;
+  if (L.timing) {
+    for (size_t k = 1; k < marks.size(); ++k) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, marks[k - 1].second, marks[k].second);
+      int kind = marks[k].first;
+      if (kind >= 0 && kind < PBS_NUM_KERNEL_KINDS) {
+        res->kernel_ms[kind] += d;
+        res->kernel_count[kind] += 1;
+      }
+    }
+  }
+  res->status = out.status;
+  res->breakdown = out.breakdown;
+  res->iterations = out.iterations;
+  res->failure_iter = out.failure_iter;
+  res->n_records = out.n_records;
+  res->r0_norm = out.r0_norm;
+  res->nonfinite_index = -1;
+  if (out.nf_row != (unsigned long long)kNoError) {
+    res->nonfinite_tag = out.nf_tag;
+    res->nonfinite_index = (long long)out.nf_row;
+    return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output");
+  }
+  if (out.status < 0) return set_err(ctx, PBS_ERR_CUDA, "solver ended without a status");
+  // SpMV count as the reference tallies it (solvers.py:613-723, 530-569)
+  const long long reached = out.status == PBS_MAX_ITERS || out.iterations == cfg->max_iters
+                                ? cfg->max_iters
+                                : out.iterations + 1;
+  const long long completed = out.iterations;
+  long long nrep = 0;
+  if (rr)
+    for (long long i = 1; i < completed && i < cutoff; ++i)
+      if (i % cfg->rr_epoch == 0) ++nrep;
+  res->n_replacements = nrep;
+  if (pipelined)
+    res->n_spmv = 2 + reached + completed + 5 * nrep;
+  else
+    res->n_spmv = 1 + reached + completed;
+  return PBS_OK;
+}
+
+static int copy_history(pbs_mat* m, const pbs_result* res, double* hist_rel, uint8_t* hist_flags,
+                        double* hist_coef) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  long long k = res->n_records;
+  if (k <= 0) return PBS_OK;
+  if (hist_rel) CK(cudaMemcpy(hist_rel, ws->hist_rel, sizeof(double) * k, cudaMemcpyDeviceToHost));
+  if (hist_flags) CK(cudaMemcpy(hist_flags, ws->hist_flags, k, cudaMemcpyDeviceToHost));
+  if (hist_coef) CK(cudaMemcpy(hist_coef, ws->hist_coef, sizeof(double) * 4 * k, cudaMemcpyDeviceToHost));
+  return PBS_OK;
+}
+
+// ============================================================== C-ABI
+
+PBS_EXPORT const char* pbs_last_error(pbs_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+PBS_EXPORT int pbs_init(int device, pbs_ctx** out) {
+  pbs_ctx* ctx = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return set_err(nullptr, PBS_ERR_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= count) return set_err(nullptr, PBS_ERR_INVALID, "device index out of range");
+  ctx = new pbs_ctx();
+  ctx->device = device;
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  ctx->sms = prop.multiProcessorCount;
+  ctx->cc_major = prop.major;
+  ctx->cc_minor = prop.minor;
+  if (prop.major != 10) {
+    std::string msg = std::string("libpbsafe is built for sm_100a; device is sm_") +
+                      std::to_string(prop.major) + std::to_string(prop.minor);
+    delete ctx;
+    return set_err(nullptr, PBS_ERR_UNSUPPORTED, msg);
+  }
+  CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
+  ctx->stream = ctx->own;
+  CK(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * kNumDots));
+  CK(cudaMalloc(&ctx->tmp_state, sizeof(SolverState)));
+  *out = ctx;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_destroy(pbs_ctx* ctx) {
+  if (!ctx) return PBS_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->scratch);
+  cudaFree(ctx->partials);
+  cudaFree(ctx->tmp_state);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_device_info(pbs_ctx* ctx, int* sm_count, int* cc_major, int* cc_minor) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  if (sm_count) *sm_count = ctx->sms;
+  if (cc_major) *cc_major = ctx->cc_major;
+  if (cc_minor) *cc_minor = ctx->cc_minor;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_set_stream(pbs_ctx* ctx, uintptr_t stream) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  ctx->stream = stream ? (cudaStream_t)stream : ctx->own;
+  return PBS_OK;
+}
+
+__global__ void cvt_i64_i32_kernel(const long long* in, int* out, long long n, int* bad, long long ncols) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    long long c = in[i];
+    if (c < 0 || c >= ncols) *bad = 1;
+    out[i] = (int)c;
+  }
+}
+
+PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                              const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
+                              const double* values, pbs_mat** out) {
+  if (!ctx || !out) return set_err(ctx, PBS_ERR_INVALID, "NULL argument");
+  if (n_rows < 0 || n_cols < 0 || nnz < 0) return set_err(ctx, PBS_ERR_INVALID, "negative matrix dimension");
+  if (n_cols > 0x7fffffffLL) return set_err(ctx, PBS_ERR_INVALID, "n_cols exceeds the int32 column index range");
+  if (col_bytes != 4 && col_bytes != 8) return set_err(ctx, PBS_ERR_INVALID, "col_bytes must be 4 or 8");
+  if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
+    return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with nnz arrays");
+  CK(cudaSetDevice(ctx->device));
+  pbs_mat* m = new pbs_mat();
+  m->ctx = ctx;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->nnz = nnz;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMalloc(&m->rp, sizeof(long long) * (n_rows + 1)));
+  CK(cudaMalloc(&m->ci, sizeof(int) * (nnz > 0 ? nnz : 1)));
+  CK(cudaMalloc(&m->v, sizeof(double) * (nnz > 0 ? nnz : 1)));
+  CK(cudaMemcpyAsync(m->rp, row_ptr, sizeof(long long) * (n_rows + 1), cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    if (col_bytes == 4) {
+      CK(cudaMemcpyAsync(m->ci, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
+    } else {
+      // stage int64 indices in chunks and narrow on the device
+      const long long chunk = 1LL << 24;
+      long long* tmp = nullptr;
+      int* bad = nullptr;
+      CK(cudaMalloc(&tmp, sizeof(long long) * (nnz < chunk ? nnz : chunk)));
+      CK(cudaMalloc(&bad, sizeof(int)));
+      CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+      for (long long off = 0; off < nnz; off += chunk) {
+        long long len = nnz - off < chunk ? nnz - off : chunk;
+        CK(cudaMemcpyAsync(tmp, (const long long*)col_idx + off, sizeof(long long) * len,
+                           cudaMemcpyHostToDevice, s));
+        cvt_i64_i32_kernel<<<ctx->sms * 4, 256, 0, s>>>(tmp, m->ci + off, len, bad, n_cols);
+      }
+      int hbad = 0;
+      CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      cudaFree(tmp);
+      cudaFree(bad);
+      if (hbad) {
+        pbs_mat_free(m);
+        return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
+      }
+    }
+  }
+  CK(cudaStreamSynchronize(s));
+  *out = m;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t npts,
+                                  const int32_t* offsets, const double* coeffs, pbs_mat** out) {
+  if (!ctx || !out) return set_err(ctx, PBS_ERR_INVALID, "NULL argument");
+  if (dim < 1 || dim > 3) return set_err(ctx, PBS_ERR_INVALID, "dim must be 1, 2, or 3");
+  if (k < 1) return set_err(ctx, PBS_ERR_INVALID, "k must be >= 1");
+  if (npts < 1 || npts > kMaxStencil) return set_err(ctx, PBS_ERR_INVALID, "npts must be in [1, 27]");
+  long long n = 1;
+  for (int a = 0; a < dim; ++a) n *= k;
+  if (n > 0x7fffffffLL) return set_err(ctx, PBS_ERR_INVALID, "grid exceeds the supported size");
+  pbs_mat* m = new pbs_mat();
+  m->ctx = ctx;
+  m->stencil = 1;
+  m->n_rows = m->n_cols = n;
+  StencilView& S = m->sv;
+  S.n = n;
+  S.k = k;
+  S.k2 = k * k;
+  S.dim = dim;
+  S.npts = npts;
+  long long nnz = 0;
+  long long prev = -(1LL << 62);
+  for (int p = 0; p < npts; ++p) {
+    long long f = 0;
+    for (int a = 0; a < 3; ++a) S.off[p][a] = 0;
+    for (int a = 0; a < dim; ++a) {
+      int d = offsets[p * dim + a];
+      if (d < -1 || d > 1) {
+        delete m;
+        return set_err(ctx, PBS_ERR_INVALID, "stencil offsets must lie in {-1, 0, 1}");
+      }
+      S.off[p][3 - dim + a] = d;
+      long long w = 1;
+      for (int b = a + 1; b < dim; ++b) w *= k;
+      f += d * w;
+    }
+    if (f <= prev) {
+      delete m;
+      return set_err(ctx, PBS_ERR_INVALID, "stencil offsets must be sorted by flattened offset");
+    }
+    prev = f;
+    S.foff[p] = f;
+    S.coef[p] = coeffs[p];
+    long long cnt = 1;
+    for (int a = 0; a < dim; ++a) cnt *= (k - (offsets[p * dim + a] != 0 ? 1 : 0));
+    nnz += cnt;
+  }
+  m->nnz = nnz;
+  *out = m;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
+  if (!m) return PBS_OK;
+  cudaSetDevice(m->ctx->device);
+  cudaStreamSynchronize(m->ctx->stream);
+  free_ws(m->ws);
+  cudaFree(m->rp);
+  cudaFree(m->ci);
+  cudaFree(m->v);
+  delete m;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_mat_info(pbs_mat* m, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* is_stencil) {
+  if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
+  if (n_rows) *n_rows = m->n_rows;
+  if (n_cols) *n_cols = m->n_cols;
+  if (nnz) *nnz = m->nnz;
+  if (is_stencil) *is_stencil = m->stencil;
+  return PBS_OK;
+}
+
+static int reset_tmp_state(pbs_ctx* ctx) {
+  SolverState h{};
+  h.run_all = 1;
+  h.run_spine = 1;
+  h.nf_row = (unsigned long long)kNoError;
+  CK(cudaMemcpyAsync(ctx->tmp_state, &h, sizeof(h), cudaMemcpyHostToDevice, ctx->stream));
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t* nonfinite_index) {
+  if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
+  pbs_ctx* ctx = m->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = reset_tmp_state(ctx);
+  if (rc) return rc;
+  Launcher L{ctx, m, ctx->stream};
+  EpiStore e{d_y, ctx->tmp_state, PBS_TAG_AX, 0};
+  spmv_launch(L, d_x, e, 0, m->n_rows, KS);
+  unsigned long long row = 0;
+  CK(cudaMemcpyAsync(&row, &ctx->tmp_state->nf_row, sizeof(row), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (nonfinite_index) *nonfinite_index = row == (unsigned long long)kNoError ? -1 : (int64_t)row;
+  return PBS_OK;
+}
+
+static int solve_common(pbs_mat* m, int32_t method, const pbs_config* cfg) {
+  pbs_ctx* ctx = m ? m->ctx : nullptr;
+  if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
+  if (m->n_rows != m->n_cols) return set_err(ctx, PBS_ERR_INVALID, "solver needs a square operator");
+  if (method < 0 || method > 2) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
+  int rc = validate_cfg(ctx, cfg);
+  if (rc) return rc;
+  CK(cudaSetDevice(ctx->device));
+  return ensure_ws(m, cfg->max_iters + 1);
+}
+
+PBS_EXPORT int pbs_solve(pbs_mat* m, int32_t method, const double* b, const double* x0,
+                         const pbs_config* cfg, double* x_out, double* hist_rel, uint8_t* hist_flags,
+                         double* hist_coef, pbs_result* res) {
+  int rc = solve_common(m, method, cfg);
+  if (rc) return rc;
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  cudaStream_t s = ctx->stream;
+  const size_t bytes = sizeof(double) * ws->n;
+  CK(cudaMemcpyAsync(ws->V.v[VB], b, bytes, cudaMemcpyHostToDevice, s));
+  if (x0)
+    CK(cudaMemcpyAsync(ws->V.v[VX], x0, bytes, cudaMemcpyHostToDevice, s));
+  else
+    CK(cudaMemsetAsync(ws->V.v[VX], 0, bytes, s));
+  rc = run_solve(m, method, cfg, res);
+  if (rc) return rc;
+  if (x_out) CK(cudaMemcpy(x_out, ws->V.v[VX], bytes, cudaMemcpyDeviceToHost));
+  return copy_history(m, res, hist_rel, hist_flags, hist_coef);
+}
+
+PBS_EXPORT int pbs_solve_dev(pbs_mat* m, int32_t method, const double* d_b, const double* d_x0,
+                             const pbs_config* cfg, double* d_x_out, double* hist_rel,
+                             uint8_t* hist_flags, double* hist_coef, pbs_result* res) {
+  int rc = solve_common(m, method, cfg);
+  if (rc) return rc;
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  cudaStream_t s = ctx->stream;
+  const size_t bytes = sizeof(double) * ws->n;
+  CK(cudaMemcpyAsync(ws->V.v[VB], d_b, bytes, cudaMemcpyDeviceToDevice, s));
+  if (d_x0)
+    CK(cudaMemcpyAsync(ws->V.v[VX], d_x0, bytes, cudaMemcpyDeviceToDevice, s));
+  else
+    CK(cudaMemsetAsync(ws->V.v[VX], 0, bytes, s));
+  rc = run_solve(m, method, cfg, res);
+  if (rc) return rc;
+  if (d_x_out) CK(cudaMemcpyAsync(d_x_out, ws->V.v[VX], bytes, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  return copy_history(m, res, hist_rel, hist_flags, hist_coef);
+}
+
+// single-iteration parity seam
+PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in, int32_t reduce_mode,
+                            int32_t plan_workers, double* outv) {
+  if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
+  pbs_ctx* ctx = m->ctx;
+  CK(cudaSetDevice(ctx->device));
+  int rc = ensure_ws(m, 4);
+  if (rc) return rc;
+  Workspace* ws = m->ws;
+  cudaStream_t s = ctx->stream;
+  Mode md;
+  md.plan = reduce_mode == PBS_REDUCE_PLAN;
+  md.store_temps = 1;
+  if (md.plan && (rc = ensure_plan(m, plan_workers))) return rc;
+  const int order[16] = {VX, VR, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL, VR0S, VB, VAS};
+  const size_t bytes = sizeof(double) * ws->n;
+  for (int k = 0; k < 16; ++k)
+    CK(cudaMemcpyAsync(ws->V.v[order[k]], d_state[k], bytes, cudaMemcpyDeviceToDevice, s));
+  const long long j = (long long)in[0];
+  SolverState h{};
+  h.tol = -1.0;  // never converge inside a single step
+  h.max_iters = j + 2;
+  h.record_history = 1;
+  h.alpha = in[1];
+  h.zeta = in[2];
+  h.f_prev = in[3];
+  h.r0_norm = in[4];
+  h.iter = j;
+  h.run_all = 1;
+  h.run_spine = 1;
+  h.status = -1;
+  h.failure_iter = -1;
+  h.nf_row = (unsigned long long)kNoError;
+  h.hist_rel = ws->hist_rel;
+  h.hist_flags = ws->hist_flags;
+  h.hist_coef = ws->hist_coef;
+  h.mirror = nullptr;
+  CK(cudaMemcpyAsync(ws->st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  Launcher L{ctx, m, s};
+  // the batch of iteration j over the given state, then the check
+  int np;
+  if (md.plan) {
+    np = plan_dots(L, ws, KD);
+  } else {
+    long long nblk = (ws->n + kThreads - 1) / kThreads;
+    np = grid_for(ctx, (const void*)dots9_tree_kernel, nblk);
+    dots9_tree_kernel<<<np, kThreads, 0, s>>>(ws->n, ws->V.v[VS], ws->V.v[VY], ws->V.v[VR],
+                                              ws->V.v[VR0S], ws->V.v[VT], ws->partials, ws->st);
+  }
+  finalize_kernel<<<1, 288, 0, s>>>(ws->st, ws->partials, np, md.plan, 0);
+  // iteration body without its trailing finalize
+  {
+    auto& V = ws->V.v;
+    EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
+    spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+    if (in[5] != 0.0) {
+      vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+      EpiStore eq{V[VQ], ws->st, PBS_TAG_AO, 0};
+      spmv_launch(L, V[VO], eq, 0, ws->n, KRS);
+      EpiStore ew{V[VW], ws->st, PBS_TAG_AU, 0};
+      spmv_launch(L, V[VU], ew, 0, ws->n, KRS);
+      vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+      EpiResid er{V[VB], V[VR], nullptr, ws->st};
+      spmv_launch(L, V[VX], er, 0, ws->n, KRS);
+      EpiStore el{V[VL], ws->st, PBS_TAG_AT, 0};
+      spmv_launch(L, V[VT], el, 0, ws->n, KRS);
+      EpiStore eg{V[VG], ws->st, PBS_TAG_AY, 0};
+      spmv_launch(L, V[VY], eg, 0, ws->n, KRS);
+      EpiDots es{V[VS], V[VY], V[VR], V[VR0S], V[VT], nullptr, ws->st, PBS_TAG_AR, 0};
+      spmv_launch(L, V[VR], es, 0, ws->n, KRS);
+    } else {
+      vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, 1);
+      EpiK3 e3{};
+      e3.as = V[VAS];
+      e3.l = V[VL];
+      e3.g = V[VG];
+      e3.s = V[VS];
+      e3.y = V[VY];
+      e3.r = V[VR];
+      e3.r0s = V[VR0S];
+      e3.t = V[VT];
+      e3.q_out = V[VQ];
+      e3.partials = nullptr;
+      e3.st = ws->st;
+      spmv_launch(L, V[VW], e3, 0, ws->n, KK3);
+    }
+  }
+  for (int k = 0; k < 16; ++k)
+    CK(cudaMemcpyAsync(d_state[k], ws->V.v[order[k]], bytes, cudaMemcpyDeviceToDevice, s));
+  SolverState out;
+  CK(cudaMemcpyAsync(&out, ws->st, sizeof(out), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  outv[0] = out.alpha;
+  outv[1] = out.beta;
+  outv[2] = out.zeta;
+  outv[3] = out.eta;
+  for (int k = 0; k < kNumDots; ++k) outv[4 + k] = out.dots[k];
+  outv[13] = out.status;
+  if (out.nf_row != (unsigned long long)kNoError) return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output");
+  return PBS_OK;
+}
+
+// ------------------------------------------------------- kernel backend table
+
+static int scratch(pbs_ctx* ctx, size_t bytes, void** p) {
+  if (bytes > ctx->scratch_bytes) {
+    cudaFree(ctx->scratch);
+    ctx->scratch = nullptr;
+    size_t cap = bytes < (1 << 20) ? (1 << 20) : bytes;
+    CK(cudaMalloc(&ctx->scratch, cap));
+    ctx->scratch_bytes = cap;
+  }
+  *p = ctx->scratch;
+  return PBS_OK;
+}
+
+static size_t al(size_t b) { return (b + 255) / 256 * 256; }
+
+PBS_EXPORT int pbs_k_spmv_range(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                                const int64_t* col_idx, const double* values, const double* x,
+                                double* out, int64_t lo, int64_t hi) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  if (lo < 0 || hi > n_rows || lo > hi) return set_err(ctx, PBS_ERR_INVALID, "row range out of bounds");
+  if (hi == lo) return PBS_OK;
+  CK(cudaSetDevice(ctx->device));
+  const long long nnz = row_ptr[n_rows];
+  size_t b_rp = al(sizeof(long long) * (n_rows + 1)), b_ci = al(sizeof(long long) * (nnz + 1)),
+         b_ci32 = al(sizeof(int) * (nnz + 1)), b_v = al(sizeof(double) * (nnz + 1)),
+         b_x = al(sizeof(double) * (n_cols + 1)), b_y = al(sizeof(double) * (n_rows + 1));
+  char* base;
+  int rc = scratch(ctx, b_rp + b_ci + b_ci32 + b_v + b_x + b_y + 256, (void**)&base);
+  if (rc) return rc;
+  long long* d_rp = (long long*)base;
+  long long* d_ci64 = (long long*)(base + b_rp);
+  int* d_ci = (int*)(base + b_rp + b_ci);
+  double* d_v = (double*)(base + b_rp + b_ci + b_ci32);
+  double* d_x = (double*)(base + b_rp + b_ci + b_ci32 + b_v);
+  double* d_y = (double*)(base + b_rp + b_ci + b_ci32 + b_v + b_x);
+  int* d_bad = (int*)(base + b_rp + b_ci + b_ci32 + b_v + b_x + b_y);
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(d_rp, row_ptr, sizeof(long long) * (n_rows + 1), cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    CK(cudaMemcpyAsync(d_ci64, col_idx, sizeof(long long) * nnz, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int), s));
+    cvt_i64_i32_kernel<<<ctx->sms, 256, 0, s>>>(d_ci64, d_ci, nnz, d_bad, n_cols > 0 ? n_cols : 1);
+  }
+  if (n_cols > 0) CK(cudaMemcpyAsync(d_x, x, sizeof(double) * n_cols, cudaMemcpyHostToDevice, s));
+  pbs_mat tmp;
+  tmp.ctx = ctx;
+  tmp.rp = d_rp;
+  tmp.ci = d_ci;
+  tmp.v = d_v;
+  tmp.n_rows = n_rows;
+  tmp.n_cols = n_cols;
+  tmp.nnz = nnz;
+  Launcher L{ctx, &tmp, s};
+  EpiStore e{d_y, nullptr, 0, 0};
+  spmv_launch(L, d_x, e, lo, hi, KS);
+  CK(cudaMemcpyAsync(out + lo, d_y + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  tmp.rp = nullptr;
+  tmp.ci = nullptr;
+  tmp.v = nullptr;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_k_dot_range(pbs_ctx* ctx, const double* x, const double* y, int64_t lo, int64_t hi,
+                               double* result) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  if (hi <= lo) {
+    *result = 0.0;
+    return PBS_OK;
+  }
+  CK(cudaSetDevice(ctx->device));
+  const long long n = hi - lo;
+  size_t b = al(sizeof(double) * n);
+  char* base;
+  int rc = scratch(ctx, 2 * b + 256, (void**)&base);
+  if (rc) return rc;
+  double* dx = (double*)base;
+  double* dy = (double*)(base + b);
+  double* dout = (double*)(base + 2 * b);
+  cudaStream_t s = ctx->stream;
+  CK(cudaMemcpyAsync(dx, x + lo, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dy, y + lo, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  long long nblk = (n + kThreads - 1) / kThreads;
+  int grid = grid_for(ctx, (const void*)dot_partial_kernel, nblk);
+  dot_partial_kernel<<<grid, kThreads, 0, s>>>(dx, dy, 0, n, ctx->partials);
+  dot_final_kernel<<<1, 32, 0, s>>>(ctx->partials, grid, dout);
+  CK(cudaMemcpyAsync(result, dout, sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_k_lincomb(pbs_ctx* ctx, int32_t kind, int64_t n, double* out, const double* sc,
+                             const double* a, const double* b, const double* c, const double* d) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  if (kind < 2 || kind > 7) return set_err(ctx, PBS_ERR_INVALID, "unknown lincomb kind");
+  if (n <= 0) return PBS_OK;
+  CK(cudaSetDevice(ctx->device));
+  size_t bb = al(sizeof(double) * n);
+  char* base;
+  int rc = scratch(ctx, 5 * bb, (void**)&base);
+  if (rc) return rc;
+  double* dv[5];
+  for (int k = 0; k < 5; ++k) dv[k] = (double*)(base + k * bb);
+  const double* in[4] = {a, b, c, d};
+  int nin = kind == 2 ? 2 : (kind == 4 ? 4 : 3);
+  cudaStream_t s = ctx->stream;
+  for (int k = 0; k < nin; ++k)
+    CK(cudaMemcpyAsync(dv[k], in[k], sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  long long nblk = (n + kThreads - 1) / kThreads;
+  int grid = grid_for(ctx, (const void*)lincomb_kernel, nblk);
+  lincomb_kernel<<<grid, kThreads, 0, s>>>(kind, n, dv[4], sc[0], sc[1], sc[2], sc[3], dv[0], dv[1],
+                                           dv[2], dv[3]);
+  CK(cudaMemcpyAsync(out, dv[4], sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_dot_batch_dev(pbs_ctx* ctx, int64_t n, const double* d_s, const double* d_y,
+                                 const double* d_r, const double* d_r0s, const double* d_t,
+                                 int32_t reduce_mode, int32_t plan_workers, double* out9) {
+  if (!ctx) return set_err(nullptr, PBS_ERR_INVALID, "ctx is NULL");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  int rc = reset_tmp_state(ctx);
+  if (rc) return rc;
+  int np;
+  int chain = reduce_mode == PBS_REDUCE_PLAN;
+  long long* d_bounds = nullptr;
+  if (chain) {
+    std::vector<long long> b;
+    np = plan_balanced(n, plan_workers < 1 ? 1 : plan_workers, b);
+    if (np > kMaxParts) return set_err(ctx, PBS_ERR_INVALID, "plan_workers too large");
+    CK(cudaMalloc(&d_bounds, sizeof(long long) * (np + 1)));
+    CK(cudaMemcpyAsync(d_bounds, b.data(), sizeof(long long) * (np + 1), cudaMemcpyHostToDevice, s));
+    dots9_plan_kernel<<<np, 32, 0, s>>>(d_bounds, d_s, d_y, d_r, d_r0s, d_t, ctx->partials, nullptr);
+  } else {
+    long long nblk = (n + kThreads - 1) / kThreads;
+    np = grid_for(ctx, (const void*)dots9_tree_kernel, nblk);
+    dots9_tree_kernel<<<np, kThreads, 0, s>>>(n, d_s, d_y, d_r, d_r0s, d_t, ctx->partials, nullptr);
+  }
+  // reuse the finalize reduction with a state whose run_all makes it reduce;
+  // tol < 0 and max_iters > 0 keep the check from stopping anything
+  SolverState h{};
+  h.tol = -1.0;
+  h.max_iters = 1LL << 60;
+  h.iter = 1;
+  h.run_all = 1;
+  h.run_spine = 1;
+  h.alpha = 1.0;
+  h.zeta = 1.0;
+  h.f_prev = 1.0;
+  h.r0_norm = 1.0;
+  h.nf_row = (unsigned long long)kNoError;
+  CK(cudaMemcpyAsync(ctx->tmp_state, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  finalize_kernel<<<1, 288, 0, s>>>(ctx->tmp_state, ctx->partials, np, chain, 0);
+  CK(cudaMemcpyAsync(out9, ctx->tmp_state->dots, sizeof(double) * kNumDots, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(d_bounds);
+  CK(cudaGetLastError());
+  return PBS_OK;
+}

@@ -1,0 +1,140 @@
+"""Operation counters of a device solve (drop-in subset of pipesafe.instrument).
+
+The reference ticks ``OpCounters`` inside its loop (instrument.py:49-87,
+solvers.py:613-733).  The device loop has no host in it, so the counters are
+synthesised afterwards from what the device reports (iterations, stop check,
+replacement schedule) with the reference's per-update tallies; the snapshot
+sequence is the one the reference would have produced, so
+``per_iteration_costs`` (instrument.py:118-171) applies unchanged.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+# (#Ax, #dots, #reductions) a steady-state iteration must cost (instrument.py:28-32)
+EXPECTED_PER_ITERATION = {
+    "ssbicgsafe2": (2, 9, 1),
+    "pbicgsafe": (2, 9, 1),
+}
+EXPECTED_WORKSPACE = {"ssbicgsafe2": 10, "pbicgsafe": 15, "pbicgsafe-rr": 15}
+
+# per-update (scalar mults, vector adds) exactly as the reference tallies them
+_PIPE_STEADY = (21, 22)   # solvers.py:679-724
+_PIPE_REPLACE = (12, 13)  # solvers.py:679-706 with the replacement branch
+_SS_ITER = (13, 14)       # solvers.py:563-580
+
+
+class CounterAssertionError(AssertionError):
+    """A steady-state per-iteration cost deviated from the cost model."""
+
+
+@dataclass
+class OpCounters:
+    n_spmv: int = 0
+    n_dots: int = 0
+    n_reductions: int = 0
+    n_scalar_mults: int = 0
+    n_vec_adds: int = 0
+    n_monitor_spmv: int = 0
+    n_workspace_vectors: int = 0
+    snapshots: list[tuple[int, int, int, int, int]] = field(default_factory=list)
+
+    def spmv(self, k: int = 1) -> None:
+        self.n_spmv += k
+
+    def batch(self, n_dots: int) -> None:
+        self.n_dots += n_dots
+        self.n_reductions += 1
+
+    def updates(self, mults: int, adds: int) -> None:
+        self.n_scalar_mults += mults
+        self.n_vec_adds += adds
+
+    def snapshot(self) -> None:
+        self.snapshots.append(
+            (self.n_spmv, self.n_dots, self.n_reductions, self.n_scalar_mults, self.n_vec_adds)
+        )
+
+    def as_dict(self) -> dict:
+        return {
+            "n_spmv": self.n_spmv, "n_dots": self.n_dots, "n_reductions": self.n_reductions,
+            "n_scalar_mults": self.n_scalar_mults, "n_vec_adds": self.n_vec_adds,
+            "n_monitor_spmv": self.n_monitor_spmv, "n_workspace_vectors": self.n_workspace_vectors,
+        }
+
+
+def synthesize(method: str, iterations: int, stopped_in_loop: bool, replaced_at) -> OpCounters:
+    """Counters the reference loop would have ticked for this outcome.
+
+    ``iterations`` completed iterations; ``stopped_in_loop`` when a loop check
+    (not the post-loop final record) ended the solve, in which case that
+    iteration's batch and spine SpMV were still counted; ``replaced_at`` the
+    set of completed iterations that ran residual replacement.
+    """
+    pipelined = method != "ssbicgsafe2"
+    c = OpCounters(n_workspace_vectors=16 if pipelined else 11)
+    c.spmv(2 if pipelined else 1)
+    c.updates(0, 1)
+    c.snapshot()
+    for i in range(iterations):
+        c.batch(5 if i == 0 else 9)
+        c.spmv()
+        if pipelined:
+            if i in replaced_at:
+                c.spmv(6)
+                c.updates(*_PIPE_REPLACE)
+            else:
+                c.spmv()
+                c.updates(*_PIPE_STEADY)
+        else:
+            c.spmv()
+            c.updates(*_SS_ITER)
+        c.snapshot()
+    if stopped_in_loop:
+        c.batch(5 if iterations == 0 else 9)
+        c.spmv()
+    return c
+
+
+@dataclass
+class CostRow:
+    method: str
+    ax_per_iter: int
+    dots_per_iter: int
+    reductions_per_iter: int
+    scalar_mults_per_iter: int
+    vec_adds_per_iter: int
+    workspace_vectors: int
+    tabulated_workspace_vectors: int | None
+    steady_iterations: int
+
+    def as_dict(self) -> dict:
+        return dict(self.__dict__)
+
+
+def per_iteration_costs(counters: OpCounters, method: str) -> CostRow:
+    """Steady-state per-iteration costs from snapshots (instrument.py:118-171)."""
+    snaps = counters.snapshots
+    if len(snaps) < 4:
+        raise ValueError("need at least three completed iterations to measure steady state")
+    deltas = [tuple(b[k] - a[k] for k in range(5)) for a, b in zip(snaps, snaps[1:])]
+    steady = deltas[1:]
+    if method in EXPECTED_PER_ITERATION:
+        if any(d != steady[0] for d in steady):
+            raise CounterAssertionError(f"{method}: steady-state deltas not constant: {sorted(set(steady))}")
+        row = steady[0]
+        for k, name in enumerate(("n_spmv", "n_dots", "n_reductions")):
+            if row[k] != EXPECTED_PER_ITERATION[method][k]:
+                raise CounterAssertionError(
+                    f"{method}: {name} per iteration = {row[k]}, cost model says "
+                    f"{EXPECTED_PER_ITERATION[method][k]}")
+        rep, count = row, len(steady)
+    else:
+        tally: dict[tuple, int] = {}
+        for d in steady:
+            tally[d] = tally.get(d, 0) + 1
+        rep = max(tally, key=tally.get)
+        count = tally[rep]
+    return CostRow(method, rep[0], rep[1], rep[2], rep[3], rep[4], counters.n_workspace_vectors,
+                   EXPECTED_WORKSPACE.get(method), count)

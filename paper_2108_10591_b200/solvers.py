@@ -1,0 +1,289 @@
+"""Drop-in solver entry points (pipesafe.solvers) running on the B200.
+
+Same names, arguments, validation and return types as the reference
+(solvers.py:44-114, 133-145, 742-803): ``solve(A, b, method, x0, config,
+engine, trace_hook) -> SolveOutcome``.  The whole iteration loop runs on the
+device (libpbsafe.so): SpMVs, fused updates, the packed 9-dot batch, the
+coefficient step, convergence/breakdown checks and the history all stay in
+HBM; the host sees the outcome once.  There is no CPU path: without the
+library or a B200 these functions raise.
+
+``engine`` accepts a :class:`DeviceEngine`, or a reference-style engine
+exposing ``.plan`` (a balanced PartitionPlan), in which case the dot batch
+follows that plan's chains and combine order and the solve is bitwise equal
+to the reference driven by the same engine (small systems; it is a parity
+mode, one thread per range).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+from enum import Enum
+
+import numpy as np
+
+from . import _lib
+from .coefficients import BREAKDOWN_QUANTITIES, CoefficientSet
+from .instrument import OpCounters, synthesize
+from .linalg import CsrMatrix, NonFiniteVectorError, check_finite
+from .operators import DeviceMatrix
+from .reduction import PartitionPlan
+
+
+class SolveStatus(Enum):
+    CONVERGED = "converged"
+    MAX_ITERS = "max_iters"
+    BREAKDOWN = "breakdown"
+    NON_FINITE = "non_finite"
+
+
+_STATUS = {0: SolveStatus.CONVERGED, 1: SolveStatus.MAX_ITERS, 2: SolveStatus.BREAKDOWN,
+           3: SolveStatus.NON_FINITE}
+
+
+@dataclass
+class SolverConfig:
+    """Knobs shared by every method (solvers.py:51-78)."""
+
+    tol: float = 1e-8
+    max_iters: int = 10_000
+    rr_epoch: int = 100
+    rr_cutoff: int | None = None
+    record_history: bool = True
+    monitor_every: int = 0
+    deterministic: bool = True
+
+    def __post_init__(self):
+        if not self.tol > 0.0:
+            raise ValueError("tol must be positive")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+        if self.rr_epoch < 1:
+            raise ValueError("rr_epoch must be >= 1")
+        if self.rr_cutoff is not None and not 0 <= self.rr_cutoff <= self.max_iters:
+            raise ValueError("rr_cutoff must lie in [0, max_iters]")
+        if self.monitor_every < 0:
+            raise ValueError("monitor_every must be >= 0")
+
+
+@dataclass
+class IterationRecord:
+    """State at the convergence check of one iteration (solvers.py:81-95)."""
+
+    iter: int
+    rel_res_recur: float
+    rel_res_true: float | None = None
+    replaced: bool = False
+    coefficients: CoefficientSet | None = None
+
+
+@dataclass
+class SolveOutcome:
+    """solvers.py:98-114, plus ``device``: timings/launch counts of the device run."""
+
+    status: SolveStatus
+    iterations: int
+    x: np.ndarray
+    history: list[IterationRecord]
+    counters: OpCounters
+    r0_norm: float
+    final_rel_res_recur: float
+    best_rel_res_recur: float
+    breakdown_quantity: str | None = None
+    failure_iter: int | None = None
+    drift: list = field(default_factory=list)
+    device: dict = field(default_factory=dict)
+
+    @property
+    def converged(self) -> bool:
+        return self.status is SolveStatus.CONVERGED
+
+
+def write_history_csv(path: str, history: list[IterationRecord]) -> None:
+    """``iter,rel_res_recur,rel_res_true,replaced`` rows, %.17g (solvers.py:117-130)."""
+    with open(path, "w", encoding="ascii") as fh:
+        fh.write("iter,rel_res_recur,rel_res_true,replaced\n")
+        for rec in history:
+            true_s = "" if rec.rel_res_true is None else format(rec.rel_res_true, ".17g")
+            fh.write(f"{rec.iter},{format(rec.rel_res_recur, '.17g')},{true_s},{int(rec.replaced)}\n")
+
+
+@dataclass
+class DeviceEngine:
+    """Where and how a solve runs (stands in for the reference's ReductionEngine).
+
+    reduce="tree": fixed-shape block-tree dot batch (deterministic, full speed).
+    reduce="plan": the reference's PartitionPlan.balanced(n, workers) chains
+    with a left-to-right combine — bitwise the reference's results.
+    """
+
+    device: int | None = None
+    reduce: str = "tree"
+    workers: int = 1
+    use_graphs: bool = True
+    timing: bool = False
+
+    def __post_init__(self):
+        if self.reduce not in ("tree", "plan"):
+            raise ValueError(f"unknown reduce mode {self.reduce!r}")
+        if self.workers < 1:
+            raise ValueError("workers must be >= 1")
+
+
+def _engine_params(engine, n: int) -> DeviceEngine:
+    if engine is None:
+        return DeviceEngine()
+    if isinstance(engine, DeviceEngine):
+        return engine
+    plan = getattr(engine, "plan", None)
+    if plan is not None and hasattr(plan, "ranges"):
+        mine = PartitionPlan(plan.n, tuple(tuple(r) for r in plan.ranges))
+        if mine.n != n:
+            raise ValueError(f"plan covers {mine.n} rows, system has {n}")
+        if not mine.is_balanced():
+            raise ValueError("only PartitionPlan.balanced plans are supported on the device")
+        return DeviceEngine(reduce="plan", workers=mine.worker_count)
+    raise TypeError(f"unsupported engine {type(engine).__name__}")
+
+
+def _prepare(A, b, x0):
+    """solvers.py:133-145: shape/finite validation, x0 copied."""
+    if A.n_rows != A.n_cols:
+        raise ValueError(f"solver needs a square operator, got {A.shape}")
+    b = np.asarray(b, dtype=np.float64)
+    if b.shape != (A.n_rows,):
+        raise ValueError(f"rhs has shape {b.shape}, matrix is {A.shape}")
+    check_finite(b, "right-hand side")
+    if x0 is None:
+        return np.ascontiguousarray(b), None
+    x = np.array(x0, dtype=np.float64)
+    if x.shape != (A.n_rows,):
+        raise ValueError(f"x0 has shape {x.shape}, matrix is {A.shape}")
+    check_finite(x, "initial guess")
+    return np.ascontiguousarray(b), np.ascontiguousarray(x)
+
+
+_TRACE_NAMES = ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l")
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
+    config = config or SolverConfig()
+    b, x0 = _prepare(A, b, x0)
+    n = A.n_rows
+    if config.monitor_every > 0:
+        raise NotImplementedError("monitor_every (DriftMonitor) is not available on the device path")
+    eng = _engine_params(engine, n)
+    own = not isinstance(A, DeviceMatrix)
+    dm = DeviceMatrix.from_csr(A, device=eng.device) if own else A
+    try:
+        cfg = _lib.Config()
+        cfg.tol = config.tol
+        cfg.max_iters = config.max_iters
+        cfg.rr_epoch = config.rr_epoch
+        cfg.rr_cutoff = -1 if config.rr_cutoff is None else config.rr_cutoff
+        cfg.record_history = 1 if config.record_history else 0
+        cfg.reduce_mode = _lib.REDUCE_PLAN if eng.reduce == "plan" else _lib.REDUCE_TREE
+        cfg.plan_workers = eng.workers
+        cfg.use_graphs = 1 if eng.use_graphs else 0
+        cfg.timing = 1 if eng.timing else 0
+        cb_keep = None
+        if trace_hook is not None:
+            def _cb(i, vecs, _user):
+                ws = {name: np.ctypeslib.as_array(vecs[k], shape=(n,))
+                      for k, name in enumerate(_TRACE_NAMES)}
+                trace_hook(int(i), ws)
+            cb_keep = _lib.TRACE_FN(_cb)
+            cfg.trace_fn = cb_keep
+        slots = config.max_iters + 1
+        x = np.empty(n)
+        rel = np.empty(slots)
+        flags = np.zeros(slots, dtype=np.uint8)
+        coef = np.empty((slots, 4))
+        res = _lib.Result()
+        rc = _lib.load().pbs_solve(dm.handle, _lib.METHOD_IDS[method], _ptr(b), _ptr(x0), C.byref(cfg),
+                                   _ptr(x), _ptr(rel), _ptr(flags), _ptr(coef), C.byref(res))
+    finally:
+        if own:
+            dm.free()
+    if rc == _lib.PBS_ERR_NONFINITE:
+        tag = _lib.SPMV_TAGS.get(res.nonfinite_tag, "?")
+        idx = int(res.nonfinite_index)
+        raise NonFiniteVectorError(f"matvec {tag!r} output row has non-finite entry at index {idx}", idx)
+    if rc == _lib.PBS_ERR_INVALID:
+        raise ValueError(_lib.last_error(dm.ctx.handle))
+    _lib.check(rc, dm.ctx.handle)
+
+    k = int(res.n_records)
+    history = []
+    for i in range(k):
+        rec = IterationRecord(i, float(rel[i]), replaced=bool(flags[i] & _lib.HIST_REPLACED))
+        if flags[i] & _lib.HIST_HAS_COEF:
+            rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
+                                              zeta=float(coef[i, 2]), eta=float(coef[i, 3]))
+        history.append(rec)
+    status = _STATUS[res.status]
+    iterations = int(res.iterations)
+    stopped_in_loop = iterations < config.max_iters  # a loop check ended it
+    replaced_at = set()
+    if method == "pbicgsafe-rr":
+        cutoff = config.rr_cutoff if config.rr_cutoff is not None else config.max_iters
+        replaced_at = {i for i in range(1, iterations) if i % config.rr_epoch == 0 and i < cutoff}
+    counters = synthesize(method, iterations, stopped_in_loop, replaced_at)
+    best = min((r.rel_res_recur for r in history), default=math.inf)
+    final = history[-1].rel_res_recur if history else math.inf
+    device = {
+        "device_ms": float(res.device_ms),
+        "kernel_launches": int(res.kernel_launches),
+        "n_spmv": int(res.n_spmv),
+        "kernel_ms": {name: float(res.kernel_ms[j]) for j, name in enumerate(_lib.KERNEL_KINDS)},
+        "kernel_count": {name: int(res.kernel_count[j]) for j, name in enumerate(_lib.KERNEL_KINDS)},
+        "reduce": eng.reduce,
+    }
+    return SolveOutcome(
+        status=status,
+        iterations=iterations,
+        x=x,
+        history=history,
+        counters=counters,
+        r0_norm=float(res.r0_norm),
+        final_rel_res_recur=final,
+        best_rel_res_recur=best,
+        breakdown_quantity=BREAKDOWN_QUANTITIES.get(int(res.breakdown)) if status is SolveStatus.BREAKDOWN else None,
+        failure_iter=None if res.failure_iter < 0 else int(res.failure_iter),
+        device=device,
+    )
+
+
+def solve_pbicgsafe(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Pipelined single-reduction solver (solvers.py:742-758) on the device."""
+    return _solve_device(A, b, "pbicgsafe", x0, config, engine, trace_hook)
+
+
+def solve_pbicgsafe_rr(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Pipelined solver with scheduled residual replacement (solvers.py:761-779)."""
+    return _solve_device(A, b, "pbicgsafe-rr", x0, config, engine, trace_hook)
+
+
+def solve_ssbicgsafe2(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Single-reduction comparator, batch after s = A r (solvers.py:485-592)."""
+    return _solve_device(A, b, "ssbicgsafe2", x0, config, engine, trace_hook)
+
+
+METHODS = {
+    "ssbicgsafe2": solve_ssbicgsafe2,
+    "pbicgsafe": solve_pbicgsafe,
+    "pbicgsafe-rr": solve_pbicgsafe_rr,
+}
+
+
+def solve(A, b, method: str = "pbicgsafe", x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Dispatch by name (solvers.py:791-803)."""
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}; choose from {sorted(METHODS)}")
+    return METHODS[method](A, b, x0=x0, config=config, engine=engine, trace_hook=trace_hook)
