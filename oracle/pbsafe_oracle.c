@@ -122,9 +122,31 @@ typedef struct {
   int64_t* bounds;
 } or_plan;
 
+/* Neumaier-compensated dot over [lo, hi): a near-exact reference order used
+ * only to bracket the reduction-order sensitivity of iteration counts (the
+ * reference has no such mode). */
+static double dot_compensated(const double* x, const double* y, int64_t lo, int64_t hi) {
+  double s = 0.0, c = 0.0;
+  for (int64_t k = lo; k < hi; ++k) {
+    double p = x[k] * y[k];
+    double t = s + p;
+    if (fabs(s) >= fabs(p)) c += (s - t) + p;
+    else c += (p - t) + s;
+    s = t;
+  }
+  return s + c;
+}
+
+static int g_compensated = 0;
+
 /* reduction.py:282-294: per range sequential partials, left-to-right combine */
 static void plan_batch(const or_plan* P, int npairs, const double* const* xs,
                        const double* const* ys, double* out) {
+  if (g_compensated) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int p = 0; p < npairs; ++p) out[p] = dot_compensated(xs[p], ys[p], 0, P->bounds[P->workers]);
+    return;
+  }
   int64_t W = P->workers;
   double* part = (double*)malloc(sizeof(double) * (size_t)(W * npairs));
 #pragma omp parallel for schedule(dynamic, 1) collapse(2)
@@ -328,12 +350,14 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   if (cfg->threads > 0) omp_set_num_threads(cfg->threads);
 #endif
   memset(res, 0, sizeof(*res));
+  g_compensated = cfg->workers < 0;  /* workers < 0: compensated dots (bracketing only) */
   res->failure_iter = -1;
   res->nonfinite_index = -1;
   mat_t A = {n, rp, ci, v, res};
   or_plan P;
-  P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(cfg->workers + 2));
-  P.workers = or_plan_balanced(n, cfg->workers, P.bounds);
+  int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;
+  P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(wk + 2));
+  P.workers = or_plan_balanced(n, wk, P.bounds);
   hist_t H = {hist_rel, hist_replaced, hist_coef, hist_has_coef, 0};
   const int pipelined = cfg->method != M_SSBICGSAFE2;
   const int replace_residuals = cfg->method == M_PBICGSAFE_RR;

@@ -58,7 +58,7 @@ struct SolverState {
   // non-finite SpMV output (NonFiniteVectorError): first row, tag
   unsigned long long nf_row;
   int nf_tag;
-  int pad;
+  unsigned int done_ctas;  // last-CTA ticket of the fused finalize (reset by the last CTA)
   // history (device arrays, max_iters+1 slots)
   double* hist_rel;
   unsigned char* hist_flags;
@@ -111,11 +111,21 @@ __device__ __forceinline__ double asdd(double base, double s, double a, double w
   return add(base, mul(s, sub(a, mul(w, b))));
 }
 
-// Block-level reduction of 9 per-thread partials into partials[blk*9 + j];
-// fixed shape (xor-butterfly in warps, then warps in index order), so the
-// result depends only on the data-to-thread mapping, never on timing.
+template <int NT, bool NAMED>
+__device__ __forceinline__ void block_bar() {
+  if (NAMED)
+    asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
+  else
+    __syncthreads();
+}
+
+// Block-level reduction of 9 per-thread partials into out[j] (threads 0..8
+// write, then __threadfence so a last-CTA reader sees them).  Fixed shape
+// (xor-butterfly in warps, then warps in index order): the result depends only
+// on the data-to-thread mapping, never on timing.
+template <int NT, bool NAMED>
 __device__ __forceinline__ void block_reduce9(double (&acc)[kNumDots], double* out) {
-  __shared__ double red[kThreads / 32][kNumDots];
+  __shared__ double red[NT / 32][kNumDots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < kNumDots; ++j) {
@@ -124,12 +134,13 @@ __device__ __forceinline__ void block_reduce9(double (&acc)[kNumDots], double* o
     for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
     if (lane == 0) red[warp][j] = v;
   }
-  __syncthreads();
+  block_bar<NT, NAMED>();
   if (threadIdx.x < kNumDots) {
     double v = red[0][threadIdx.x];
 #pragma unroll
-    for (int w = 1; w < kThreads / 32; ++w) v = add(v, red[w][threadIdx.x]);
+    for (int w = 1; w < NT / 32; ++w) v = add(v, red[w][threadIdx.x]);
     out[threadIdx.x] = v;
+    __threadfence();
   }
 }
 

@@ -129,11 +129,11 @@ struct Workspace {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   double* trace_host = nullptr;  // pinned staging for trace_hook (13 vectors)
   // graph cache: key -> exec
-  std::map<long long, cudaGraphExec_t> graphs;
+  std::map<long long, std::pair<cudaGraphExec_t, long long>> graphs;  // exec, kernels per launch
 };
 
 static void free_graphs(Workspace* ws) {
-  for (auto& kv : ws->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto& kv : ws->graphs) cudaGraphExecDestroy(kv.second.first);
   ws->graphs.clear();
 }
 
@@ -161,7 +161,7 @@ static int ensure_ws(pbs_mat* m, long long hist_slots) {
     ws = new Workspace();
     m->ws = ws;
     ws->n = m->n_rows;
-    ws->stride = ((size_t)(ws->n > 0 ? ws->n : 1) + 31) / 32 * 32;
+    ws->stride = ((size_t)ws->n + 2 + 31) / 32 * 32;  // +2: aligned bulk-copy over-read
     CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
     for (int k = 0; k < kNumVecs; ++k) ws->V.v[k] = ws->base + ws->stride * k;
     CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kNumDots));
@@ -269,6 +269,32 @@ void Launcher::trace_point() {
   trace_cfg->trace_fn(iter, ptrs, trace_cfg->trace_user);
 }
 
+// pipelined CSR engine: stage count from the opt-in shared-memory limit
+template <class Epi>
+static int pipe_config(pbs_ctx* ctx, int* stages, size_t* smem) {
+  using LY = StageLayout<Epi::kIn>;
+  const void* k = (const void*)csr_pipe_kernel<Epi>;
+  auto it = ctx->occ.find(k);
+  int st;
+  if (it == ctx->occ.end()) {
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+    const size_t budget = (size_t)optin - 1024 - 64;  // static smem of the kernel
+    st = (int)((budget - kPipeBarrierBytes) / LY::bytes);
+    if (st > kMaxStages) st = kMaxStages;
+    if (st < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
+    size_t bytes = kPipeBarrierBytes + (size_t)st * LY::bytes;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    ctx->occ[k] = st;
+  } else {
+    st = it->second;
+  }
+  *stages = st;
+  *smem = kPipeBarrierBytes + (size_t)st * LY::bytes;
+  return PBS_OK;
+}
+
 template <class Epi>
 static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long long hi, int kind) {
   pbs_mat* m = L.m;
@@ -276,8 +302,11 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   int grid;
   if (!m->stencil) {
     CsrView A{m->rp, m->ci, m->v, lo, hi};
-    grid = grid_for(L.ctx, (const void*)csr_spmv_kernel<Epi>, nblk);
-    csr_spmv_kernel<Epi><<<grid, kThreads, 0, L.s>>>(A, x, epi);
+    int stages;
+    size_t smem;
+    if (pipe_config<Epi>(L.ctx, &stages, &smem)) return 0;
+    grid = (int)(nblk < L.ctx->sms ? (nblk > 0 ? nblk : 1) : L.ctx->sms);
+    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, stages);
   } else {
     StencilView S = m->sv;
     S.row_lo = lo;
@@ -313,6 +342,78 @@ struct Mode {
   int store_temps = 0;
 };
 
+// ---- epilogue constructors (pointers into the workspace)
+
+static EpiStore epi_store(Workspace* ws, int out, int tag, int spine) {
+  EpiStore e{};
+  e.y = ws->V.v[out];
+  e.st = ws->st;
+  e.tag = tag;
+  e.spine = spine;
+  return e;
+}
+
+static EpiResid epi_resid(Workspace* ws, bool with_r0s) {
+  EpiResid e{};
+  e.r = ws->V.v[VR];
+  e.r0s = with_r0s ? ws->V.v[VR0S] : nullptr;
+  e.st = ws->st;
+  e.in[0] = ws->V.v[VB];
+  return e;
+}
+
+static DotSink sink_for(Workspace* ws, const Mode& md, int fuse, int replaced) {
+  DotSink k{};
+  k.partials = md.plan ? nullptr : ws->partials;
+  k.fuse = md.plan ? 0 : fuse;
+  k.replaced = replaced;
+  return k;
+}
+
+static EpiDots epi_dots(Workspace* ws, const Mode& md, int spine, int fuse, int replaced) {
+  EpiDots e{};
+  auto& V = ws->V.v;
+  e.s = V[VS];
+  e.st = ws->st;
+  e.tag = PBS_TAG_AR;
+  e.spine = spine;
+  e.sink = sink_for(ws, md, fuse, replaced);
+  e.in[0] = V[VY];
+  e.in[1] = V[VR];
+  e.in[2] = V[VR0S];
+  e.in[3] = V[VT];
+  return e;
+}
+
+static EpiK3 epi_k3(Workspace* ws, const Mode& md, int fuse) {
+  EpiK3 e{};
+  auto& V = ws->V.v;
+  e.l = V[VL];
+  e.g = V[VG];
+  e.s = V[VS];
+  e.q_out = md.store_temps ? V[VQ] : nullptr;
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, fuse, 0);
+  const int in[8] = {VAS, VL, VG, VS, VY, VR, VR0S, VT};
+  for (int k = 0; k < 8; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+static EpiSS3 epi_ss3(Workspace* ws) {
+  EpiSS3 e{};
+  auto& V = ws->V.v;
+  e.w = V[VW];
+  e.t = V[VT];
+  e.z = V[VZ];
+  e.y = V[VY];
+  e.x = V[VX];
+  e.r = V[VR];
+  e.st = ws->st;
+  const int in[8] = {VO, VS, VU, VP, VY, VZ, VX, VR};
+  for (int k = 0; k < 8; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
 // batch partials over (s, y, r, r0s, t) for PLAN mode (tree mode fuses them
 // into the producing SpMV); returns nparts
 static int plan_dots(Launcher& L, Workspace* ws, int kind) {
@@ -328,80 +429,63 @@ static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int repl
   L.done(KF);
 }
 
-// s = A r (+ dot partials); returns nparts
-static int spmv_s_dots(Launcher& L, Workspace* ws, const Mode& md, int kind, int spine) {
-  auto& V = ws->V.v;
-  EpiDots e{V[VS], V[VY], V[VR], V[VR0S], V[VT], md.plan ? nullptr : ws->partials, ws->st,
-            PBS_TAG_AR, spine};
-  int grid = spmv_launch(L, V[VR], e, 0, ws->n, kind);
-  if (md.plan) return plan_dots(L, ws, KD);
-  return grid;
+// s = A r (+ the batch of the next check); tree mode fuses the check into the
+// SpMV's last CTA, plan mode runs the plan chains + a separate finalize
+static void spmv_s_check(Launcher& L, Workspace* ws, const Mode& md, int kind, int spine, int replaced) {
+  spmv_launch(L, ws->V.v[VR], epi_dots(ws, md, spine, 1, replaced), 0, ws->n, kind);
+  if (md.plan) finalize(L, ws, plan_dots(L, ws, KD), 1, replaced);
 }
 
 // setup of the pipelined methods (solvers.py:612-631) + check 0
 static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
-  auto& V = ws->V.v;
-  EpiResid er{V[VB], V[VR], V[VR0S], ws->st};
-  spmv_launch(L, V[VX], er, 0, ws->n, KS);
-  int np = spmv_s_dots(L, ws, md, KS, 0);
-  finalize(L, ws, np, md.plan, 0);
+  spmv_launch(L, ws->V.v[VX], epi_resid(ws, true), 0, ws->n, KS);
+  spmv_s_check(L, ws, md, KS, 0, 0);
 }
 
-// one steady p-BiCGSafe iteration (K1 K2 K3 F)
+// one steady p-BiCGSafe iteration: K1, K2, K3 (+ fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
-  spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+  spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
   vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
-  EpiK3 e3{};
-  e3.as = V[VAS];
-  e3.l = V[VL];
-  e3.g = V[VG];
-  e3.s = V[VS];
-  e3.y = V[VY];
-  e3.r = V[VR];
-  e3.r0s = V[VR0S];
-  e3.t = V[VT];
-  e3.q_out = md.store_temps ? V[VQ] : nullptr;
-  e3.partials = md.plan ? nullptr : ws->partials;
-  e3.st = ws->st;
-  int np = spmv_launch(L, V[VW], e3, 0, ws->n, KK3);
-  if (md.plan) np = plan_dots(L, ws, KD);
-  L.trace_point();
-  finalize(L, ws, np, md.plan, 0);
+  const int grid = spmv_launch(L, V[VW], epi_k3(ws, md, L.trace_cfg ? 0 : 1), 0, ws->n, KK3);
+  if (md.plan) {
+    int np = plan_dots(L, ws, KD);
+    L.trace_point();
+    finalize(L, ws, np, 1, 0);
+  } else if (L.trace_cfg) {
+    L.trace_point();  // tracing: the check runs after the hook, as in the reference
+    finalize(L, ws, grid, 0, 0);
+  }
 }
 
 // residual-replacement iteration (solvers.py:676-713)
 static void iter_replace(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
-  spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+  spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
   vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-  EpiStore eq{V[VQ], ws->st, PBS_TAG_AO, 0};
-  spmv_launch(L, V[VO], eq, 0, ws->n, KRS);
-  EpiStore ew{V[VW], ws->st, PBS_TAG_AU, 0};
-  spmv_launch(L, V[VU], ew, 0, ws->n, KRS);
+  spmv_launch(L, V[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
+  spmv_launch(L, V[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
   vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-  EpiResid er{V[VB], V[VR], nullptr, ws->st};
-  spmv_launch(L, V[VX], er, 0, ws->n, KRS);
-  EpiStore el{V[VL], ws->st, PBS_TAG_AT, 0};
-  spmv_launch(L, V[VT], el, 0, ws->n, KRS);
-  EpiStore eg{V[VG], ws->st, PBS_TAG_AY, 0};
-  spmv_launch(L, V[VY], eg, 0, ws->n, KRS);
-  int np = spmv_s_dots(L, ws, md, KRS, 0);
-  L.trace_point();
-  finalize(L, ws, np, md.plan, 1);
+  spmv_launch(L, V[VX], epi_resid(ws, false), 0, ws->n, KRS);
+  spmv_launch(L, V[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
+  spmv_launch(L, V[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
+  if (L.trace_cfg) {
+    int np = spmv_launch(L, V[VR], epi_dots(ws, md, 0, 0, 1), 0, ws->n, KRS);
+    if (md.plan) np = plan_dots(L, ws, KD);
+    L.trace_point();
+    finalize(L, ws, np, md.plan, 1);
+  } else {
+    spmv_s_check(L, ws, md, KRS, 0, 1);
+  }
 }
 
-// one ssBiCGSafe2 iteration (solvers.py:528-587): s = A r + batch, check,
+// one ssBiCGSafe2 iteration (solvers.py:528-587): s = A r + batch + check,
 // p o u, w = A u + t z y x r
 static void iter_ss(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  int np = spmv_s_dots(L, ws, md, KK1, 1);
-  finalize(L, ws, np, md.plan, 0);
+  spmv_s_check(L, ws, md, KK1, 1, 0);
   vec_launch(L, pou_kernel, ws->n, KK2, ws->V, ws->n, ws->st);
-  EpiSS3 e{V[VW], V[VO], V[VS], V[VU], V[VP], V[VT], V[VZ], V[VY], V[VX], V[VR], ws->st};
-  spmv_launch(L, V[VU], e, 0, ws->n, KK3);
+  spmv_launch(L, V[VU], epi_ss3(ws), 0, ws->n, KK3);
   L.trace_point();
 }
 
@@ -424,11 +508,12 @@ static void final_ss(Launcher& L, Workspace* ws, const Mode& md) {
 typedef void (*IterFn)(Launcher&, Workspace*, const Mode&);
 
 static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const Mode& md,
-                     cudaGraphExec_t* out) {
+                     cudaGraphExec_t* out, long long* nkernels) {
   Workspace* ws = m->ws;
   auto it = ws->graphs.find(key);
   if (it != ws->graphs.end()) {
-    *out = it->second;
+    *out = it->second.first;
+    *nkernels = it->second.second;
     return PBS_OK;
   }
   cudaGraph_t g;
@@ -441,8 +526,9 @@ static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const M
   e = cudaGraphInstantiate(&ge, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
-  ws->graphs[key] = ge;
+  ws->graphs[key] = {ge, L.launches};
   *out = ge;
+  *nkernels = L.launches;
   return PBS_OK;
 }
 
@@ -517,8 +603,7 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   if (pipelined) {
     setup_pipelined(L, ws, md);
   } else {
-    EpiResid er{ws->V.v[VB], ws->V.v[VR], ws->V.v[VR0S], ws->st};
-    spmv_launch(L, ws->V.v[VX], er, 0, n, KS);
+    spmv_launch(L, ws->V.v[VX], epi_resid(ws, true), 0, n, KS);
   }
   const long long lookahead = 6;
   long long launched_graph_kernels = 0;
@@ -540,10 +625,11 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
       if (graphs) {
         long long key = key_base + (!pipelined ? 2 : (replace ? 1 : 0));
         cudaGraphExec_t ge;
-        int rc = get_graph(ctx, m, key, fn, md, &ge);
+        long long nk = 0;
+        int rc = get_graph(ctx, m, key, fn, md, &ge, &nk);
         if (rc) return rc;
         CK(cudaGraphLaunch(ge, s));
-        launched_graph_kernels += !pipelined ? 4 + md.plan : (replace ? 10 : 4) + md.plan;
+        launched_graph_kernels += nk;
       } else {
         L.iter = j;
         fn(L, ws, md);
@@ -702,9 +788,13 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
   m->n_cols = n_cols;
   m->nnz = nnz;
   cudaStream_t s = ctx->stream;
-  CK(cudaMalloc(&m->rp, sizeof(long long) * (n_rows + 1)));
-  CK(cudaMalloc(&m->ci, sizeof(int) * (nnz > 0 ? nnz : 1)));
-  CK(cudaMalloc(&m->v, sizeof(double) * (nnz > 0 ? nnz : 1)));
+  // padding: the pipelined SpMV bulk-copies 16-byte-aligned windows
+  CK(cudaMalloc(&m->rp, sizeof(long long) * (n_rows + 4)));
+  CK(cudaMalloc(&m->ci, sizeof(int) * (nnz + 8)));
+  CK(cudaMalloc(&m->v, sizeof(double) * (nnz + 4)));
+  CK(cudaMemsetAsync(m->rp + n_rows + 1, 0, sizeof(long long) * 3, s));
+  CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
+  CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
   CK(cudaMemcpyAsync(m->rp, row_ptr, sizeof(long long) * (n_rows + 1), cudaMemcpyHostToDevice, s));
   if (nnz > 0) {
     CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
@@ -828,7 +918,10 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
   int rc = reset_tmp_state(ctx);
   if (rc) return rc;
   Launcher L{ctx, m, ctx->stream};
-  EpiStore e{d_y, ctx->tmp_state, PBS_TAG_AX, 0};
+  EpiStore e{};
+  e.y = d_y;
+  e.st = ctx->tmp_state;
+  e.tag = PBS_TAG_AX;
   spmv_launch(L, d_x, e, 0, m->n_rows, KS);
   unsigned long long row = 0;
   CK(cudaMemcpyAsync(&row, &ctx->tmp_state->nf_row, sizeof(row), cudaMemcpyDeviceToHost, ctx->stream));
@@ -939,41 +1032,26 @@ PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in
                                               ws->V.v[VR0S], ws->V.v[VT], ws->partials, ws->st);
   }
   finalize_kernel<<<1, 288, 0, s>>>(ws->st, ws->partials, np, md.plan, 0);
-  // iteration body without its trailing finalize
+  // iteration body without its trailing check
   {
     auto& V = ws->V.v;
-    EpiStore e1{V[VAS], ws->st, PBS_TAG_AS, 1};
-    spmv_launch(L, V[VS], e1, 0, ws->n, KK1);
+    Mode nm = md;  // the step's batch comes first; the body's partials are not needed
+    spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
     if (in[5] != 0.0) {
       vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-      EpiStore eq{V[VQ], ws->st, PBS_TAG_AO, 0};
-      spmv_launch(L, V[VO], eq, 0, ws->n, KRS);
-      EpiStore ew{V[VW], ws->st, PBS_TAG_AU, 0};
-      spmv_launch(L, V[VU], ew, 0, ws->n, KRS);
+      spmv_launch(L, V[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
+      spmv_launch(L, V[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
       vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-      EpiResid er{V[VB], V[VR], nullptr, ws->st};
-      spmv_launch(L, V[VX], er, 0, ws->n, KRS);
-      EpiStore el{V[VL], ws->st, PBS_TAG_AT, 0};
-      spmv_launch(L, V[VT], el, 0, ws->n, KRS);
-      EpiStore eg{V[VG], ws->st, PBS_TAG_AY, 0};
-      spmv_launch(L, V[VY], eg, 0, ws->n, KRS);
-      EpiDots es{V[VS], V[VY], V[VR], V[VR0S], V[VT], nullptr, ws->st, PBS_TAG_AR, 0};
-      spmv_launch(L, V[VR], es, 0, ws->n, KRS);
+      spmv_launch(L, V[VX], epi_resid(ws, false), 0, ws->n, KRS);
+      spmv_launch(L, V[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
+      spmv_launch(L, V[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
+      nm.plan = 1;  // no partials
+      spmv_launch(L, V[VR], epi_dots(ws, nm, 0, 0, 0), 0, ws->n, KRS);
     } else {
       vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, 1);
-      EpiK3 e3{};
-      e3.as = V[VAS];
-      e3.l = V[VL];
-      e3.g = V[VG];
-      e3.s = V[VS];
-      e3.y = V[VY];
-      e3.r = V[VR];
-      e3.r0s = V[VR0S];
-      e3.t = V[VT];
-      e3.q_out = V[VQ];
-      e3.partials = nullptr;
-      e3.st = ws->st;
-      spmv_launch(L, V[VW], e3, 0, ws->n, KK3);
+      nm.plan = 1;
+      nm.store_temps = 1;
+      spmv_launch(L, V[VW], epi_k3(ws, nm, 0), 0, ws->n, KK3);
     }
   }
   for (int k = 0; k < 16; ++k)
@@ -1016,8 +1094,8 @@ PBS_EXPORT int pbs_k_spmv_range(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, co
   if (hi == lo) return PBS_OK;
   CK(cudaSetDevice(ctx->device));
   const long long nnz = row_ptr[n_rows];
-  size_t b_rp = al(sizeof(long long) * (n_rows + 1)), b_ci = al(sizeof(long long) * (nnz + 1)),
-         b_ci32 = al(sizeof(int) * (nnz + 1)), b_v = al(sizeof(double) * (nnz + 1)),
+  size_t b_rp = al(sizeof(long long) * (n_rows + 4)), b_ci = al(sizeof(long long) * (nnz + 1)),
+         b_ci32 = al(sizeof(int) * (nnz + 8)), b_v = al(sizeof(double) * (nnz + 4)),
          b_x = al(sizeof(double) * (n_cols + 1)), b_y = al(sizeof(double) * (n_rows + 1));
   char* base;
   int rc = scratch(ctx, b_rp + b_ci + b_ci32 + b_v + b_x + b_y + 256, (void**)&base);
@@ -1047,7 +1125,8 @@ PBS_EXPORT int pbs_k_spmv_range(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, co
   tmp.n_cols = n_cols;
   tmp.nnz = nnz;
   Launcher L{ctx, &tmp, s};
-  EpiStore e{d_y, nullptr, 0, 0};
+  EpiStore e{};
+  e.y = d_y;
   spmv_launch(L, d_x, e, lo, hi, KS);
   CK(cudaMemcpyAsync(out + lo, d_y + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

@@ -1,29 +1,34 @@
 // spmv.cuh — SpMV engines with fused epilogues (sm_100a).
 //
-// Two engines feed one epilogue interface (Epi::row(i, y) per output row,
-// Epi::finish() once per thread at the end):
+// Both engines hand each output row to an epilogue: Epi::row(i, y, in[])
+// where in[] holds the row's values of the epilogue's kIn input vectors.
 //
-//  * csr_spmv: a CTA owns 256 consecutive rows at a time (grid-stride over
-//    row blocks, grid = SMs x resident CTAs).  The row block's nonzeros are
-//    streamed through shared memory in 2048-product chunks: coalesced,
-//    evict-first loads of values / int32 col_idx, an L1-cached gather of x,
-//    one rounded product per nonzero.  Each thread then sums its own row from
-//    shared memory in ascending column order (kernels.py:95-100 order), so
-//    the result is bitwise the reference's, while HBM sees each matrix byte
-//    once and every lane does useful loads.
-//  * stencil_spmv: matrix-free constant-coefficient stencil, one thread per
-//    row, neighbours visited in ascending flattened offset (= CSR column
-//    order), out-of-grid neighbours skipped (Dirichlet elimination) — bitwise
+//  * csr_pipe_kernel — CSR, warp-specialised and TMA-fed.  One CTA per SM:
+//    a producer warp streams each 256-row block's slice of row_ptr, its
+//    contiguous nonzero range of values / int32 col_idx (in <=2048-nonzero
+//    chunks) and the epilogue's input-vector segments into a ring of shared
+//    memory stages with 1-D bulk async copies (cp.async.bulk, completion on
+//    mbarriers); eight consumer warps own one row each per block, gather x
+//    (L1-cached) and accumulate the row sequentially in ascending column order
+//    (kernels.py:95-100), so the product is bitwise the reference's while HBM
+//    sees every matrix byte once with the copy engine keeping it busy.
+//  * stencil_spmv_kernel — matrix-free constant-coefficient stencil, one
+//    thread per row, neighbours in ascending flattened offset (= CSR column
+//    order), out-of-grid neighbours skipped (Dirichlet elimination): bitwise
 //    equal to the CSR of the same stencil.
 //
 // Epilogues (SURVEY §8(d) kernel plan):
 //   EpiStore  y = A x                          (K1: As = A s; rr products)
 //   EpiResid  r = b - A x  (+ r0s = r)         (setup; rr "r = b - A x")
-//   EpiK3     Aw -> l, g, s updates + next 9 dot partials (solvers.py:717-723, 467-482)
+//   EpiK3     Aw -> l, g, s + next 9 dot partials (solvers.py:717-723, 467-482)
 //   EpiDots   s = A r + 9 dot partials          (setup s0 = A r0; rr s = A r)
-//   EpiSS3    w = A u -> t, z, y, x, r updates  (ssBiCGSafe2, solvers.py:569-580)
+//   EpiSS3    w = A u -> t, z, y, x, r          (ssBiCGSafe2, solvers.py:569-580)
+// Epilogues with dot partials finish with a fixed-shape block reduction and,
+// when `fuse` is set, the last CTA to finish runs the coefficient check.
 #pragma once
 #include "common.cuh"
+#include "finalize.cuh"
+#include "ptx.cuh"
 
 namespace pbs {
 
@@ -37,41 +42,13 @@ struct CsrView {
 struct StencilView {
   long long n, k, k2;
   int dim, npts;
-  int off[kMaxStencil][3];     // (dz,)dy,dx per point, padded to 3 axes from the left
-  long long foff[kMaxStencil]; // flattened offset
+  int off[kMaxStencil][3];      // (dz,)dy,dx per point, padded to 3 axes from the left
+  long long foff[kMaxStencil];  // flattened offset
   double coef[kMaxStencil];
   long long row_lo, row_hi;
 };
 
 // ---------------------------------------------------------------- epilogues
-
-struct EpiStore {
-  double* y;
-  SolverState* st;
-  int tag;
-  int spine;  // gate on run_spine instead of run_all
-  __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
-  __device__ void row(long long i, double v) {
-    y[i] = v;
-    if (tag && !isfinite(v)) report_nonfinite(st, tag, i);
-  }
-  __device__ void finish() {}
-};
-
-struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
-  const double* b;
-  double* r;
-  double* r0s;  // nullable: also r0s = r (solvers.py:617)
-  SolverState* st;
-  __device__ bool active() const { return gate_all(st); }
-  __device__ void row(long long i, double ax) {
-    if (!isfinite(ax)) report_nonfinite(st, PBS_TAG_AX, i);
-    double rv = lc2(1.0, b[i], -1.0, ax);
-    r[i] = rv;
-    if (r0s) r0s[i] = rv;
-  }
-  __device__ void finish() {}
-};
 
 struct Dots9 {
   double acc[kNumDots];
@@ -93,33 +70,81 @@ struct Dots9 {
   }
 };
 
-struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
-  double* s;
-  const double *y, *r, *r0s, *t;
-  double* partials;  // nullable: PBS_REDUCE_PLAN computes the batch separately
-  SolverState* st;
-  int tag;
-  int spine;
-  Dots9 d;
-  __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
-  __device__ void init() { d.zero(); }
-  __device__ void row(long long i, double v) {
-    s[i] = v;
-    if (!isfinite(v)) report_nonfinite(st, tag, i);
-    if (partials) d.add_row(v, y[i], r[i], r0s[i], t[i]);
-  }
-  __device__ void finish() {
-    if (partials) block_reduce9(d.acc, partials + (size_t)blockIdx.x * kNumDots);
+// dot-partial sink shared by the epilogues that carry the batch
+struct DotSink {
+  double* partials;  // nullptr: no partials (PBS_REDUCE_PLAN computes them separately)
+  int fuse;          // last CTA runs finalize_tail (check + coefficients)
+  int replaced;      // the record this check writes follows a replacement
+  template <int NT, bool NAMED>
+  __device__ void finish(Dots9& d, SolverState* st) {
+    if (!partials) return;
+    block_reduce9<NT, NAMED>(d.acc, partials + (size_t)blockIdx.x * kNumDots);
+    if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced);
   }
 };
 
-struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
-  const double* as;
-  double *l, *g, *s;
-  const double *y, *r, *r0s, *t;
-  double* q_out;     // nullable (single-step parity: expose q)
-  double* partials;  // nullable (PBS_REDUCE_PLAN)
+struct EpiStore {
+  static constexpr int kIn = 0;
+  double* y;
   SolverState* st;
+  int tag;
+  int spine;  // gate on run_spine instead of run_all
+  const double* in[1];
+  __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
+  __device__ void init() {}
+  __device__ void row(long long i, double v, const double*) {
+    y[i] = v;
+    if (tag && !isfinite(v)) report_nonfinite(st, tag, i);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() {}
+};
+
+struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
+  static constexpr int kIn = 1;
+  double* r;
+  double* r0s;  // nullable: also r0s = r (solvers.py:617)
+  SolverState* st;
+  const double* in[kIn];  // b
+  __device__ bool active() const { return gate_all(st); }
+  __device__ void init() {}
+  __device__ void row(long long i, double ax, const double* v) {
+    if (!isfinite(ax)) report_nonfinite(st, PBS_TAG_AX, i);
+    const double rv = lc2(1.0, v[0], -1.0, ax);
+    r[i] = rv;
+    if (r0s) r0s[i] = rv;
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() {}
+};
+
+struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
+  static constexpr int kIn = 4;
+  double* s;
+  SolverState* st;
+  int tag;
+  int spine;
+  DotSink sink;
+  const double* in[kIn];  // y r r0s t
+  Dots9 d;
+  __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
+  __device__ void init() { d.zero(); }
+  __device__ void row(long long i, double v, const double* in4) {
+    s[i] = v;
+    if (!isfinite(v)) report_nonfinite(st, tag, i);
+    if (sink.partials) d.add_row(v, in4[0], in4[1], in4[2], in4[3]);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+
+struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
+  static constexpr int kIn = 8;
+  double *l, *g, *s;
+  double* q_out;  // nullable (single-step parity: expose q)
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // As l g s y r r0s t
   double alpha, beta, zeta, eta;
   Dots9 d;
   __device__ bool active() const { return gate_all(st); }
@@ -130,29 +155,28 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
     zeta = st->zeta;
     eta = st->eta;
   }
-  __device__ void row(long long i, double aw) {
+  __device__ void row(long long i, double aw, const double* v) {
     if (!isfinite(aw)) report_nonfinite(st, PBS_TAG_AW, i);
-    const double asv = as[i];
-    const double q = lc2(1.0, asv, beta, l[i]);                  // q = As + beta*l
-    const double lv = lc2(1.0, q, -1.0, aw);                     // l = q - A w
-    const double gv = lc3(zeta, asv, eta, g[i], -alpha, aw);     // g = zeta As + eta g - alpha Aw
-    const double sv = lc3(1.0, s[i], -alpha, q, -1.0, gv);       // s = s - alpha q - g
+    const double asv = v[0];
+    const double q = lc2(1.0, asv, beta, v[1]);               // q = As + beta*l
+    const double lv = lc2(1.0, q, -1.0, aw);                  // l = q - A w
+    const double gv = lc3(zeta, asv, eta, v[2], -alpha, aw);  // g = zeta As + eta g - alpha Aw
+    const double sv = lc3(1.0, v[3], -alpha, q, -1.0, gv);    // s = s - alpha q - g
     l[i] = lv;
     g[i] = gv;
     s[i] = sv;
     if (q_out) q_out[i] = q;
-    if (partials) d.add_row(sv, y[i], r[i], r0s[i], t[i]);
+    if (sink.partials) d.add_row(sv, v[4], v[5], v[6], v[7]);
   }
-  __device__ void finish() {
-    if (partials) block_reduce9(d.acc, partials + (size_t)blockIdx.x * kNumDots);
-  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
 };
 
 struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:569-580)
-  double* w;
-  const double *o, *s, *u, *p;
-  double *t, *z, *y, *x, *r;
+  static constexpr int kIn = 8;
+  double *w, *t, *z, *y, *x, *r;
   SolverState* st;
+  const double* in[kIn];  // o s u p y z x r
   double alpha, zeta, eta;
   __device__ bool active() const { return gate_all(st); }
   __device__ void init() {
@@ -160,88 +184,195 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
     zeta = st->zeta;
     eta = st->eta;
   }
-  __device__ void row(long long i, double wv) {
+  __device__ void row(long long i, double wv, const double* v) {
     if (!isfinite(wv)) report_nonfinite(st, PBS_TAG_AU, i);
-    const double ov = o[i];
-    const double yv = lc3(zeta, s[i], eta, y[i], -alpha, wv);
-    const double zv = lc3(zeta, r[i], eta, z[i], -alpha, u[i]);
+    const double ov = v[0];
+    const double yv = lc3(zeta, v[1], eta, v[4], -alpha, wv);  // y = zeta s + eta y - alpha w
+    const double zv = lc3(zeta, v[7], eta, v[5], -alpha, v[2]);  // z = zeta r + eta z - alpha u
     w[i] = wv;
-    t[i] = lc2(1.0, ov, -1.0, wv);
+    t[i] = lc2(1.0, ov, -1.0, wv);                              // t = o - w
     z[i] = zv;
     y[i] = yv;
-    x[i] = lc3(1.0, x[i], alpha, p[i], 1.0, zv);
-    r[i] = lc3(1.0, r[i], -alpha, ov, -1.0, yv);
+    x[i] = lc3(1.0, v[6], alpha, v[3], 1.0, zv);                // x = x + alpha p + z
+    r[i] = lc3(1.0, v[7], -alpha, ov, -1.0, yv);                // r = r - alpha o - y
   }
+  template <int NT, bool NAMED>
   __device__ void finish() {}
 };
 
-template <class E>
-__device__ __forceinline__ auto epi_init(E& e, int) -> decltype(e.init(), void()) { e.init(); }
-template <class E>
-__device__ __forceinline__ void epi_init(E&, long) {}
+// --------------------------------------------------- CSR pipelined engine
 
-// ------------------------------------------------------------------- engines
+constexpr int kPipeRows = 256;        // rows per block = consumer threads
+constexpr int kPipeChunk = 2048;      // nonzeros per stage
+constexpr int kConsumerWarps = kPipeRows / 32;
+constexpr int kPipeThreads = kPipeRows + 32;  // + one producer warp
+constexpr int kMaxStages = 8;
+
+struct PipeHdr {
+  long long r0, c0, c1;
+  int nr, first, last, dv, dci, dr;  // dv/dci/dr: 16-byte alignment shifts of v, ci, row slices
+};
+
+__host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
+
+template <int KIN>
+struct StageLayout {
+  static constexpr size_t hdr = 0;
+  static constexpr size_t rp = 128;
+  static constexpr size_t v = rp + align128(sizeof(long long) * (kPipeRows + 2));
+  static constexpr size_t ci = v + align128(sizeof(double) * (kPipeChunk + 2));
+  static constexpr size_t ein = ci + align128(sizeof(int) * (kPipeChunk + 4));
+  static constexpr size_t ein_stride = kPipeRows + 2;  // doubles per staged input segment
+  static constexpr size_t bytes = ein + align128(sizeof(double) * ein_stride * (KIN > 0 ? KIN : 1));
+};
+constexpr size_t kPipeBarrierBytes = 256;
 
 template <class Epi>
-__global__ void __launch_bounds__(kThreads) csr_spmv_kernel(CsrView A, const double* __restrict__ x,
-                                                            Epi epi) {
-  if (!epi.active()) return;
-  Epi e = epi;
-  epi_init(e, 0);
-  __shared__ double prod[kChunk];
-  __shared__ long long srp[kThreads + 1];
-  constexpr int U = kChunk / kThreads;
-  const int t = threadIdx.x;
-  const long long nrows = A.row_hi - A.row_lo;
-  const long long nblk = (nrows + kThreads - 1) / kThreads;
-  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    const long long r0 = A.row_lo + blk * kThreads;
-    const int nr = (int)min((long long)kThreads, A.row_hi - r0);
-    for (int i = t; i <= nr; i += kThreads) srp[i] = __ldg(A.rp + r0 + i);
-    __syncthreads();
-    const long long base = srp[0], end = srp[nr];
-    long long my_s = 0, my_e = 0;
-    if (t < nr) {
-      my_s = srp[t];
-      my_e = srp[t + 1];
+__global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
+                                                                   Epi epi, int stages) {
+  __shared__ int go;
+  if (threadIdx.x == 0) go = epi.active();  // one gate decision per CTA
+  __syncthreads();
+  if (!go) return;
+  using L = StageLayout<Epi::kIn>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + kMaxStages;
+  unsigned char* stage0 = smem + kPipeBarrierBytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
     }
-    double acc = 0.0;
-    for (long long c0 = base; c0 < end; c0 += kChunk) {
-      const int len = (int)min((long long)kChunk, end - c0);
-      double vv[U];
-      int cc[U];
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long nrows = A.row_hi - A.row_lo;
+  const long long nblk = (nrows + kPipeRows - 1) / kPipeRows;
+
+  if (warp == kConsumerWarps) {
+    // ----------------------------------------------------------- producer
+    if (lane != 0) return;
+    int s = 0;
+    uint32_t ph = 0;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+      const long long r0 = A.row_lo + blk * kPipeRows;
+      const long long r0a = r0 & ~1LL;
+      const int nr = (int)min((long long)kPipeRows, A.row_hi - r0);
+      const int dr = (int)(r0 - r0a);
+      const long long base = __ldg(A.rp + r0), end = __ldg(A.rp + r0 + nr);
+      const long long nch = end > base ? (end - base + kPipeChunk - 1) / kPipeChunk : 1;
+      for (long long c = 0; c < nch; ++c) {
+        mbar_wait(&empty[s], ph ^ 1);
+        unsigned char* st = stage0 + (size_t)s * L::bytes;
+        const long long c0 = base + c * kPipeChunk;
+        const long long c1 = min(end, c0 + kPipeChunk);
+        const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
+        const long long c0b = c0 & ~3LL, c1b = (c1 + 3) & ~3LL;
+        PipeHdr* h = reinterpret_cast<PipeHdr*>(st + L::hdr);
+        h->r0 = r0;
+        h->c0 = c0;
+        h->c1 = c1;
+        h->nr = nr;
+        h->first = c == 0;
+        h->last = c == nch - 1;
+        h->dv = (int)(c0 - c0a);
+        h->dci = (int)(c0 - c0b);
+        h->dr = dr;
+        const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
+        const uint32_t bc = (uint32_t)((c1b - c0b) * sizeof(int));
+        uint32_t total = bv + bc;
+        const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
+        const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
+        if (c == 0) total += brp + Epi::kIn * bin;
+        mbar_arrive_expect_tx(&full[s], total);
+        if (bv) bulk_g2s(st + L::v, A.v + c0a, bv, &full[s]);
+        if (bc) bulk_g2s(st + L::ci, A.ci + c0b, bc, &full[s]);
+        if (c == 0) {
+          bulk_g2s(st + L::rp, A.rp + r0a, brp, &full[s]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = t + u * kThreads;
-        if (k < len) {
-          vv[u] = __ldcs(A.v + c0 + k);
-          cc[u] = __ldcs(A.ci + c0 + k);
+          for (int e = 0; e < Epi::kIn; ++e)
+            bulk_g2s(st + L::ein + (size_t)e * L::ein_stride * sizeof(double), epi.in[e] + r0a, bin, &full[s]);
+        }
+        if (++s == stages) {
+          s = 0;
+          ph ^= 1;
         }
       }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int k = t + u * kThreads;
-        if (k < len) prod[k] = mul(vv[u], __ldg(x + cc[u]));
-      }
-      __syncthreads();
-      if (t < nr) {
-        const long long lo = max(my_s, c0), hi = min(my_e, c0 + len);
-        for (long long k = lo; k < hi; ++k) acc = add(acc, prod[k - c0]);
-      }
-      __syncthreads();
     }
-    if (t < nr) e.row(r0 + t, acc);
+    return;
   }
-  e.finish();
+
+  // ------------------------------------------------------------- consumers
+  Epi e = epi;
+  e.init();
+  const int t = threadIdx.x;
+  int s = 0;
+  uint32_t ph = 0;
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    double acc = 0.0;
+    long long my_s = 0, my_e = 0, r0 = 0;
+    int nr = 0;
+    double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+    for (;;) {
+      mbar_wait(&full[s], ph);
+      const unsigned char* st = stage0 + (size_t)s * L::bytes;
+      const PipeHdr h = *reinterpret_cast<const PipeHdr*>(st + L::hdr);
+      if (h.first) {
+        r0 = h.r0;
+        nr = h.nr;
+        if (t < nr) {
+          const long long* rps = reinterpret_cast<const long long*>(st + L::rp);
+          my_s = rps[t + h.dr];
+          my_e = rps[t + h.dr + 1];
+#pragma unroll
+          for (int k = 0; k < Epi::kIn; ++k)
+            inr[k] = reinterpret_cast<const double*>(st + L::ein)[k * L::ein_stride + t + h.dr];
+        }
+      }
+      if (t < nr) {
+        const double* vs = reinterpret_cast<const double*>(st + L::v) + h.dv - h.c0;
+        const int* cs = reinterpret_cast<const int*>(st + L::ci) + h.dci - h.c0;
+        const long long lo = max(my_s, h.c0), hi = min(my_e, h.c1);
+        for (long long k = lo; k < hi; k += 8) {
+          double vv[8], xv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (k + u < hi) {
+              vv[u] = vs[k + u];
+              xv[u] = __ldg(x + cs[k + u]);
+            }
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (k + u < hi) acc = add(acc, mul(vv[u], xv[u]));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == stages) {
+        s = 0;
+        ph ^= 1;
+      }
+      if (h.last) break;
+    }
+    if (t < nr) e.row(r0 + t, acc, inr);
+  }
+  e.template finish<kPipeRows, true>();
 }
+
+// ------------------------------------------------------ stencil engine
 
 // NP > 0: compile-time point count (fully unrolled); NP == 0: runtime npts
 template <class Epi, int DIM, int NP>
 __global__ void __launch_bounds__(kThreads) stencil_spmv_kernel(const __grid_constant__ StencilView S,
                                                                 const double* __restrict__ x, Epi epi) {
-  if (!epi.active()) return;
+  __shared__ int go;
+  if (threadIdx.x == 0) go = epi.active();  // one gate decision per CTA
+  __syncthreads();
+  if (!go) return;
   Epi e = epi;
-  epi_init(e, 0);
+  e.init();
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = S.row_lo + (long long)blockIdx.x * kThreads + threadIdx.x; i < S.row_hi; i += stride) {
     int c[3] = {0, 0, 0};
@@ -259,9 +390,12 @@ __global__ void __launch_bounds__(kThreads) stencil_spmv_kernel(const __grid_con
     } else {
       c[2] = (int)i;
     }
+    double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+#pragma unroll
+    for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][i];
     const int km1 = (int)S.k - 1;
-    double acc = 0.0;
     const int npts = NP > 0 ? NP : S.npts;
+    double acc = 0.0;
 #pragma unroll
     for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
       if (NP == 0 && p >= npts) break;
@@ -273,9 +407,9 @@ __global__ void __launch_bounds__(kThreads) stencil_spmv_kernel(const __grid_con
       }
       if (ok) acc = add(acc, mul(S.coef[p], __ldg(x + i + S.foff[p])));
     }
-    e.row(i, acc);
+    e.row(i, acc, inr);
   }
-  e.finish();
+  e.template finish<kThreads, false>();
 }
 
 }  // namespace pbs

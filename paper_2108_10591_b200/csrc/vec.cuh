@@ -2,6 +2,7 @@
 // single-CTA coefficient/bookkeeping kernel (sm_100a).
 #pragma once
 #include "common.cuh"
+#include "finalize.cuh"
 
 namespace pbs {
 
@@ -14,13 +15,22 @@ struct VecPtrs {
   double* v[kNumVecs];
 };
 
+// Gate of the first kernel after the spine SpMV: once a check has stopped the
+// solve, the stop iteration's spine product has now run, so close the spine
+// gate for any iterations the host launched ahead.
+__device__ __forceinline__ bool gate_after_spine(SolverState* st) {
+  if (gate_all(st)) return true;
+  if (st && blockIdx.x == 0 && threadIdx.x == 0 && !dev_err(st) && !st->run_all) st->run_spine = 0;
+  return false;
+}
+
 // ---------------------------------------------------------------------------
 // K2: block 1 of the pipelined iteration (solvers.py:678-701, 715) in one
 // pass.  Reads r p u s t y As l g w z x (12 vectors), writes p u w t z y x r
 // (8); o and q stay in registers unless the single-step seam asks for them.
 __global__ void __launch_bounds__(kThreads) k2_update_kernel(VecPtrs V, long long n, SolverState* st,
                                                              int store_temps) {
-  if (!gate_all(st)) return;
+  if (!gate_after_spine(st)) return;
   const double alpha = st->alpha, beta = st->beta, zeta = st->zeta, eta = st->eta;
   double *__restrict__ x = V.v[VX], *__restrict__ r = V.v[VR], *__restrict__ p = V.v[VP],
          *__restrict__ u = V.v[VU], *__restrict__ t = V.v[VT], *__restrict__ w = V.v[VW],
@@ -58,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k2_update_kernel(VecPtrs V, long lon
 
 // p, o, u (solvers.py:678-683; also ssBiCGSafe2 solvers.py:563-568)
 __global__ void __launch_bounds__(kThreads) pou_kernel(VecPtrs V, long long n, SolverState* st) {
-  if (!gate_all(st)) return;
+  if (!gate_after_spine(st)) return;
   const double beta = st->beta, zeta = st->zeta, eta = st->eta;
   double *__restrict__ p = V.v[VP], *__restrict__ u = V.v[VU], *__restrict__ o = V.v[VO];
   const double *__restrict__ r = V.v[VR], *__restrict__ s = V.v[VS], *__restrict__ t = V.v[VT],
@@ -163,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const
     acc[DH] = add(acc[DH], mul(r0, tv));
     acc[DR] = add(acc[DR], mul(rv, rv));
   }
-  block_reduce9(acc, partials + (size_t)blockIdx.x * kNumDots);
+  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kNumDots);
 }
 
 // PartitionPlan chains (reduction.py:282-283 with kernels.py:103-107): block w
@@ -183,149 +193,6 @@ __global__ void dots9_plan_kernel(const long long* bounds, const double* s, cons
   double acc = 0.0;
   for (long long k = lo; k < hi; ++k) acc = add(acc, mul(xa[k], ya[k]));
   partials[(size_t)blockIdx.x * kNumDots + j] = acc;
-}
-
-// ---------------------------------------------------------------------------
-// Coefficient step + _Run bookkeeping for check j (solvers.py:645-674,
-// 736-739; coefficients.py:35-106).  One thread.
-
-__device__ __forceinline__ bool guard(double q, double scale) {
-  return !isfinite(q) || fabs(q) <= mul(1e-14, scale);
-}
-
-__device__ void check_iteration(SolverState* st, long long j, const double* d, int replaced) {
-  const bool first = j == 0;
-  if (first) st->r0_norm = sqrt(d[DR]);
-  // _Run.rel_of (solvers.py:176-179): Python max(rr, 0.0) keeps rr unless 0.0 > rr
-  double rel;
-  if (st->r0_norm == 0.0) {
-    rel = 0.0;
-  } else {
-    const double m = (0.0 > d[DR]) ? 0.0 : d[DR];
-    rel = sqrt(m) / st->r0_norm;
-  }
-  long long slot = st->n_records;
-  if (st->record_history) {
-    st->hist_rel[slot] = rel;
-    st->hist_flags[slot] = replaced ? PBS_HIST_REPLACED : 0;
-    st->n_records = slot + 1;
-  }
-  auto stop = [&](int status, long long iters, bool failure) {
-    st->status = status;
-    st->iterations = iters;
-    if (failure) st->failure_iter = j;
-    st->run_all = 0;
-    if (st->spine_done) st->run_spine = 0;
-  };
-  if (j == st->max_iters) {  // final record after the loop
-    stop(rel <= st->tol ? PBS_CONVERGED : PBS_MAX_ITERS, st->max_iters, false);
-    st->run_spine = 0;
-    return;
-  }
-  if (!isfinite(rel)) return stop(PBS_NON_FINITE, j, true);
-  if (rel <= st->tol) return stop(PBS_CONVERGED, j, false);
-  // compute_alpha_beta_safe (coefficients.py:60-84)
-  const double f = d[DF], g = d[DG], h = first ? 0.0 : d[DH];
-  double alpha, beta;
-  int q = PBS_BD_NONE;
-  if (first) {
-    if (guard(g, fabs(g))) q = PBS_BD_INITIAL_ALPHA;
-    alpha = f / g;
-    beta = 0.0;
-  } else {
-    const double denom_beta = mul(st->zeta, st->f_prev);
-    if (guard(denom_beta, fabs(denom_beta))) {
-      q = PBS_BD_BETA;
-    } else {
-      beta = mul(st->alpha, f) / denom_beta;
-      const double bh = mul(beta, h);
-      const double denom_alpha = add(g, bh);
-      if (guard(denom_alpha, add(fabs(g), fabs(bh)))) q = PBS_BD_ALPHA;
-      alpha = f / denom_alpha;
-    }
-  }
-  // compute_zeta_eta_safe (coefficients.py:87-106)
-  double zeta = 0.0, eta = 0.0;
-  if (q == PBS_BD_NONE) {
-    const double a = d[DA], b = first ? 0.0 : d[DB], c = first ? 0.0 : d[DC], dd = d[DD],
-                 e = first ? 0.0 : d[DE];
-    if (first || (b == 0.0 && c == 0.0 && e == 0.0)) {
-      if (guard(a, fabs(a))) q = PBS_BD_ZETA;
-      zeta = dd / a;
-      eta = 0.0;
-    } else {
-      const double ab = mul(a, b), cc = mul(c, c);
-      const double det = sub(ab, cc);
-      if (guard(det, add(fabs(ab), cc))) {
-        q = PBS_BD_ZETA_ETA;
-      } else {
-        zeta = sub(mul(b, dd), mul(c, e)) / det;
-        eta = sub(mul(a, e), mul(c, dd)) / det;
-      }
-    }
-  }
-  if (q != PBS_BD_NONE) {
-    st->breakdown = q;
-    return stop(PBS_BREAKDOWN, j, true);
-  }
-  st->alpha = alpha;
-  st->beta = beta;
-  st->zeta = zeta;
-  st->eta = eta;
-  st->f_prev = f;
-  if (st->record_history) {
-    st->hist_coef[4 * slot + 0] = alpha;
-    st->hist_coef[4 * slot + 1] = beta;
-    st->hist_coef[4 * slot + 2] = zeta;
-    st->hist_coef[4 * slot + 3] = eta;
-    st->hist_flags[slot] |= PBS_HIST_HAS_COEF;
-  }
-  if (!(isfinite(alpha) && isfinite(beta) && isfinite(zeta) && isfinite(eta)))
-    return stop(PBS_NON_FINITE, j, true);
-}
-
-// Finalize: reduce the batch partials (tree: xor-butterfly per dot across
-// nparts blocks; plan: left-to-right chain, reduction.py:285-294), then run
-// the check for j = st->iter and advance st->iter.  9 warps, 1 CTA.
-__global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const double* partials, int nparts,
-                                                       int chain, int replaced) {
-  __shared__ double dots[kNumDots];
-  __shared__ int work;
-  if (threadIdx.x == 0) work = !dev_err(st) && st->run_all;
-  __syncthreads();
-  const long long j = st->iter;
-  if (work) {
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    double acc;
-    if (chain) {
-      if (lane == 0) {
-        acc = partials[warp];
-        for (int b = 1; b < nparts; ++b) acc = add(acc, partials[(size_t)b * kNumDots + warp]);
-        dots[warp] = acc;
-      }
-    } else {
-      acc = 0.0;
-      for (int b = lane; b < nparts; b += 32) acc = add(acc, partials[(size_t)b * kNumDots + warp]);
-      for (int o = 16; o > 0; o >>= 1) acc = add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-      if (lane == 0) dots[warp] = acc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < kNumDots; ++k) st->dots[k] = dots[k];
-      check_iteration(st, j, dots, replaced);
-    }
-  } else if (threadIdx.x == 0 && !dev_err(st)) {
-    st->run_spine = 0;  // the stop iteration's spine product has run
-  }
-  if (threadIdx.x == 0) {
-    st->iter = j + 1;
-    if (st->mirror) {
-      st->mirror->iter = j + 1;
-      st->mirror->run_all = st->run_all;
-      st->mirror->err = dev_err(st) ? 1 : 0;
-      __threadfence_system();
-    }
-  }
 }
 
 }  // namespace pbs

@@ -1,0 +1,54 @@
+"""Profiling driver: a fixed number of p-BiCGSafe iterations on a BASELINE config.
+
+Launch sequence is deterministic (no graphs unless --graphs): 1 SpMV (b = A·1),
+then setup (2 SpMV + finalize) and 4 kernels per iteration, so ncu's -s/-c
+select exact kernels, e.g.
+
+    ncu --metrics gpu__time_duration.sum -c 200 --csv python tools/prof_solve.py --iters 40
+"""
+
+import argparse
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--iters", type=int, default=40)
+    ap.add_argument("--operator", default="csr", choices=("csr", "stencil"))
+    ap.add_argument("--method", default="pbicgsafe")
+    ap.add_argument("--graphs", action="store_true")
+    ap.add_argument("--repeat", type=int, default=1)
+    args = ap.parse_args()
+    import torch
+
+    import paper_2108_10591_b200 as pb
+    from paper_2108_10591_b200 import problems
+    from paper_2108_10591_b200.operators import DeviceMatrix
+
+    torch.cuda.set_device(0)
+    st = problems.config_stencil(args.config)
+    if args.operator == "csr":
+        rp, ci, v = problems.stencil_csr(st, col_dtype=np.int32)
+        dm = DeviceMatrix.from_csr((rp, ci, v))
+    else:
+        dm = DeviceMatrix.from_stencil(st)
+    n = dm.n_rows
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    b = torch.empty_like(ones)
+    dm.spmv_dev(ones.data_ptr(), b.data_ptr())
+    bh = b.cpu().numpy()
+    cfg = pb.SolverConfig(tol=1e-30, max_iters=args.iters)
+    for _ in range(args.repeat):
+        out = pb.solve(dm, bh, method=args.method, config=cfg, engine=pb.DeviceEngine(use_graphs=args.graphs))
+    print(f"{args.config} {args.operator} {args.method}: {out.iterations} iterations, "
+          f"{out.device['device_ms']:.3f} ms, launches {out.device['kernel_launches']}")
+
+
+if __name__ == "__main__":
+    main()
