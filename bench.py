@@ -242,14 +242,20 @@ def run_ours(args):
     # roofline of the dominant kernel (K3: Aw SpMV + l,g,s epilogue + 9 dot partials)
     peak, peak_src = peaks()
     m_a = 12 * nnz + 8 * (n + 1)
-    k3_bytes = m_a + 12 * 8 * n
-    k1_bytes = m_a + 2 * 8 * n
-    k2_bytes = 20 * 8 * n
-    it_bytes = 2 * m_a + 34 * 8 * n
+    k3_bytes = m_a + 12 * 8 * n     # w gather, As l g s y r r0s t reads, l g s writes
+    k12_bytes = m_a + 20 * 8 * n    # s gather, r p u t y l g w z x reads, As p u w t z y x r writes
+    it_bytes = 2 * m_a + 34 * 8 * n  # SURVEY 8(d) three-phase minimum (K1, K2, K3)
+    it_bytes_fused = 2 * m_a + 32 * 8 * n  # this schedule: K1+K2 fused (As not re-read)
     kms = {name: sum(r.kernel_ms[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
     kcnt = {name: sum(r.kernel_count[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
     k3_avg = kms["K3_Aw_epilogue"] / max(kcnt["K3_Aw_epilogue"], 1)
     k3_gbs = k3_bytes / (k3_avg * 1e-3) / 1e9
+    k12_avg = kms["K1_As"] / max(kcnt["K1_As"], 1)
+    k12_gbs = k12_bytes / (k12_avg * 1e-3) / 1e9
+    if kms["K1_As"] > kms["K3_Aw_epilogue"]:  # dominant kernel = larger share of the step
+        dom = ("K12 (As CSR SpMV + fused p u w t z y x r updates)", k12_bytes, k12_avg, k12_gbs)
+    else:
+        dom = ("K3 (Aw CSR SpMV + l,g,s updates + next 9-dot partials + fused check)", k3_bytes, k3_avg, k3_gbs)
     tim_ms = sum(r.device_ms for r in tres)
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "k3_dram_bytes.json")
@@ -259,13 +265,15 @@ def run_ours(args):
         except Exception:
             traffic = None
     kernels = {}
-    for name, byt in (("K1_As", k1_bytes), ("K2_update", k2_bytes), ("K3_Aw_epilogue", k3_bytes)):
+    for name, byt in (("K1_As", k12_bytes), ("K3_Aw_epilogue", k3_bytes)):
         if kcnt[name]:
             avg = kms[name] / kcnt[name]
             kernels[name] = {"avg_us": avg * 1e3, "alg_bytes": byt, "GBps": byt / (avg * 1e-3) / 1e9,
                              "frac": byt / (avg * 1e-3) / 1e9 / peak, "share_of_step": kms[name] / tim_ms}
-    fin = kms["F_finalize"] / max(kcnt["F_finalize"], 1)
-    kernels["F_finalize"] = {"avg_us": fin * 1e3, "share_of_step": kms["F_finalize"] / tim_ms}
+    kernels["K1_As"]["name"] = "K12: As = A s fused with the row-local p u w t z y x r updates"
+    if kcnt["F_finalize"]:
+        fin = kms["F_finalize"] / kcnt["F_finalize"]
+        kernels["F_finalize"] = {"avg_us": fin * 1e3, "share_of_step": kms["F_finalize"] / tim_ms}
 
     # e2e through the public API, pinned host buffers, upload + solve + readback per step
     e2e = None
@@ -307,15 +315,16 @@ def run_ours(args):
                        "l2": "inputs larger than L2: CSR 192 MB + 18 workspace vectors 302 MB per solve "
                              "vs 126 MB L2",
                        "graphs": True},
-            "roofline": {"bound": "hbm", "achieved": k3_gbs, "peak": peak, "unit": "GB/s",
-                         "frac": k3_gbs / peak, "traffic": traffic,
-                         "kernel": "K3 (Aw CSR SpMV + l,g,s updates + next 9-dot partials)",
-                         "alg_bytes_per_launch": k3_bytes, "avg_launch_us": k3_avg * 1e3,
+            "roofline": {"bound": "hbm", "achieved": dom[3], "peak": peak, "unit": "GB/s",
+                         "frac": dom[3] / peak, "traffic": traffic, "kernel": dom[0],
+                         "alg_bytes_per_launch": dom[1], "avg_launch_us": dom[2] * 1e3,
                          "peak_source": peak_src},
             "iteration_roofline": {"alg_bytes_per_iter": it_bytes,
                                    "achieved_GBps": it_bytes * iters_per_s / world / 1e9,
                                    "frac": it_bytes * iters_per_s / world / 1e9 / peak,
-                                   "note": "B_iter = 2*(12 nnz + 8(n+1)) + 34*8n (SURVEY 8(d))"},
+                                   "note": "B_iter = 2*(12 nnz + 8(n+1)) + 34*8n (SURVEY 8(d)); this "
+                                           "schedule moves 2*(12 nnz+8(n+1)) + 32*8n (K1+K2 fused)",
+                                   "frac_own_schedule": it_bytes_fused * iters_per_s / world / 1e9 / peak},
             "kernels": kernels,
             "timing_mode_it_per_s": world * sum(r.iterations for r in tres) / (tim_ms / 1e3),
             "e2e": e2e,

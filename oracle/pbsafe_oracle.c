@@ -122,19 +122,41 @@ typedef struct {
   int64_t* bounds;
 } or_plan;
 
-/* Neumaier-compensated dot over [lo, hi): a near-exact reference order used
- * only to bracket the reduction-order sensitivity of iteration counts (the
- * reference has no such mode). */
+/* Near-exact dot over [lo, hi): double-double accumulation with exact
+ * products (Dekker TwoProduct, no FMA needed), rounded once at the end — in
+ * all but pathological cases the correctly rounded dot, hence independent of
+ * summation order.  The reference has no such mode; it is the order-free
+ * yardstick for the GPU's double-double tree batch (iteration-count
+ * parity). */
+typedef struct {
+  double hi, lo;
+} dd_t;
+
+static dd_t dd_add(dd_t a, dd_t b) {
+  double s = a.hi + b.hi;
+  double bb = s - a.hi;
+  double e = (a.hi - (s - bb)) + (b.hi - bb);
+  e = e + (a.lo + b.lo);
+  double hi = s + e;
+  dd_t r = {hi, e - (hi - s)};
+  return r;
+}
+
+static dd_t two_prod(double a, double b) {
+  const double sp = 134217729.0; /* 2^27 + 1 */
+  double p = a * b;
+  double ca = sp * a, cb = sp * b;
+  double ah = ca - (ca - a), al = a - ah;
+  double bh = cb - (cb - b), bl = b - bh;
+  double err = ((ah * bh - p) + ah * bl + al * bh) + al * bl;
+  dd_t r = {p, err};
+  return r;
+}
+
 static double dot_compensated(const double* x, const double* y, int64_t lo, int64_t hi) {
-  double s = 0.0, c = 0.0;
-  for (int64_t k = lo; k < hi; ++k) {
-    double p = x[k] * y[k];
-    double t = s + p;
-    if (fabs(s) >= fabs(p)) c += (s - t) + p;
-    else c += (p - t) + s;
-    s = t;
-  }
-  return s + c;
+  dd_t acc = {0.0, 0.0};
+  for (int64_t k = lo; k < hi; ++k) acc = dd_add(acc, two_prod(x[k], y[k]));
+  return acc.hi + acc.lo;
 }
 
 static int g_compensated = 0;
@@ -350,7 +372,7 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   if (cfg->threads > 0) omp_set_num_threads(cfg->threads);
 #endif
   memset(res, 0, sizeof(*res));
-  g_compensated = cfg->workers < 0;  /* workers < 0: compensated dots (bracketing only) */
+  g_compensated = cfg->workers < 0;  /* workers < 0: near-exact dots (order-free yardstick) */
   res->failure_iter = -1;
   res->nonfinite_index = -1;
   mat_t A = {n, rp, ci, v, res};

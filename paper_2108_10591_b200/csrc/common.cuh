@@ -18,6 +18,7 @@ namespace pbs {
 constexpr int kThreads = 256;          // CTA size of every streaming kernel
 constexpr int kChunk = 2048;           // CSR products staged per smem chunk (16 KiB)
 constexpr int kNumDots = 9;            // a b c d e f g h r  (reduction.py:32)
+constexpr int kPartStride = 2 * kNumDots;  // doubles per partial record (double-double)
 constexpr int kMaxStencil = 27;
 constexpr long long kNoError = 0x7fffffffffffffffLL;
 
@@ -119,27 +120,56 @@ __device__ __forceinline__ void block_bar() {
     __syncthreads();
 }
 
-// Block-level reduction of 9 per-thread partials into out[j] (threads 0..8
-// write, then __threadfence so a last-CTA reader sees them).  Fixed shape
-// (xor-butterfly in warps, then warps in index order): the result depends only
-// on the data-to-thread mapping, never on timing.
+// ---- double-double accumulation of the dot batch --------------------------
+// Each dot is carried as an unevaluated sum hi + lo (~106 bits): products are
+// split exactly (TwoProduct via fma), sums by TwoSum.  The rounded result
+// hi + lo is the correctly rounded dot in all but pathological cases, so the
+// batch no longer depends on the reduction order (iteration-
+// count parity).
+struct Ddbl {
+  double hi, lo;
+};
+
+__device__ __forceinline__ Ddbl dd_add(Ddbl a, Ddbl b) {
+  const double s = add(a.hi, b.hi);
+  const double bb = sub(s, a.hi);
+  double e = add(sub(a.hi, sub(s, bb)), sub(b.hi, bb));
+  e = add(e, add(a.lo, b.lo));
+  const double hi = add(s, e);
+  return Ddbl{hi, sub(e, sub(hi, s))};
+}
+
+__device__ __forceinline__ Ddbl dd_prod(double a, double b) {
+  const double p = mul(a, b);
+  return Ddbl{p, __fma_rn(a, b, -p)};
+}
+
+__device__ __forceinline__ Ddbl dd_shfl_xor(Ddbl v, int o) {
+  return Ddbl{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
+}
+
+// Block-level reduction of 9 per-thread double-double partials into
+// out[2*j], out[2*j+1] (threads 0..8 write, then __threadfence so a last-CTA
+// reader sees them).  Fixed shape (xor-butterfly in warps, then warps in
+// index order): the result depends only on the data-to-thread mapping.
 template <int NT, bool NAMED>
-__device__ __forceinline__ void block_reduce9(double (&acc)[kNumDots], double* out) {
-  __shared__ double red[NT / 32][kNumDots];
+__device__ __forceinline__ void block_reduce9(Ddbl (&acc)[kNumDots], double* out) {
+  __shared__ Ddbl red[NT / 32][kNumDots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < kNumDots; ++j) {
-    double v = acc[j];
+    Ddbl v = acc[j];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = add(v, __shfl_xor_sync(0xffffffffu, v, o));
+    for (int o = 16; o > 0; o >>= 1) v = dd_add(v, dd_shfl_xor(v, o));
     if (lane == 0) red[warp][j] = v;
   }
   block_bar<NT, NAMED>();
   if (threadIdx.x < kNumDots) {
-    double v = red[0][threadIdx.x];
+    Ddbl v = red[0][threadIdx.x];
 #pragma unroll
-    for (int w = 1; w < NT / 32; ++w) v = add(v, red[w][threadIdx.x]);
-    out[threadIdx.x] = v;
+    for (int w = 1; w < NT / 32; ++w) v = dd_add(v, red[w][threadIdx.x]);
+    out[2 * threadIdx.x] = v.hi;
+    out[2 * threadIdx.x + 1] = v.lo;
     __threadfence();
   }
 }

@@ -115,33 +115,37 @@ __device__ __forceinline__ void publish(SolverState* st, long long next_iter) {
   }
 }
 
-// Reduce partials[nparts][9] -> dots[9] with NT threads, fixed shape:
-// dot j is summed by a team of T = NT/9 threads (strided, sequential per
-// thread), then the team's values left to right.  chain: left-to-right over
-// parts (reduction.py:285-294 _combine) by one thread per dot.
+// Reduce partial records (kPartStride doubles each: hi/lo per dot) -> dots[9]
+// with NT threads, fixed shape: dot j is summed in double-double by a team of
+// T = NT/9 threads (strided, sequential per thread), then the team's values
+// in order, then rounded once.  chain: the reference's left-to-right combine
+// of plain per-range values (reduction.py:285-294 _combine), one thread per dot.
 template <int NT, bool NAMED>
 __device__ void reduce_parts(const double* partials, int nparts, int chain, double* dots) {
   constexpr int T = NT / kNumDots;
-  __shared__ double team[kNumDots][T];
+  __shared__ Ddbl team[kNumDots][T];
   const int t = threadIdx.x;
   if (chain) {
     if (t < kNumDots) {
-      double acc = __ldcg(partials + t);
-      for (int b = 1; b < nparts; ++b) acc = add(acc, __ldcg(partials + (size_t)b * kNumDots + t));
+      double acc = __ldcg(partials + 2 * t);
+      for (int b = 1; b < nparts; ++b) acc = add(acc, __ldcg(partials + (size_t)b * kPartStride + 2 * t));
       dots[t] = acc;
     }
   } else {
     const int j = t / T, l = t % T;
     if (j < kNumDots) {
-      double acc = 0.0;
-      for (int b = l; b < nparts; b += T) acc = add(acc, __ldcg(partials + (size_t)b * kNumDots + j));
+      Ddbl acc{0.0, 0.0};
+      for (int b = l; b < nparts; b += T) {
+        const double* p = partials + (size_t)b * kPartStride + 2 * j;
+        acc = dd_add(acc, Ddbl{__ldcg(p), __ldcg(p + 1)});
+      }
       team[j][l] = acc;
     }
     block_bar<NT, NAMED>();
     if (t < kNumDots) {
-      double acc = team[t][0];
-      for (int k = 1; k < T; ++k) acc = add(acc, team[t][k]);
-      dots[t] = acc;
+      Ddbl acc = team[t][0];
+      for (int k = 1; k < T; ++k) acc = dd_add(acc, team[t][k]);
+      dots[t] = add(acc.hi, acc.lo);
     }
   }
   block_bar<NT, NAMED>();

@@ -164,7 +164,7 @@ static int ensure_ws(pbs_mat* m, long long hist_slots) {
     ws->stride = ((size_t)ws->n + 2 + 31) / 32 * 32;  // +2: aligned bulk-copy over-read
     CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
     for (int k = 0; k < kNumVecs; ++k) ws->V.v[k] = ws->base + ws->stride * k;
-    CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kNumDots));
+    CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kPartStride));
     CK(cudaMalloc(&ws->st, sizeof(SolverState)));
     CK(cudaHostAlloc(&ws->mirror_h, sizeof(HostMirror), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ws->mirror_d, ws->mirror_h, 0));
@@ -269,17 +269,34 @@ void Launcher::trace_point() {
   trace_cfg->trace_fn(iter, ptrs, trace_cfg->trace_user);
 }
 
-// pipelined CSR engine: stage count from the opt-in shared-memory limit
+// pipelined CSR engine: CTAs per SM (PBS_PIPE_CTAS, default 2) and the stage
+// count that fills the shared memory those CTAs share
+static int pipe_ctas_per_sm() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PBS_PIPE_CTAS");
+    v = e ? atoi(e) : 2;
+    if (v < 1) v = 1;
+    if (v > 4) v = 4;
+  }
+  return v;
+}
+
 template <class Epi>
 static int pipe_config(pbs_ctx* ctx, int* stages, size_t* smem) {
-  using LY = StageLayout<Epi::kIn>;
+  using LY = StageLayout;
   const void* k = (const void*)csr_pipe_kernel<Epi>;
   auto it = ctx->occ.find(k);
   int st;
   if (it == ctx->occ.end()) {
+    int per_sm = 0;
+    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-    const size_t budget = (size_t)optin - 1024 - 64;  // static smem of the kernel
+    // per-CTA budget: the SM's shared memory split between the resident CTAs,
+    // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
+    size_t budget = (size_t)per_sm / pipe_ctas_per_sm() - 1024 - 2048;
+    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
     st = (int)((budget - kPipeBarrierBytes) / LY::bytes);
     if (st > kMaxStages) st = kMaxStages;
     if (st < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
@@ -305,7 +322,8 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     int stages;
     size_t smem;
     if (pipe_config<Epi>(L.ctx, &stages, &smem)) return 0;
-    grid = (int)(nblk < L.ctx->sms ? (nblk > 0 ? nblk : 1) : L.ctx->sms);
+    const long long cap = (long long)L.ctx->sms * pipe_ctas_per_sm();
+    grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, stages);
   } else {
     StencilView S = m->sv;
@@ -385,6 +403,26 @@ static EpiDots epi_dots(Workspace* ws, const Mode& md, int spine, int fuse, int 
   return e;
 }
 
+static EpiK12 epi_k12(Workspace* ws, const Mode& md) {
+  EpiK12 e{};
+  auto& V = ws->V.v;
+  e.as = V[VAS];
+  e.p = V[VP];
+  e.u = V[VU];
+  e.w = V[VW];
+  e.t = V[VT];
+  e.z = V[VZ];
+  e.y = V[VY];
+  e.x = V[VX];
+  e.r = V[VR];
+  e.o_out = md.store_temps ? V[VO] : nullptr;
+  e.q_out = md.store_temps ? V[VQ] : nullptr;
+  e.st = ws->st;
+  const int in[11] = {VR, VP, VU, VS, VT, VY, VL, VG, VW, VZ, VX};
+  for (int k = 0; k < 11; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
 static EpiK3 epi_k3(Workspace* ws, const Mode& md, int fuse) {
   EpiK3 e{};
   auto& V = ws->V.v;
@@ -442,11 +480,11 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
   spmv_s_check(L, ws, md, KS, 0, 0);
 }
 
-// one steady p-BiCGSafe iteration: K1, K2, K3 (+ fused check of j+1)
+// one steady p-BiCGSafe iteration: K12 (As = A s + row-local updates), K3
+// (Aw + l g s + the fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
-  vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
+  spmv_launch(L, V[VS], epi_k12(ws, md), 0, ws->n, KK1);
   const int grid = spmv_launch(L, V[VW], epi_k3(ws, md, L.trace_cfg ? 0 : 1), 0, ws->n, KK3);
   if (md.plan) {
     int np = plan_dots(L, ws, KD);
@@ -731,7 +769,7 @@ PBS_EXPORT int pbs_init(int device, pbs_ctx** out) {
   }
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
   ctx->stream = ctx->own;
-  CK(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * kNumDots));
+  CK(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * kPartStride));
   CK(cudaMalloc(&ctx->tmp_state, sizeof(SolverState)));
   *out = ctx;
   return PBS_OK;
@@ -1036,8 +1074,8 @@ PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in
   {
     auto& V = ws->V.v;
     Mode nm = md;  // the step's batch comes first; the body's partials are not needed
-    spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
     if (in[5] != 0.0) {
+      spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
       vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
       spmv_launch(L, V[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
       spmv_launch(L, V[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
@@ -1048,9 +1086,9 @@ PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in
       nm.plan = 1;  // no partials
       spmv_launch(L, V[VR], epi_dots(ws, nm, 0, 0, 0), 0, ws->n, KRS);
     } else {
-      vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, 1);
       nm.plan = 1;
       nm.store_temps = 1;
+      spmv_launch(L, V[VS], epi_k12(ws, nm), 0, ws->n, KK1);
       spmv_launch(L, V[VW], epi_k3(ws, nm, 0), 0, ws->n, KK3);
     }
   }

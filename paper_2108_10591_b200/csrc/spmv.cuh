@@ -4,12 +4,13 @@
 // where in[] holds the row's values of the epilogue's kIn input vectors.
 //
 //  * csr_pipe_kernel — CSR, warp-specialised and TMA-fed.  One CTA per SM:
-//    a producer warp streams each 256-row block's slice of row_ptr, its
+//    a producer warp streams each 256-row block's slice of row_ptr and its
 //    contiguous nonzero range of values / int32 col_idx (in <=2048-nonzero
-//    chunks) and the epilogue's input-vector segments into a ring of shared
-//    memory stages with 1-D bulk async copies (cp.async.bulk, completion on
-//    mbarriers); eight consumer warps own one row each per block, gather x
-//    (L1-cached) and accumulate the row sequentially in ascending column order
+//    chunks) into a ring of shared-memory stages with 1-D bulk async copies
+//    (cp.async.bulk, completion on mbarriers); eight consumer warps own one
+//    row each per block, prefetch the epilogue's row inputs with coalesced
+//    loads, gather x (L1-cached) and accumulate the row sequentially in
+//    ascending column order
 //    (kernels.py:95-100), so the product is bitwise the reference's while HBM
 //    sees every matrix byte once with the copy engine keeping it busy.
 //  * stencil_spmv_kernel — matrix-free constant-coefficient stencil, one
@@ -18,7 +19,8 @@
 //    equal to the CSR of the same stencil.
 //
 // Epilogues (SURVEY §8(d) kernel plan):
-//   EpiStore  y = A x                          (K1: As = A s; rr products)
+//   EpiStore  y = A x                          (rr products, plain SpMV)
+//   EpiK12    As = A s -> p u w t z y x r       (K1 fused with the row-local K2, solvers.py:678-715)
 //   EpiResid  r = b - A x  (+ r0s = r)         (setup; rr "r = b - A x")
 //   EpiK3     Aw -> l, g, s + next 9 dot partials (solvers.py:717-723, 467-482)
 //   EpiDots   s = A r + 9 dot partials          (setup s0 = A r0; rr s = A r)
@@ -51,22 +53,22 @@ struct StencilView {
 // ---------------------------------------------------------------- epilogues
 
 struct Dots9 {
-  double acc[kNumDots];
+  Ddbl acc[kNumDots];
   __device__ void zero() {
 #pragma unroll
-    for (int j = 0; j < kNumDots; ++j) acc[j] = 0.0;
+    for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
   }
-  // _safe_batch pairs (solvers.py:471-481)
+  // _safe_batch pairs (solvers.py:471-481), double-double accumulation
   __device__ void add_row(double s, double y, double r, double r0s, double t) {
-    acc[DA] = add(acc[DA], mul(s, s));
-    acc[DB] = add(acc[DB], mul(y, y));
-    acc[DC] = add(acc[DC], mul(s, y));
-    acc[DD] = add(acc[DD], mul(s, r));
-    acc[DE] = add(acc[DE], mul(y, r));
-    acc[DF] = add(acc[DF], mul(r0s, r));
-    acc[DG] = add(acc[DG], mul(r0s, s));
-    acc[DH] = add(acc[DH], mul(r0s, t));
-    acc[DR] = add(acc[DR], mul(r, r));
+    acc[DA] = dd_add(acc[DA], dd_prod(s, s));
+    acc[DB] = dd_add(acc[DB], dd_prod(y, y));
+    acc[DC] = dd_add(acc[DC], dd_prod(s, y));
+    acc[DD] = dd_add(acc[DD], dd_prod(s, r));
+    acc[DE] = dd_add(acc[DE], dd_prod(y, r));
+    acc[DF] = dd_add(acc[DF], dd_prod(r0s, r));
+    acc[DG] = dd_add(acc[DG], dd_prod(r0s, s));
+    acc[DH] = dd_add(acc[DH], dd_prod(r0s, t));
+    acc[DR] = dd_add(acc[DR], dd_prod(r, r));
   }
 };
 
@@ -78,19 +80,21 @@ struct DotSink {
   template <int NT, bool NAMED>
   __device__ void finish(Dots9& d, SolverState* st) {
     if (!partials) return;
-    block_reduce9<NT, NAMED>(d.acc, partials + (size_t)blockIdx.x * kNumDots);
+    block_reduce9<NT, NAMED>(d.acc, partials + (size_t)blockIdx.x * kPartStride);
     if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced);
   }
 };
 
 struct EpiStore {
   static constexpr int kIn = 0;
+  static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double* y;
   SolverState* st;
   int tag;
   int spine;  // gate on run_spine instead of run_all
   const double* in[1];
   __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
+  __device__ void on_skip() const {}
   __device__ void init() {}
   __device__ void row(long long i, double v, const double*) {
     y[i] = v;
@@ -102,11 +106,13 @@ struct EpiStore {
 
 struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
   static constexpr int kIn = 1;
+  static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double* r;
   double* r0s;  // nullable: also r0s = r (solvers.py:617)
   SolverState* st;
   const double* in[kIn];  // b
   __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
   __device__ void init() {}
   __device__ void row(long long i, double ax, const double* v) {
     if (!isfinite(ax)) report_nonfinite(st, PBS_TAG_AX, i);
@@ -120,6 +126,7 @@ struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
 
 struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   static constexpr int kIn = 4;
+  static constexpr int kGatherBatch = 4;  // x gathers in flight per row
   double* s;
   SolverState* st;
   int tag;
@@ -128,6 +135,7 @@ struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   const double* in[kIn];  // y r r0s t
   Dots9 d;
   __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
+  __device__ void on_skip() const {}
   __device__ void init() { d.zero(); }
   __device__ void row(long long i, double v, const double* in4) {
     s[i] = v;
@@ -138,8 +146,61 @@ struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
 };
 
+struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local K2 updates)
+  static constexpr int kIn = 11;
+  static constexpr int kGatherBatch = 8;  // x gathers in flight per row
+  double* as;  // As is kept for K3
+  double *p, *u, *w, *t, *z, *y, *x, *r;
+  double *o_out, *q_out;  // nullable (single-step parity)
+  SolverState* st;
+  const double* in[kIn];  // r p u s t y l g w z x
+  double alpha, beta, zeta, eta;
+  int full;  // 0: the check stopped the solve; only the spine product runs
+  __device__ bool active() const { return gate_spine(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() {
+    full = gate_all(st);
+    alpha = st->alpha;
+    beta = st->beta;
+    zeta = st->zeta;
+    eta = st->eta;
+  }
+  __device__ void row(long long i, double asv, const double* v) {
+    as[i] = asv;
+    if (!isfinite(asv)) report_nonfinite(st, PBS_TAG_AS, i);
+    if (!full) return;
+    const double rv = v[0], pv = v[1], uv = v[2], sv = v[3], tv = v[4], yv = v[5];
+    const double lv = v[6], gv = v[7], wv = v[8], zv = v[9], xv = v[10];
+    const double pn = asd(rv, beta, pv, uv);              // p = r + beta*(p - u)
+    const double o = lc2(1.0, sv, beta, tv);              // o = s + beta*t
+    const double un = lcn(zeta, o, eta, yv, beta, uv);    // u = zeta*o + eta*(y + beta*u)
+    const double q = lc2(1.0, asv, beta, lv);             // q = As + beta*l
+    const double wn = lcn(zeta, q, eta, gv, beta, wv);    // w = zeta*q + eta*(g + beta*w)
+    const double tn = lc2(1.0, o, -1.0, wn);              // t = o - w
+    const double zn = lc3(zeta, rv, eta, zv, -alpha, un); // z = zeta*r + eta*z - alpha*u
+    const double yn = lc3(zeta, sv, eta, yv, -alpha, wn); // y = zeta*s + eta*y - alpha*w
+    const double xn = lc3(1.0, xv, alpha, pn, 1.0, zn);   // x = x + alpha*p + z
+    const double rn = lc3(1.0, rv, -alpha, o, -1.0, yn);  // r = r - alpha*o - y
+    p[i] = pn;
+    u[i] = un;
+    w[i] = wn;
+    t[i] = tn;
+    z[i] = zn;
+    y[i] = yn;
+    x[i] = xn;
+    r[i] = rn;
+    if (o_out) {
+      o_out[i] = o;
+      q_out[i] = q;
+    }
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() {}
+};
+
 struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
   static constexpr int kIn = 8;
+  static constexpr int kGatherBatch = 4;  // x gathers in flight per row
   double *l, *g, *s;
   double* q_out;  // nullable (single-step parity: expose q)
   SolverState* st;
@@ -148,6 +209,11 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
   double alpha, beta, zeta, eta;
   Dots9 d;
   __device__ bool active() const { return gate_all(st); }
+  // the stop iteration's spine product (K12) has run: close the spine gate for
+  // iterations the host launched ahead
+  __device__ void on_skip() const {
+    if (!dev_err(st) && !st->run_all) st->run_spine = 0;
+  }
   __device__ void init() {
     d.zero();
     alpha = st->alpha;
@@ -174,11 +240,13 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
 
 struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:569-580)
   static constexpr int kIn = 8;
+  static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double *w, *t, *z, *y, *x, *r;
   SolverState* st;
   const double* in[kIn];  // o s u p y z x r
   double alpha, zeta, eta;
   __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
   __device__ void init() {
     alpha = st->alpha;
     zeta = st->zeta;
@@ -215,26 +283,26 @@ struct PipeHdr {
 
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
 
-template <int KIN>
 struct StageLayout {
   static constexpr size_t hdr = 0;
   static constexpr size_t rp = 128;
   static constexpr size_t v = rp + align128(sizeof(long long) * (kPipeRows + 2));
   static constexpr size_t ci = v + align128(sizeof(double) * (kPipeChunk + 2));
-  static constexpr size_t ein = ci + align128(sizeof(int) * (kPipeChunk + 4));
-  static constexpr size_t ein_stride = kPipeRows + 2;  // doubles per staged input segment
-  static constexpr size_t bytes = ein + align128(sizeof(double) * ein_stride * (KIN > 0 ? KIN : 1));
+  static constexpr size_t bytes = ci + align128(sizeof(int) * (kPipeChunk + 4));
 };
 constexpr size_t kPipeBarrierBytes = 256;
 
 template <class Epi>
-__global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
                                                                    Epi epi, int stages) {
   __shared__ int go;
-  if (threadIdx.x == 0) go = epi.active();  // one gate decision per CTA
+  if (threadIdx.x == 0) {
+    go = epi.active();  // one gate decision per CTA
+    if (!go && blockIdx.x == 0) epi.on_skip();
+  }
   __syncthreads();
   if (!go) return;
-  using L = StageLayout<Epi::kIn>;
+  using L = StageLayout;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
   uint64_t* empty = full + kMaxStages;
@@ -284,16 +352,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(CsrView A, co
         const uint32_t bc = (uint32_t)((c1b - c0b) * sizeof(int));
         uint32_t total = bv + bc;
         const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
-        const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
-        if (c == 0) total += brp + Epi::kIn * bin;
+        if (c == 0) total += brp;
         mbar_arrive_expect_tx(&full[s], total);
         if (bv) bulk_g2s(st + L::v, A.v + c0a, bv, &full[s]);
         if (bc) bulk_g2s(st + L::ci, A.ci + c0b, bc, &full[s]);
         if (c == 0) {
           bulk_g2s(st + L::rp, A.rp + r0a, brp, &full[s]);
-#pragma unroll
-          for (int e = 0; e < Epi::kIn; ++e)
-            bulk_g2s(st + L::ein + (size_t)e * L::ein_stride * sizeof(double), epi.in[e] + r0a, bin, &full[s]);
         }
         if (++s == stages) {
           s = 0;
@@ -323,28 +387,30 @@ __global__ void __launch_bounds__(kPipeThreads, 1) csr_pipe_kernel(CsrView A, co
         r0 = h.r0;
         nr = h.nr;
         if (t < nr) {
+          // epilogue inputs: coalesced loads issued now, consumed after the row
+          // sum, so their latency hides behind the x gathers
+#pragma unroll
+          for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][r0 + t];
           const long long* rps = reinterpret_cast<const long long*>(st + L::rp);
           my_s = rps[t + h.dr];
           my_e = rps[t + h.dr + 1];
-#pragma unroll
-          for (int k = 0; k < Epi::kIn; ++k)
-            inr[k] = reinterpret_cast<const double*>(st + L::ein)[k * L::ein_stride + t + h.dr];
         }
       }
       if (t < nr) {
         const double* vs = reinterpret_cast<const double*>(st + L::v) + h.dv - h.c0;
         const int* cs = reinterpret_cast<const int*>(st + L::ci) + h.dci - h.c0;
         const long long lo = max(my_s, h.c0), hi = min(my_e, h.c1);
-        for (long long k = lo; k < hi; k += 8) {
-          double vv[8], xv[8];
+        constexpr int U = Epi::kGatherBatch;
+        for (long long k = lo; k < hi; k += U) {
+          double vv[U], xv[U];
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < U; ++u)
             if (k + u < hi) {
               vv[u] = vs[k + u];
               xv[u] = __ldg(x + cs[k + u]);
             }
 #pragma unroll
-          for (int u = 0; u < 8; ++u)
+          for (int u = 0; u < U; ++u)
             if (k + u < hi) acc = add(acc, mul(vv[u], xv[u]));
         }
       }
@@ -368,7 +434,10 @@ template <class Epi, int DIM, int NP>
 __global__ void __launch_bounds__(kThreads) stencil_spmv_kernel(const __grid_constant__ StencilView S,
                                                                 const double* __restrict__ x, Epi epi) {
   __shared__ int go;
-  if (threadIdx.x == 0) go = epi.active();  // one gate decision per CTA
+  if (threadIdx.x == 0) {
+    go = epi.active();  // one gate decision per CTA
+    if (!go && blockIdx.x == 0) epi.on_skip();
+  }
   __syncthreads();
   if (!go) return;
   Epi e = epi;

@@ -151,34 +151,34 @@ __global__ void dot_final_kernel(const double* partials, int nparts, double* out
   if (threadIdx.x == 0) *out = acc;
 }
 
-// batch of the 9 safe dots, tree order, into partials[blk*9 + j]
+// batch of the 9 safe dots, double-double tree, into partials[blk*kPartStride]
 __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const double* s, const double* y,
                                                               const double* r, const double* r0s,
                                                               const double* t, double* partials,
                                                               const SolverState* st) {
   if (st && !gate_all(st)) return;
-  double acc[kNumDots];
+  Ddbl acc[kNumDots];
 #pragma unroll
-  for (int j = 0; j < kNumDots; ++j) acc[j] = 0.0;
+  for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
     const double sv = s[i], yv = y[i], rv = r[i], r0 = r0s[i], tv = t[i];
-    acc[DA] = add(acc[DA], mul(sv, sv));
-    acc[DB] = add(acc[DB], mul(yv, yv));
-    acc[DC] = add(acc[DC], mul(sv, yv));
-    acc[DD] = add(acc[DD], mul(sv, rv));
-    acc[DE] = add(acc[DE], mul(yv, rv));
-    acc[DF] = add(acc[DF], mul(r0, rv));
-    acc[DG] = add(acc[DG], mul(r0, sv));
-    acc[DH] = add(acc[DH], mul(r0, tv));
-    acc[DR] = add(acc[DR], mul(rv, rv));
+    acc[DA] = dd_add(acc[DA], dd_prod(sv, sv));
+    acc[DB] = dd_add(acc[DB], dd_prod(yv, yv));
+    acc[DC] = dd_add(acc[DC], dd_prod(sv, yv));
+    acc[DD] = dd_add(acc[DD], dd_prod(sv, rv));
+    acc[DE] = dd_add(acc[DE], dd_prod(yv, rv));
+    acc[DF] = dd_add(acc[DF], dd_prod(r0, rv));
+    acc[DG] = dd_add(acc[DG], dd_prod(r0, sv));
+    acc[DH] = dd_add(acc[DH], dd_prod(r0, tv));
+    acc[DR] = dd_add(acc[DR], dd_prod(rv, rv));
   }
-  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kNumDots);
+  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
 }
 
 // PartitionPlan chains (reduction.py:282-283 with kernels.py:103-107): block w
 // handles range [bounds[w], bounds[w+1]); thread j < 9 sums pair j
-// sequentially in ascending index order -> partials[w*9 + j].
+// sequentially in ascending index order -> partials[w*kPartStride + 2j].
 __global__ void dots9_plan_kernel(const long long* bounds, const double* s, const double* y,
                                   const double* r, const double* r0s, const double* t,
                                   double* partials, const SolverState* st) {
@@ -192,7 +192,8 @@ __global__ void dots9_plan_kernel(const long long* bounds, const double* s, cons
   const long long lo = bounds[blockIdx.x], hi = bounds[blockIdx.x + 1];
   double acc = 0.0;
   for (long long k = lo; k < hi; ++k) acc = add(acc, mul(xa[k], ya[k]));
-  partials[(size_t)blockIdx.x * kNumDots + j] = acc;
+  partials[(size_t)blockIdx.x * kPartStride + 2 * j] = acc;
+  partials[(size_t)blockIdx.x * kPartStride + 2 * j + 1] = 0.0;
 }
 
 }  // namespace pbs

@@ -168,24 +168,48 @@ def test_stencil_operator_bitwise_vs_reference(pb, name):
     _assert_outcome_bitwise(out, g, name)
 
 
+def oracle_ensemble(spec, A, b, x0, workers=(1, 2, 3, 8, 64, 512, 4096)):
+    """Iteration counts of the reference algorithm under different reduction
+    orders: PartitionPlan.balanced(n, W) chains (bitwise the reference's for
+    each W) plus near-exact double-double dots (workers=-1)."""
+    counts = {}
+    n = A.n_rows
+    for w in tuple(w for w in workers if w <= max(n, 1)) + (-1,):
+        o = orc.solve(A.row_ptr, A.col_idx, A.values, b, x0=x0, method=spec["method"], tol=spec["tol"],
+                      max_iters=spec["max_iters"], rr_epoch=spec.get("rr_epoch", 100),
+                      rr_cutoff=spec.get("rr_cutoff"), workers=w)
+        counts[w] = (o["status"], o["iterations"])
+    return counts
+
+
 @pytest.mark.parametrize("graphs", [True, False])
 @pytest.mark.parametrize("name", gc.case_names())
 def test_solve_tree_mode_matches_reference(pb, name, graphs):
+    """Fast path: the iteration count must fall inside the reference's own
+    reduction-order ensemble, widened by the north star's ±2%."""
     spec, A, b, x0, g = gc.load_case(name, orc.spmv)
     out = pb.solve(A, b, method=spec["method"], x0=x0, config=_cfg(pb, spec),
                    engine=pb.DeviceEngine(use_graphs=graphs))
-    ref_it = int(g["iterations"])
+    ens = oracle_ensemble(spec, A, b, x0)
     assert out.status.value == str(g["status"]), name
-    assert abs(out.iterations - ref_it) <= max(2, math.ceil(0.02 * ref_it)), (name, out.iterations, ref_it)
-    # identical first check (r0 from an exact SpMV; one dot reassociated)
+    assert all(st == str(g["status"]) for st, _ in ens.values()), ens
+    lo = min(c for _, c in ens.values())
+    hi = max(c for _, c in ens.values())
+    assert math.floor(0.98 * lo) - 1 <= out.iterations <= math.ceil(1.02 * hi) + 1, (name, out.iterations, ens)
     assert out.r0_norm == pytest.approx(float(g["r0_norm"]), rel=1e-13)
-    # early history agrees to rounding
-    m = min(8, len(out.history), len(g["rel"]))
+    m = min(6, len(out.history), len(g["rel"]))
     np.testing.assert_allclose([r.rel_res_recur for r in out.history[:m]], g["rel"][:m], rtol=1e-9)
     if str(g["status"]) == "converged" and int(g["n"]) > 2:
-        xs = g["x"]
-        err = np.linalg.norm(out.x - xs) / max(np.linalg.norm(xs), 1e-300)
-        assert err < 1e-5, (name, err)
+        true = np.linalg.norm(b - orc.spmv(A.row_ptr, A.col_idx, A.values, out.x)) / max(out.r0_norm, 1e-300)
+        assert true <= 100 * spec["tol"] + 1e-14, (name, true)
+
+
+def test_tree_mode_is_deterministic(pb):
+    spec, A, b, x0, g = gc.load_case("cd3d16_pbicgsafe", orc.spmv)
+    outs = [pb.solve(A, b, config=_cfg(pb, spec), engine=pb.DeviceEngine(use_graphs=gr)) for gr in (True, False, True)]
+    for o in outs[1:]:
+        assert np.array_equal([r.rel_res_recur for r in o.history], [r.rel_res_recur for r in outs[0].history])
+        assert np.array_equal(o.x, outs[0].x)
 
 
 @pytest.mark.parametrize("name", gc.case_names(trace=True))
@@ -303,6 +327,18 @@ def test_c2_spmv_bitwise_csr_and_stencil(pb, c2):
         dm.free()
 
 
+def test_c2_plan_mode_bitwise_vs_oracle(pb, c2):
+    """Full-size config 2 in the reference's order (PartitionPlan W=16): whole solve bitwise."""
+    st, rp, ci, v, b = c2
+    A = pb.CsrMatrix(len(rp) - 1, len(rp) - 1, rp, ci, v)
+    ref = orc.solve(rp, ci, v, b, tol=1e-10, max_iters=2000, workers=16, threads=os.cpu_count() or 1)
+    out = pb.solve(A, b, config=pb.SolverConfig(tol=1e-10, max_iters=2000),
+                   engine=pb.DeviceEngine(reduce="plan", workers=16))
+    assert out.iterations == ref["iterations"]
+    assert np.array_equal([r.rel_res_recur for r in out.history], ref["rel"])
+    assert np.array_equal(out.x, ref["x"])
+
+
 def test_c2_first_iterations_track_oracle(pb, c2):
     st, rp, ci, v, b = c2
     A = pb.CsrMatrix(len(rp) - 1, len(rp) - 1, rp, ci, v)
@@ -320,8 +356,8 @@ def test_c2_solve_converges_with_certificate(pb, c2):
     for method in ("pbicgsafe", "pbicgsafe-rr", "ssbicgsafe2"):
         out = pb.solve(dm, b, method=method, config=pb.SolverConfig(tol=1e-10, max_iters=2000))
         assert out.status.value == "converged", method
-        # the oracle ensemble converges in 336-352 iterations here
-        assert 300 <= out.iterations <= 400, (method, out.iterations)
+        # oracle ensemble on this system: 316-352 over reduction orders
+        assert 300 <= out.iterations <= 370, (method, out.iterations)
         true = np.linalg.norm(b - orc.spmv(rp, ci, v, out.x)) / out.r0_norm
         assert true <= 1e-8, (method, true)
     dm.free()
