@@ -85,6 +85,7 @@ __device__ __forceinline__ void report_nonfinite(SolverState* st, int tag, long 
   if (st == nullptr) return;
   atomicMin(&st->nf_row, (unsigned long long)row);
   st->nf_tag = tag;
+  if (st->mirror) st->mirror->err = 1;  // lets the host stop launching at once
 }
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }

@@ -654,7 +654,16 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
       if (ws->mirror_h->err) goto loop_end;
       if (!ws->mirror_h->run_all && j >= dev_iter) goto loop_end;
       if (j <= dev_iter + lookahead) break;
-      if (cudaStreamQuery(s) == cudaSuccess) continue;  // re-read the mirror
+      if (cudaStreamQuery(s) == cudaSuccess) {
+        // idle device but the mirror did not advance far enough: every
+        // launched iteration was gated off (stopped or failed) -> read the
+        // authoritative state and stop if nothing is left to run
+        SolverState chk;
+        CK(cudaMemcpy(&chk, ws->st, sizeof(chk), cudaMemcpyDeviceToHost));
+        if (chk.nf_row != (unsigned long long)kNoError || !chk.run_all) goto loop_end;
+        if (ws->mirror_h->iter == dev_iter) goto loop_end;  // no progress possible
+        continue;
+      }
       std::this_thread::yield();
     }
     {
