@@ -72,6 +72,7 @@ struct pbs_mat {
   int* ci = nullptr;
   double* v = nullptr;
   StencilView sv{};
+  XWin xwin{};  // x windows of the pipelined CSR engine (nwin = 0: gather x)
   Workspace* ws = nullptr;
 };
 
@@ -283,32 +284,29 @@ static int pipe_ctas_per_sm() {
 }
 
 template <class Epi>
-static int pipe_config(pbs_ctx* ctx, int* stages, size_t* smem) {
-  using LY = StageLayout;
+static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem) {
+  const BlockLayout BL(W.total, Epi::kIn);
+  int per_sm = 0, optin = 0;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  // per-CTA budget: the SM's shared memory split between the resident CTAs,
+  // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
+  size_t budget = (size_t)per_sm / pipe_ctas_per_sm() - 1024 - 2048;
+  if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
+  budget -= kPipeBarrierBytes;
+  int n = (int)(budget / (BL.bytes + ChunkLayout::bytes));
+  if (n > 4) n = 4;
+  if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
+  *bslots = n;
+  *cstages = n;
+  *smem = kPipeBarrierBytes + (size_t)n * (BL.bytes + ChunkLayout::bytes);
   const void* k = (const void*)csr_pipe_kernel<Epi>;
   auto it = ctx->occ.find(k);
-  int st;
-  if (it == ctx->occ.end()) {
-    int per_sm = 0;
-    cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
-    int optin = 0;
-    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-    // per-CTA budget: the SM's shared memory split between the resident CTAs,
-    // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
-    size_t budget = (size_t)per_sm / pipe_ctas_per_sm() - 1024 - 2048;
-    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
-    st = (int)((budget - kPipeBarrierBytes) / LY::bytes);
-    if (st > kMaxStages) st = kMaxStages;
-    if (st < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
-    size_t bytes = kPipeBarrierBytes + (size_t)st * LY::bytes;
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (it == ctx->occ.end() || (size_t)it->second < *smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
     if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
-    ctx->occ[k] = st;
-  } else {
-    st = it->second;
+    ctx->occ[k] = (int)*smem;
   }
-  *stages = st;
-  *smem = kPipeBarrierBytes + (size_t)st * LY::bytes;
   return PBS_OK;
 }
 
@@ -318,13 +316,13 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   long long nblk = (hi - lo + kThreads - 1) / kThreads;
   int grid;
   if (!m->stencil) {
-    CsrView A{m->rp, m->ci, m->v, lo, hi};
-    int stages;
+    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
+    int bslots, cstages;
     size_t smem;
-    if (pipe_config<Epi>(L.ctx, &stages, &smem)) return 0;
+    if (pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem)) return 0;
     const long long cap = (long long)L.ctx->sms * pipe_ctas_per_sm();
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
-    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, stages);
+    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages);
   } else {
     StencilView S = m->sv;
     S.row_lo = lo;
@@ -819,6 +817,104 @@ __global__ void cvt_i64_i32_kernel(const long long* in, int* out, long long n, i
   }
 }
 
+// Offset histogram for the x windows: bin = floor((col - row) / 256); per bin
+// the min / max offset seen (warp-aggregated atomics); |bin| >= kBins -> wide.
+constexpr int kBins = 65536;
+__global__ void offset_bins_kernel(const long long* rp, const int* ci, long long n_rows, int* bmin, int* bmax,
+                                   int* wide) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  const long long r_first = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (long long rb = (long long)blockIdx.x * blockDim.x; rb < n_rows; rb += stride) {
+    const long long row = rb + threadIdx.x;
+    const bool live = row < n_rows;
+    long long s = 0, e = 0;
+    if (live) {
+      s = rp[row];
+      e = rp[row + 1];
+    }
+    int len = (int)(e - s), maxlen = len;
+    for (int o = 16; o > 0; o >>= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    for (int k = 0; k < maxlen; ++k) {
+      const bool act = k < len;
+      long long off = act ? (long long)ci[s + k] - row : 0;
+      const long long bin = off >= 0 ? off / 256 : -((-off + 255) / 256);
+      const bool in = act && bin > -kBins && bin < kBins;
+      if (act && !in) *wide = 1;
+      const int key = in ? (int)bin : 0x7fffffff;
+      const unsigned grp = __match_any_sync(0xffffffffu, key);
+      const int o32 = (int)off;
+      const int gmin = __reduce_min_sync(grp, in ? o32 : 0x7fffffff);
+      const int gmax = __reduce_max_sync(grp, in ? o32 : (int)0x80000000);
+      if (in && (threadIdx.x & 31) == __ffs(grp) - 1) {
+        atomicMin(bmin + bin + kBins, gmin);
+        atomicMax(bmax + bin + kBins, gmax);
+      }
+    }
+  }
+  (void)r_first;
+}
+
+// clusters of row offsets -> x windows (<= kMaxWin, <= kMaxWinElems staged)
+static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
+  m->xwin = XWin{};
+  if (m->n_rows == 0 || m->nnz == 0 || m->n_cols > 0x7fffffffLL) return PBS_OK;
+  cudaStream_t s = ctx->stream;
+  int *bmin = nullptr, *bmax = nullptr, *wide = nullptr;
+  CK(cudaMalloc(&bmin, sizeof(int) * 2 * kBins));
+  CK(cudaMalloc(&bmax, sizeof(int) * 2 * kBins));
+  CK(cudaMalloc(&wide, sizeof(int)));
+  std::vector<int> hmin(2 * kBins, 0x7fffffff), hmax(2 * kBins, (int)0x80000000);
+  CK(cudaMemcpyAsync(bmin, hmin.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(bmax, hmax.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(wide, 0, sizeof(int), s));
+  offset_bins_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->rp, m->ci, m->n_rows, bmin, bmax, wide);
+  int hwide = 0;
+  CK(cudaMemcpyAsync(hmin.data(), bmin, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(hmax.data(), bmax, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  cudaFree(bmin);
+  cudaFree(bmax);
+  cudaFree(wide);
+  if (hwide) return PBS_OK;
+  std::vector<std::pair<int, int>> cl;  // [min, max] offsets
+  for (int b = 0; b < 2 * kBins; ++b) {
+    if (hmin[b] > hmax[b]) continue;
+    if (!cl.empty() && (long long)hmin[b] - cl.back().second <= kPipeRows + 4)
+      cl.back().second = hmax[b] > cl.back().second ? hmax[b] : cl.back().second;
+    else
+      cl.push_back({hmin[b], hmax[b]});
+  }
+  while (cl.size() > (size_t)kMaxWin) {  // merge across the smallest gap
+    size_t best = 0;
+    long long gap = -1;
+    for (size_t i = 0; i + 1 < cl.size(); ++i) {
+      long long g = (long long)cl[i + 1].first - cl[i].second;
+      if (gap < 0 || g < gap) {
+        gap = g;
+        best = i;
+      }
+    }
+    cl[best].second = cl[best + 1].second;
+    cl.erase(cl.begin() + best + 1);
+  }
+  XWin W{};
+  long long total = 0;
+  for (size_t c = 0; c < cl.size(); ++c) {
+    W.wmin[c] = cl[c].first;
+    W.wmax[c] = cl[c].second;
+    long long cap = (long long)kPipeRows + cl[c].second - cl[c].first + 4;
+    cap = (cap + 1) & ~1LL;
+    W.cap[c] = (int)cap;
+    total += cap;
+  }
+  if (total > kMaxWinElems || cl.empty()) return PBS_OK;  // too spread: gather mode
+  W.nwin = (int)cl.size();
+  W.total = (int)total;
+  m->xwin = W;
+  return PBS_OK;
+}
+
 PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
                               const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
                               const double* values, pbs_mat** out) {
@@ -873,6 +969,11 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
     }
   }
   CK(cudaStreamSynchronize(s));
+  int rc = compute_xwin(ctx, m);
+  if (rc) {
+    pbs_mat_free(m);
+    return rc;
+  }
   *out = m;
   return PBS_OK;
 }

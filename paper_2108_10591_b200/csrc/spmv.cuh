@@ -4,13 +4,16 @@
 // where in[] holds the row's values of the epilogue's kIn input vectors.
 //
 //  * csr_pipe_kernel — CSR, warp-specialised and TMA-fed.  One CTA per SM:
-//    a producer warp streams each 256-row block's slice of row_ptr and its
-//    contiguous nonzero range of values / int32 col_idx (in <=2048-nonzero
-//    chunks) into a ring of shared-memory stages with 1-D bulk async copies
-//    (cp.async.bulk, completion on mbarriers); eight consumer warps own one
-//    row each per block, prefetch the epilogue's row inputs with coalesced
-//    loads, gather x (L1-cached) and accumulate the row sequentially in
-//    ascending column order
+//    a producer warp streams, per 256-row block, the row_ptr slice, the x
+//    windows the block's columns fall in (offset clusters measured at upload:
+//    3 plane windows for a 3D stencil) and the epilogue's input segments into
+//    a ring of block slots, and the block's contiguous nonzero range of
+//    values / int32 col_idx (<=2048-nonzero chunks) into a ring of chunk
+//    stages — all with 1-D bulk async copies (cp.async.bulk, completion on
+//    mbarriers).  Eight consumer warps own one row each per block, read x and
+//    everything else from shared memory (global gathers only for matrices
+//    whose offsets are too spread to window) and accumulate the row
+//    sequentially in ascending column order
 //    (kernels.py:95-100), so the product is bitwise the reference's while HBM
 //    sees every matrix byte once with the copy engine keeping it busy.
 //  * stencil_spmv_kernel — matrix-free constant-coefficient stencil, one
@@ -39,6 +42,7 @@ struct CsrView {
   const int* ci;
   const double* v;
   long long row_lo, row_hi;
+  long long n_cols;
 };
 
 struct StencilView {
@@ -271,30 +275,60 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
 // --------------------------------------------------- CSR pipelined engine
 
 constexpr int kPipeRows = 256;        // rows per block = consumer threads
-constexpr int kPipeChunk = 2048;      // nonzeros per stage
+constexpr int kPipeChunk = 2048;      // nonzeros per chunk stage
 constexpr int kConsumerWarps = kPipeRows / 32;
 constexpr int kPipeThreads = kPipeRows + 32;  // + one producer warp
 constexpr int kMaxStages = 8;
-
-struct PipeHdr {
-  long long r0, c0, c1;
-  int nr, first, last, dv, dci, dr;  // dv/dci/dr: 16-byte alignment shifts of v, ci, row slices
-};
+constexpr int kMaxWin = 4;            // x windows per row block
+constexpr int kMaxWinElems = 4096;    // staged x elements per row block (32 KiB)
 
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
 
-struct StageLayout {
-  static constexpr size_t hdr = 0;
-  static constexpr size_t rp = 128;
-  static constexpr size_t v = rp + align128(sizeof(long long) * (kPipeRows + 2));
+// x windows: every column of row i lies in one of [i + wmin[c], i + wmax[c]]
+// (offset clusters measured at upload); for a 256-row block starting at r0 the
+// producer stages x[r0 + wmin[c] .. r0 + 255 + wmax[c]] per cluster.  nwin = 0:
+// offsets too spread (e.g. wide random bands) -> gather x from global memory.
+struct XWin {
+  int nwin;
+  int wmin[kMaxWin], wmax[kMaxWin];
+  int cap[kMaxWin];  // staged elements reserved per cluster (even)
+  int total;         // sum of cap
+};
+
+struct BlockHdr {
+  long long r0, base, end;
+  int nr, dr, nch, pad;
+  long long ws[kMaxWin];  // first staged column per window (16-byte aligned)
+  long long we[kMaxWin];  // one past the last column that may be looked up
+};
+
+struct ChunkHdr {
+  long long c0, c1;
+  int dv, dci, last, pad;
+};
+
+// block slot: header, row_ptr slice, x windows, epilogue inputs
+struct BlockLayout {
+  size_t rp, xw, ein, bytes;
+  __host__ __device__ BlockLayout(int xw_total, int kin) {
+    rp = 256;
+    xw = rp + align128(sizeof(long long) * (kPipeRows + 2));
+    ein = xw + align128(sizeof(double) * (xw_total > 0 ? xw_total : 2));
+    bytes = ein + align128(sizeof(double) * (kPipeRows + 2) * (kin > 0 ? kin : 1));
+  }
+};
+
+// chunk stage: header, values, col_idx
+struct ChunkLayout {
+  static constexpr size_t v = 128;
   static constexpr size_t ci = v + align128(sizeof(double) * (kPipeChunk + 2));
   static constexpr size_t bytes = ci + align128(sizeof(int) * (kPipeChunk + 4));
 };
-constexpr size_t kPipeBarrierBytes = 256;
+constexpr size_t kPipeBarrierBytes = 512;
 
 template <class Epi>
 __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
-                                                                   Epi epi, int stages) {
+                                                                   Epi epi, XWin W, int bslots, int cstages) {
   __shared__ int go;
   if (threadIdx.x == 0) {
     go = epi.active();  // one gate decision per CTA
@@ -302,16 +336,23 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   }
   __syncthreads();
   if (!go) return;
-  using L = StageLayout;
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + kMaxStages;
-  unsigned char* stage0 = smem + kPipeBarrierBytes;
+  uint64_t* cfull = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* cempty = cfull + kMaxStages;
+  uint64_t* bfull = cempty + kMaxStages;
+  uint64_t* bempty = bfull + kMaxStages;
+  const BlockLayout BL(W.total, Epi::kIn);
+  unsigned char* blk0 = smem + kPipeBarrierBytes;
+  unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumerWarps);
+    for (int s = 0; s < cstages; ++s) {
+      mbar_init(&cfull[s], 1);
+      mbar_init(&cempty[s], kConsumerWarps);
+    }
+    for (int s = 0; s < bslots; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], kConsumerWarps);
     }
     fence_mbar_init();
   }
@@ -322,8 +363,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   if (warp == kConsumerWarps) {
     // ----------------------------------------------------------- producer
     if (lane != 0) return;
-    int s = 0;
-    uint32_t ph = 0;
+    int cs = 0, bs = 0;
+    uint32_t cph = 0, bph = 0;
     for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
       const long long r0 = A.row_lo + blk * kPipeRows;
       const long long r0a = r0 & ~1LL;
@@ -331,37 +372,70 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       const int dr = (int)(r0 - r0a);
       const long long base = __ldg(A.rp + r0), end = __ldg(A.rp + r0 + nr);
       const long long nch = end > base ? (end - base + kPipeChunk - 1) / kPipeChunk : 1;
+      // block slot: row_ptr slice, x windows, epilogue inputs
+      mbar_wait(&bempty[bs], bph ^ 1);
+      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+      BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
+      bh->r0 = r0;
+      bh->base = base;
+      bh->end = end;
+      bh->nr = nr;
+      bh->dr = dr;
+      bh->nch = (int)nch;
+      const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
+      const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
+      uint32_t total = brp + Epi::kIn * bin;
+      uint32_t wbytes[kMaxWin];
+      int soff = 0;
+      for (int c = 0; c < W.nwin; ++c) {
+        long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
+        if (lo < 0) lo = 0;
+        if (hi > A.n_cols) hi = A.n_cols;
+        if (hi < lo) hi = lo;
+        const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
+        bh->ws[c] = loa;
+        bh->we[c] = hi;
+        wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
+        total += wbytes[c];
+        soff += W.cap[c];
+      }
+      mbar_arrive_expect_tx(&bfull[bs], total);
+      bulk_g2s(bst + BL.rp, A.rp + r0a, brp, &bfull[bs]);
+      soff = 0;
+      for (int c = 0; c < W.nwin; ++c) {
+        if (wbytes[c]) bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + bh->ws[c], wbytes[c], &bfull[bs]);
+        soff += W.cap[c];
+      }
+#pragma unroll
+      for (int e = 0; e < Epi::kIn; ++e)
+        bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
+      if (++bs == bslots) {
+        bs = 0;
+        bph ^= 1;
+      }
+      // chunk stages: the block's nonzero range
       for (long long c = 0; c < nch; ++c) {
-        mbar_wait(&empty[s], ph ^ 1);
-        unsigned char* st = stage0 + (size_t)s * L::bytes;
+        mbar_wait(&cempty[cs], cph ^ 1);
+        unsigned char* st = chk0 + (size_t)cs * ChunkLayout::bytes;
         const long long c0 = base + c * kPipeChunk;
         const long long c1 = min(end, c0 + kPipeChunk);
         const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
         const long long c0b = c0 & ~3LL, c1b = (c1 + 3) & ~3LL;
-        PipeHdr* h = reinterpret_cast<PipeHdr*>(st + L::hdr);
-        h->r0 = r0;
+        ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
         h->c0 = c0;
         h->c1 = c1;
-        h->nr = nr;
-        h->first = c == 0;
-        h->last = c == nch - 1;
         h->dv = (int)(c0 - c0a);
         h->dci = (int)(c0 - c0b);
-        h->dr = dr;
+        h->last = c == nch - 1;
         const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
         const uint32_t bc = (uint32_t)((c1b - c0b) * sizeof(int));
-        uint32_t total = bv + bc;
-        const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
-        if (c == 0) total += brp;
-        mbar_arrive_expect_tx(&full[s], total);
-        if (bv) bulk_g2s(st + L::v, A.v + c0a, bv, &full[s]);
-        if (bc) bulk_g2s(st + L::ci, A.ci + c0b, bc, &full[s]);
-        if (c == 0) {
-          bulk_g2s(st + L::rp, A.rp + r0a, brp, &full[s]);
-        }
-        if (++s == stages) {
-          s = 0;
-          ph ^= 1;
+        mbar_arrive_expect_tx(&cfull[cs], bv + bc);
+        if (bv) bulk_g2s(st + ChunkLayout::v, A.v + c0a, bv, &cfull[cs]);
+        if (bc) bulk_g2s(st + ChunkLayout::ci, A.ci + c0b, bc, &cfull[cs]);
+        if (!bv && !bc) mbar_arrive(&cfull[cs]);  // keep the phase moving (unreachable: bc >= 16)
+        if (++cs == cstages) {
+          cs = 0;
+          cph ^= 1;
         }
       }
     }
@@ -372,33 +446,41 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   Epi e = epi;
   e.init();
   const int t = threadIdx.x;
-  int s = 0;
-  uint32_t ph = 0;
+  int cs = 0, bs = 0;
+  uint32_t cph = 0, bph = 0;
   for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
-    double acc = 0.0;
-    long long my_s = 0, my_e = 0, r0 = 0;
-    int nr = 0;
-    double inr[Epi::kIn > 0 ? Epi::kIn : 1];
-    for (;;) {
-      mbar_wait(&full[s], ph);
-      const unsigned char* st = stage0 + (size_t)s * L::bytes;
-      const PipeHdr h = *reinterpret_cast<const PipeHdr*>(st + L::hdr);
-      if (h.first) {
-        r0 = h.r0;
-        nr = h.nr;
-        if (t < nr) {
-          // epilogue inputs: coalesced loads issued now, consumed after the row
-          // sum, so their latency hides behind the x gathers
+    mbar_wait(&bfull[bs], bph);
+    const unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+    const BlockHdr* bhp = reinterpret_cast<const BlockHdr*>(bst);
+    const int nr = bhp->nr, dr = bhp->dr;
+    const long long r0 = bhp->r0;
+    long long my_s = 0, my_e = 0;
+    if (t < nr) {
+      const long long* rps = reinterpret_cast<const long long*>(bst + BL.rp);
+      my_s = rps[t + dr];
+      my_e = rps[t + dr + 1];
+    }
+    // x lookup: window c holds x[ws[c] ...] at staged offset soff[c], so
+    // x[col] = xw[col - wsb[c]] for the last window with ws[c] <= col
+    const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
+    int wsv[kMaxWin], wsb[kMaxWin];
+    {
+      int soff = 0;
 #pragma unroll
-          for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][r0 + t];
-          const long long* rps = reinterpret_cast<const long long*>(st + L::rp);
-          my_s = rps[t + h.dr];
-          my_e = rps[t + h.dr + 1];
-        }
+      for (int c = 0; c < kMaxWin; ++c) {
+        wsv[c] = c < W.nwin ? (int)bhp->ws[c] : 0x7fffffff;
+        wsb[c] = c < W.nwin ? (int)bhp->ws[c] - soff : 0;
+        soff += c < W.nwin ? W.cap[c] : 0;
       }
+    }
+    double acc = 0.0;
+    for (long long c = 0;; ++c) {
+      mbar_wait(&cfull[cs], cph);
+      const unsigned char* st = chk0 + (size_t)cs * ChunkLayout::bytes;
+      const ChunkHdr h = *reinterpret_cast<const ChunkHdr*>(st);
       if (t < nr) {
-        const double* vs = reinterpret_cast<const double*>(st + L::v) + h.dv - h.c0;
-        const int* cs = reinterpret_cast<const int*>(st + L::ci) + h.dci - h.c0;
+        const double* vs = reinterpret_cast<const double*>(st + ChunkLayout::v) + h.dv - h.c0;
+        const int* cis = reinterpret_cast<const int*>(st + ChunkLayout::ci) + h.dci - h.c0;
         const long long lo = max(my_s, h.c0), hi = min(my_e, h.c1);
         constexpr int U = Epi::kGatherBatch;
         for (long long k = lo; k < hi; k += U) {
@@ -406,8 +488,17 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
 #pragma unroll
           for (int u = 0; u < U; ++u)
             if (k + u < hi) {
+              const int col = cis[k + u];
               vv[u] = vs[k + u];
-              xv[u] = __ldg(x + cs[k + u]);
+              if (W.nwin) {
+                int b = wsb[0];
+#pragma unroll
+                for (int cc = 1; cc < kMaxWin; ++cc)
+                  if (col >= wsv[cc]) b = wsb[cc];
+                xv[u] = xw[col - b];
+              } else {
+                xv[u] = __ldg(x + col);
+              }
             }
 #pragma unroll
           for (int u = 0; u < U; ++u)
@@ -415,14 +506,26 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      if (++s == stages) {
-        s = 0;
-        ph ^= 1;
+      if (lane == 0) mbar_arrive(&cempty[cs]);
+      if (++cs == cstages) {
+        cs = 0;
+        cph ^= 1;
       }
       if (h.last) break;
     }
-    if (t < nr) e.row(r0 + t, acc, inr);
+    if (t < nr) {
+      double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+      const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
+#pragma unroll
+      for (int k = 0; k < Epi::kIn; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+      e.row(r0 + t, acc, inr);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bempty[bs]);
+    if (++bs == bslots) {
+      bs = 0;
+      bph ^= 1;
+    }
   }
   e.template finish<kPipeRows, true>();
 }
