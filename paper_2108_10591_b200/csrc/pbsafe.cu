@@ -234,6 +234,7 @@ struct Launcher {
   Workspace* trace_ws = nullptr;
   long long iter = 0;
   int trace_rc = 0;
+  int err = 0;  // first launch-configuration failure (sticky)
   void trace_point();
   void done(int kind) {
     ++launches;
@@ -276,7 +277,7 @@ static int pipe_ctas_per_sm() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PBS_PIPE_CTAS");
-    v = e ? atoi(e) : 2;
+    v = e ? atoi(e) : 1;
     if (v < 1) v = 1;
     if (v > 4) v = 4;
   }
@@ -284,19 +285,24 @@ static int pipe_ctas_per_sm() {
 }
 
 template <class Epi>
-static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem) {
+static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem, int* ctas) {
   const BlockLayout BL(W.total, Epi::kIn);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  // per-CTA budget: the SM's shared memory split between the resident CTAs,
-  // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
-  size_t budget = (size_t)per_sm / pipe_ctas_per_sm() - 1024 - 2048;
-  if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
-  budget -= kPipeBarrierBytes;
-  int n = (int)(budget / (BL.bytes + ChunkLayout::bytes));
-  if (n > 4) n = 4;
+  int n = 0, c = pipe_ctas_per_sm();
+  for (; c >= 1; --c) {
+    // per-CTA budget: the SM's shared memory split between the resident CTAs,
+    // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
+    size_t budget = (size_t)per_sm / c - 1024 - 2048;
+    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
+    budget -= kPipeBarrierBytes;
+    n = (int)(budget / (BL.bytes + ChunkLayout::bytes));
+    if (n > 4) n = 4;
+    if (n >= 2) break;
+  }
   if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
+  *ctas = c;
   *bslots = n;
   *cstages = n;
   *smem = kPipeBarrierBytes + (size_t)n * (BL.bytes + ChunkLayout::bytes);
@@ -317,10 +323,14 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   int grid;
   if (!m->stencil) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
-    int bslots, cstages;
+    int bslots, cstages, ctas;
     size_t smem;
-    if (pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem)) return 0;
-    const long long cap = (long long)L.ctx->sms * pipe_ctas_per_sm();
+    int rc = pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem, &ctas);
+    if (rc) {
+      L.err = rc;
+      return 0;
+    }
+    const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages);
   } else {
@@ -557,6 +567,10 @@ static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const M
   CK(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
   fn(L, ws, md);
   cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+  if (L.err) {
+    if (e == cudaSuccess) cudaGraphDestroy(g);
+    return L.err;
+  }
   if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
   cudaGraphExec_t ge;
   e = cudaGraphInstantiate(&ge, g, 0);
@@ -638,6 +652,7 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   if (L.timing) marks.push_back({-1, ws->ev0});
   if (pipelined) {
     setup_pipelined(L, ws, md);
+    if (L.err) return L.err;
   } else {
     spmv_launch(L, ws->V.v[VX], epi_resid(ws, true), 0, n, KS);
   }
@@ -679,6 +694,7 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
         L.iter = j;
         fn(L, ws, md);
         if (L.trace_rc) return L.trace_rc;
+        if (L.err) return L.err;
       }
     }
   }
@@ -1071,6 +1087,7 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
   e.st = ctx->tmp_state;
   e.tag = PBS_TAG_AX;
   spmv_launch(L, d_x, e, 0, m->n_rows, KS);
+  if (L.err) return L.err;
   unsigned long long row = 0;
   CK(cudaMemcpyAsync(&row, &ctx->tmp_state->nf_row, sizeof(row), cudaMemcpyDeviceToHost, ctx->stream));
   CK(cudaStreamSynchronize(ctx->stream));
@@ -1202,6 +1219,7 @@ PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in
       spmv_launch(L, V[VW], epi_k3(ws, nm, 0), 0, ws->n, KK3);
     }
   }
+  if (L.err) return L.err;
   for (int k = 0; k < 16; ++k)
     CK(cudaMemcpyAsync(d_state[k], ws->V.v[order[k]], bytes, cudaMemcpyDeviceToDevice, s));
   SolverState out;
@@ -1276,6 +1294,7 @@ PBS_EXPORT int pbs_k_spmv_range(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, co
   EpiStore e{};
   e.y = d_y;
   spmv_launch(L, d_x, e, lo, hi, KS);
+  if (L.err) return L.err;
   CK(cudaMemcpyAsync(out + lo, d_y + lo, sizeof(double) * (hi - lo), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());

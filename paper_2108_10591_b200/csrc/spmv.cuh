@@ -299,7 +299,6 @@ struct BlockHdr {
   long long r0, base, end;
   int nr, dr, nch, pad;
   long long ws[kMaxWin];  // first staged column per window (16-byte aligned)
-  long long we[kMaxWin];  // one past the last column that may be looked up
 };
 
 struct ChunkHdr {
@@ -362,53 +361,77 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
 
   if (warp == kConsumerWarps) {
     // ----------------------------------------------------------- producer
-    if (lane != 0) return;
+    // The whole warp: row-block bounds for the next 32 blocks come from one
+    // warp-wide load (no dependent load per block), and the block's bulk
+    // copies are issued by different lanes in parallel.
     int cs = 0, bs = 0;
     uint32_t cph = 0, bph = 0;
-    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    long long pf_base = 0, pf_end = 0;
+    for (long long blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
+      const int slot = (int)(q & 31);
+      if (slot == 0) {  // prefetch bounds of blocks q .. q+31 of this CTA
+        const long long b2 = blk + (long long)lane * gridDim.x;
+        if (b2 < nblk) {
+          const long long rr0 = A.row_lo + b2 * kPipeRows;
+          const long long rr1 = min(A.row_hi, rr0 + kPipeRows);
+          pf_base = __ldg(A.rp + rr0);
+          pf_end = __ldg(A.rp + rr1);
+        }
+      }
+      const long long base = __shfl_sync(0xffffffffu, pf_base, slot);
+      const long long end = __shfl_sync(0xffffffffu, pf_end, slot);
       const long long r0 = A.row_lo + blk * kPipeRows;
       const long long r0a = r0 & ~1LL;
       const int nr = (int)min((long long)kPipeRows, A.row_hi - r0);
       const int dr = (int)(r0 - r0a);
-      const long long base = __ldg(A.rp + r0), end = __ldg(A.rp + r0 + nr);
       const long long nch = end > base ? (end - base + kPipeChunk - 1) / kPipeChunk : 1;
-      // block slot: row_ptr slice, x windows, epilogue inputs
-      mbar_wait(&bempty[bs], bph ^ 1);
-      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
-      BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
-      bh->r0 = r0;
-      bh->base = base;
-      bh->end = end;
-      bh->nr = nr;
-      bh->dr = dr;
-      bh->nch = (int)nch;
       const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
       const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
-      uint32_t total = brp + Epi::kIn * bin;
+      // x windows of this block (every lane computes them; lane 1+c copies window c)
+      long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      int soff = 0;
-      for (int c = 0; c < W.nwin; ++c) {
-        long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
-        if (lo < 0) lo = 0;
-        if (hi > A.n_cols) hi = A.n_cols;
-        if (hi < lo) hi = lo;
-        const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
-        bh->ws[c] = loa;
-        bh->we[c] = hi;
-        wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
-        total += wbytes[c];
-        soff += W.cap[c];
-      }
-      mbar_arrive_expect_tx(&bfull[bs], total);
-      bulk_g2s(bst + BL.rp, A.rp + r0a, brp, &bfull[bs]);
-      soff = 0;
-      for (int c = 0; c < W.nwin; ++c) {
-        if (wbytes[c]) bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + bh->ws[c], wbytes[c], &bfull[bs]);
-        soff += W.cap[c];
-      }
+      uint32_t total = brp + Epi::kIn * bin;
 #pragma unroll
-      for (int e = 0; e < Epi::kIn; ++e)
+      for (int c = 0; c < kMaxWin; ++c) {
+        wlo[c] = 0x7fffffff;
+        wbytes[c] = 0;
+        if (c < W.nwin) {
+          long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
+          if (lo < 0) lo = 0;
+          if (hi > A.n_cols) hi = A.n_cols;
+          if (hi < lo) hi = lo;
+          const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
+          wlo[c] = loa;
+          wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
+          total += wbytes[c];
+        }
+      }
+      mbar_wait(&bempty[bs], bph ^ 1);
+      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+      if (lane == 0) {
+        BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
+        bh->r0 = r0;
+        bh->base = base;
+        bh->end = end;
+        bh->nr = nr;
+        bh->dr = dr;
+        bh->nch = (int)nch;
+#pragma unroll
+        for (int c = 0; c < kMaxWin; ++c) bh->ws[c] = wlo[c];
+        mbar_arrive_expect_tx(&bfull[bs], total);
+      }
+      __syncwarp();
+      if (lane == 0) {
+        bulk_g2s(bst + BL.rp, A.rp + r0a, brp, &bfull[bs]);
+      } else if (lane <= W.nwin) {
+        const int c = lane - 1;
+        int soff = 0;
+        for (int cc = 0; cc < c; ++cc) soff += W.cap[cc];
+        if (wbytes[c]) bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[c], wbytes[c], &bfull[bs]);
+      } else if (lane >= 8 && lane < 8 + Epi::kIn) {
+        const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
+      }
       if (++bs == bslots) {
         bs = 0;
         bph ^= 1;
@@ -421,18 +444,20 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         const long long c1 = min(end, c0 + kPipeChunk);
         const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
         const long long c0b = c0 & ~3LL, c1b = (c1 + 3) & ~3LL;
-        ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
-        h->c0 = c0;
-        h->c1 = c1;
-        h->dv = (int)(c0 - c0a);
-        h->dci = (int)(c0 - c0b);
-        h->last = c == nch - 1;
         const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
         const uint32_t bc = (uint32_t)((c1b - c0b) * sizeof(int));
-        mbar_arrive_expect_tx(&cfull[cs], bv + bc);
-        if (bv) bulk_g2s(st + ChunkLayout::v, A.v + c0a, bv, &cfull[cs]);
-        if (bc) bulk_g2s(st + ChunkLayout::ci, A.ci + c0b, bc, &cfull[cs]);
-        if (!bv && !bc) mbar_arrive(&cfull[cs]);  // keep the phase moving (unreachable: bc >= 16)
+        if (lane == 0) {
+          ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
+          h->c0 = c0;
+          h->c1 = c1;
+          h->dv = (int)(c0 - c0a);
+          h->dci = (int)(c0 - c0b);
+          h->last = c == nch - 1;
+          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
+        }
+        __syncwarp();
+        if (lane == 0 && bv) bulk_g2s(st + ChunkLayout::v, A.v + c0a, bv, &cfull[cs]);
+        if (lane == 1 && bc) bulk_g2s(st + ChunkLayout::ci, A.ci + c0b, bc, &cfull[cs]);
         if (++cs == cstages) {
           cs = 0;
           cph ^= 1;
