@@ -120,6 +120,7 @@ OR_API int64_t or_plan_balanced(int64_t n, int64_t workers, int64_t* bounds) {
 typedef struct {
   int64_t workers;
   int64_t* bounds;
+  int compensated; /* near-exact dots instead of the plan's chains */
 } or_plan;
 
 /* Near-exact dot over [lo, hi): double-double accumulation with exact
@@ -159,12 +160,11 @@ static double dot_compensated(const double* x, const double* y, int64_t lo, int6
   return acc.hi + acc.lo;
 }
 
-static int g_compensated = 0;
 
 /* reduction.py:282-294: per range sequential partials, left-to-right combine */
 static void plan_batch(const or_plan* P, int npairs, const double* const* xs,
                        const double* const* ys, double* out) {
-  if (g_compensated) {
+  if (P->compensated) {
 #pragma omp parallel for schedule(dynamic, 1)
     for (int p = 0; p < npairs; ++p) out[p] = dot_compensated(xs[p], ys[p], 0, P->bounds[P->workers]);
     return;
@@ -196,6 +196,7 @@ OR_API double or_plan_dot(int64_t workers, int64_t n, const double* x, const dou
   or_plan P;
   P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(workers + 2));
   P.workers = or_plan_balanced(n, workers, P.bounds);
+  P.compensated = 0;
   double d = plan_dot(&P, x, y);
   free(P.bounds);
   return d;
@@ -372,7 +373,6 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   if (cfg->threads > 0) omp_set_num_threads(cfg->threads);
 #endif
   memset(res, 0, sizeof(*res));
-  g_compensated = cfg->workers < 0;  /* workers < 0: near-exact dots (order-free yardstick) */
   res->failure_iter = -1;
   res->nonfinite_index = -1;
   mat_t A = {n, rp, ci, v, res};
@@ -380,6 +380,7 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;
   P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(wk + 2));
   P.workers = or_plan_balanced(n, wk, P.bounds);
+  P.compensated = cfg->workers < 0; /* workers < 0: near-exact dots (order-free yardstick) */
   hist_t H = {hist_rel, hist_replaced, hist_coef, hist_has_coef, 0};
   const int pipelined = cfg->method != M_SSBICGSAFE2;
   const int replace_residuals = cfg->method == M_PBICGSAFE_RR;

@@ -271,22 +271,33 @@ void Launcher::trace_point() {
   trace_cfg->trace_fn(iter, ptrs, trace_cfg->trace_user);
 }
 
-// pipelined CSR engine: CTAs per SM (PBS_PIPE_CTAS, default 2) and the stage
-// count that fills the shared memory those CTAs share
+// pipelined CSR engine knobs (env overrides for tuning sweeps):
+//   PBS_PIPE_CTAS    CTAs per SM tried first (falls back while slots do not fit)
+//   PBS_PIPE_CHUNK   nonzeros per chunk stage
+//   PBS_PIPE_SLOTS   block slots = chunk stages (cap)
+static int env_int(const char* name, int dflt, int lo, int hi) {
+  const char* e = getenv(name);
+  int v = e ? atoi(e) : dflt;
+  return v < lo ? lo : (v > hi ? hi : v);
+}
 static int pipe_ctas_per_sm() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PBS_PIPE_CTAS");
-    v = e ? atoi(e) : 1;
-    if (v < 1) v = 1;
-    if (v > 4) v = 4;
-  }
+  static int v = env_int("PBS_PIPE_CTAS", 2, 1, 4);
+  return v;
+}
+static int pipe_chunk() {
+  static int v = env_int("PBS_PIPE_CHUNK", 1024, 256, kPipeChunkMax) & ~3;
+  return v;
+}
+static int pipe_slots_cap() {
+  static int v = env_int("PBS_PIPE_SLOTS", 4, 2, kMaxStages);
   return v;
 }
 
 template <class Epi>
-static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem, int* ctas) {
+static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem, int* ctas,
+                       int* chunk) {
   const BlockLayout BL(W.total, Epi::kIn);
+  const ChunkLayout CL(pipe_chunk());
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
@@ -297,15 +308,16 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, s
     size_t budget = (size_t)per_sm / c - 1024 - 2048;
     if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
     budget -= kPipeBarrierBytes;
-    n = (int)(budget / (BL.bytes + ChunkLayout::bytes));
-    if (n > 4) n = 4;
+    n = (int)(budget / (BL.bytes + CL.bytes));
+    if (n > pipe_slots_cap()) n = pipe_slots_cap();
     if (n >= 2) break;
   }
   if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
   *ctas = c;
   *bslots = n;
   *cstages = n;
-  *smem = kPipeBarrierBytes + (size_t)n * (BL.bytes + ChunkLayout::bytes);
+  *chunk = pipe_chunk();
+  *smem = kPipeBarrierBytes + (size_t)n * (BL.bytes + CL.bytes);
   const void* k = (const void*)csr_pipe_kernel<Epi>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
@@ -323,16 +335,16 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   int grid;
   if (!m->stencil) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
-    int bslots, cstages, ctas;
+    int bslots, cstages, ctas, chunk;
     size_t smem;
-    int rc = pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem, &ctas);
+    int rc = pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem, &ctas, &chunk);
     if (rc) {
       L.err = rc;
       return 0;
     }
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
-    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages);
+    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages, chunk);
   } else {
     StencilView S = m->sv;
     S.row_lo = lo;

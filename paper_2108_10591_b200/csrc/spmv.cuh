@@ -275,7 +275,7 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
 // --------------------------------------------------- CSR pipelined engine
 
 constexpr int kPipeRows = 256;        // rows per block = consumer threads
-constexpr int kPipeChunk = 2048;      // nonzeros per chunk stage
+constexpr int kPipeChunkMax = 4096;   // nonzeros per chunk stage (runtime <= this)
 constexpr int kConsumerWarps = kPipeRows / 32;
 constexpr int kPipeThreads = kPipeRows + 32;  // + one producer warp
 constexpr int kMaxStages = 8;
@@ -317,17 +317,21 @@ struct BlockLayout {
   }
 };
 
-// chunk stage: header, values, col_idx
+// chunk stage: header, values, col_idx (ch nonzeros)
 struct ChunkLayout {
-  static constexpr size_t v = 128;
-  static constexpr size_t ci = v + align128(sizeof(double) * (kPipeChunk + 2));
-  static constexpr size_t bytes = ci + align128(sizeof(int) * (kPipeChunk + 4));
+  size_t v, ci, bytes;
+  __host__ __device__ ChunkLayout(int ch) {
+    v = 128;
+    ci = v + align128(sizeof(double) * (ch + 2));
+    bytes = ci + align128(sizeof(int) * (ch + 4));
+  }
 };
 constexpr size_t kPipeBarrierBytes = 512;
 
 template <class Epi>
 __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
-                                                                   Epi epi, XWin W, int bslots, int cstages) {
+                                                                   Epi epi, XWin W, int bslots, int cstages,
+                                                                   int chunk) {
   __shared__ int go;
   if (threadIdx.x == 0) {
     go = epi.active();  // one gate decision per CTA
@@ -341,6 +345,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
   const BlockLayout BL(W.total, Epi::kIn);
+  const ChunkLayout CL(chunk);
   unsigned char* blk0 = smem + kPipeBarrierBytes;
   unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -384,7 +389,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       const long long r0a = r0 & ~1LL;
       const int nr = (int)min((long long)kPipeRows, A.row_hi - r0);
       const int dr = (int)(r0 - r0a);
-      const long long nch = end > base ? (end - base + kPipeChunk - 1) / kPipeChunk : 1;
+      const long long nch = end > base ? (end - base + chunk - 1) / chunk : 1;
       const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
       const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
       // x windows of this block (every lane computes them; lane 1+c copies window c)
@@ -439,9 +444,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       // chunk stages: the block's nonzero range
       for (long long c = 0; c < nch; ++c) {
         mbar_wait(&cempty[cs], cph ^ 1);
-        unsigned char* st = chk0 + (size_t)cs * ChunkLayout::bytes;
-        const long long c0 = base + c * kPipeChunk;
-        const long long c1 = min(end, c0 + kPipeChunk);
+        unsigned char* st = chk0 + (size_t)cs * CL.bytes;
+        const long long c0 = base + c * chunk;
+        const long long c1 = min(end, c0 + chunk);
         const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
         const long long c0b = c0 & ~3LL, c1b = (c1 + 3) & ~3LL;
         const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
@@ -456,8 +461,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
           mbar_arrive_expect_tx(&cfull[cs], bv + bc);
         }
         __syncwarp();
-        if (lane == 0 && bv) bulk_g2s(st + ChunkLayout::v, A.v + c0a, bv, &cfull[cs]);
-        if (lane == 1 && bc) bulk_g2s(st + ChunkLayout::ci, A.ci + c0b, bc, &cfull[cs]);
+        if (lane == 0 && bv) bulk_g2s(st + CL.v, A.v + c0a, bv, &cfull[cs]);
+        if (lane == 1 && bc) bulk_g2s(st + CL.ci, A.ci + c0b, bc, &cfull[cs]);
         if (++cs == cstages) {
           cs = 0;
           cph ^= 1;
@@ -501,11 +506,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
     double acc = 0.0;
     for (long long c = 0;; ++c) {
       mbar_wait(&cfull[cs], cph);
-      const unsigned char* st = chk0 + (size_t)cs * ChunkLayout::bytes;
+      const unsigned char* st = chk0 + (size_t)cs * CL.bytes;
       const ChunkHdr h = *reinterpret_cast<const ChunkHdr*>(st);
       if (t < nr) {
-        const double* vs = reinterpret_cast<const double*>(st + ChunkLayout::v) + h.dv - h.c0;
-        const int* cis = reinterpret_cast<const int*>(st + ChunkLayout::ci) + h.dci - h.c0;
+        const double* vs = reinterpret_cast<const double*>(st + CL.v) + h.dv - h.c0;
+        const int* cis = reinterpret_cast<const int*>(st + CL.ci) + h.dci - h.c0;
         const long long lo = max(my_s, h.c0), hi = min(my_e, h.c1);
         constexpr int U = Epi::kGatherBatch;
         for (long long k = lo; k < hi; k += U) {

@@ -21,7 +21,8 @@ def main():
     n = A.n_rows
     r0s = b.copy()
     coef = g["coef"]
-    for i in range(0, 5):
+    for mode in (0, 1):
+     for i in range(0, 13):
         j = i + 1
         st = {k: g[f"it{i}_{k}"] for k in ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l")}
         st.update(r0s=r0s, b=b, As=np.zeros(n))
@@ -33,16 +34,16 @@ def main():
         ptrs = (C.c_void_p * 16)(*[t.data_ptr() for t in dev])
         sin = np.array([j, coef[i, 0], coef[i, 2], f_prev, float(g["r0_norm"]), 0.0])
         sout = np.zeros(14)
-        _lib.check(_lib.load().pbs_step_dev(dm.handle, ptrs, sin.ctypes.data_as(C.c_void_p), 1, 1,
+        _lib.check(_lib.load().pbs_step_dev(dm.handle, ptrs, sin.ctypes.data_as(C.c_void_p), mode, 1,
                                             sout.ctypes.data_as(C.c_void_p)), dm.ctx.handle)
         s, y, r, t = st["s"], st["y"], st["r"], st["t"]
         pairs = [(s, s), (y, y), (s, y), (s, r), (y, r), (r0s, r), (r0s, s), (r0s, t), (r, r)]
         ref_d = np.array([orc.plan_dot(a, bb, 1) for a, bb in pairs])
-        print("step", j, "dots equal", np.array_equal(sout[4:13], ref_d), "coef gpu", sout[:4].tolist(),
-              "golden", coef[j].tolist(), "diff", (sout[:4] - coef[j]).tolist())
-        q, ab = orc.alpha_beta_safe(ref_d[5], f_prev, ref_d[6], ref_d[7], coef[i, 0], coef[i, 2], False)
+        q, al, be = orc.alpha_beta_safe(ref_d[5], f_prev, ref_d[6], ref_d[7], coef[i, 0], coef[i, 2], False)
         q2, z, e = orc.zeta_eta_safe(*ref_d[:5], False)
-        print("   oracle coef from same dots", ab, z, e)
+        print("mode", mode, "step", j, "dots==", np.array_equal(sout[4:13], ref_d), "coef-golden",
+              (sout[:4] - coef[j]).tolist(), "oracle(same dots)-golden", (np.array([al, be, z, e]) - coef[j]).tolist(),
+              "dot diffs", (sout[4:13] - ref_d).tolist() if not np.array_equal(sout[4:13], ref_d) else "")
         dm.free()
 
 

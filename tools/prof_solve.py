@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--method", default="pbicgsafe")
     ap.add_argument("--graphs", action="store_true")
     ap.add_argument("--repeat", type=int, default=1)
+    ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event breakdown")
     args = ap.parse_args()
     import torch
 
@@ -45,9 +46,15 @@ def main():
     bh = b.cpu().numpy()
     cfg = pb.SolverConfig(tol=1e-30, max_iters=args.iters)
     for _ in range(args.repeat):
-        out = pb.solve(dm, bh, method=args.method, config=cfg, engine=pb.DeviceEngine(use_graphs=args.graphs))
+        out = pb.solve(dm, bh, method=args.method, config=cfg,
+                       engine=pb.DeviceEngine(use_graphs=args.graphs, timing=args.timing))
+    extra = ""
+    if args.timing:
+        kc = out.device["kernel_count"]
+        extra = " | " + " ".join(f"{k}={v / max(kc[k], 1) * 1e3:.1f}us" for k, v in out.device["kernel_ms"].items() if kc[k])
     print(f"{args.config} {args.operator} {args.method}: {out.iterations} iterations, "
-          f"{out.device['device_ms']:.3f} ms, launches {out.device['kernel_launches']}")
+          f"{out.device['device_ms']:.3f} ms ({out.device['device_ms'] / max(out.iterations, 1) * 1e3:.1f} us/it), "
+          f"launches {out.device['kernel_launches']}{extra}")
 
 
 if __name__ == "__main__":
