@@ -121,35 +121,43 @@ __device__ __forceinline__ void block_bar() {
     __syncthreads();
 }
 
-// ---- double-double accumulation of the dot batch --------------------------
-// Each dot is carried as an unevaluated sum hi + lo (~106 bits): products are
-// split exactly (TwoProduct via fma), sums by TwoSum.  The rounded result
-// hi + lo is the correctly rounded dot in all but pathological cases, so the
-// batch no longer depends on the reduction order (iteration-
-// count parity).
+// ---- compensated accumulation of the dot batch --------------------------
+// Each dot is carried as a pair (p, s): p the running sum, s the running sum
+// of the exact rounding errors of every product (TwoProduct via fma) and of
+// every addition into p (TwoSum) — Ogita, Rump & Oishi's Dot2.  The result
+// p + s is as accurate as a dot computed in twice the working precision and
+// then rounded, i.e. (except in pathological cases) the correctly rounded
+// dot, so the batch no longer depends on the reduction order (DESIGN.md,
+// iteration-count parity).  Loop-carried dependencies are one add each.
 struct Ddbl {
-  double hi, lo;
+  double hi, lo;  // p, s
 };
 
-__device__ __forceinline__ Ddbl dd_add(Ddbl a, Ddbl b) {
-  const double s = add(a.hi, b.hi);
-  const double bb = sub(s, a.hi);
-  double e = add(sub(a.hi, sub(s, bb)), sub(b.hi, bb));
-  e = add(e, add(a.lo, b.lo));
-  const double hi = add(s, e);
-  return Ddbl{hi, sub(e, sub(hi, s))};
+__device__ __forceinline__ Ddbl two_sum(double a, double b) {
+  const double s = add(a, b);
+  const double bb = sub(s, a);
+  return Ddbl{s, add(sub(a, sub(s, bb)), sub(b, bb))};
 }
 
-__device__ __forceinline__ Ddbl dd_prod(double a, double b) {
-  const double p = mul(a, b);
-  return Ddbl{p, __fma_rn(a, b, -p)};
+// accumulate one product a*b into (p, s)
+__device__ __forceinline__ Ddbl dot2_step(Ddbl acc, double a, double b) {
+  const double h = mul(a, b);
+  const double r = __fma_rn(a, b, -h);
+  const Ddbl t = two_sum(acc.hi, h);
+  return Ddbl{t.hi, add(acc.lo, add(t.lo, r))};
+}
+
+// combine two partial pairs
+__device__ __forceinline__ Ddbl dd_add(Ddbl a, Ddbl b) {
+  const Ddbl t = two_sum(a.hi, b.hi);
+  return Ddbl{t.hi, add(add(a.lo, b.lo), t.lo)};
 }
 
 __device__ __forceinline__ Ddbl dd_shfl_xor(Ddbl v, int o) {
   return Ddbl{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
 }
 
-// Block-level reduction of 9 per-thread double-double partials into
+// Block-level reduction of 9 per-thread compensated partials into
 // out[2*j], out[2*j+1] (threads 0..8 write, then __threadfence so a last-CTA
 // reader sees them).  Fixed shape (xor-butterfly in warps, then warps in
 // index order): the result depends only on the data-to-thread mapping.

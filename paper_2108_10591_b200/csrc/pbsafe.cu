@@ -288,8 +288,16 @@ static int pipe_chunk() {
   static int v = env_int("PBS_PIPE_CHUNK", 1024, 256, kPipeChunkMax) & ~3;
   return v;
 }
+static int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-row CSR engine
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PBS_CSR_ENGINE");
+    v = (e && std::string(e) == "tpr") ? 1 : ((e && std::string(e) == "tprlate") ? 2 : 0);
+  }
+  return v;
+}
 static int pipe_slots_cap() {
-  static int v = env_int("PBS_PIPE_SLOTS", 4, 2, kMaxStages);
+  static int v = env_int("PBS_PIPE_SLOTS", 2, 2, kMaxStages);
   return v;
 }
 
@@ -333,7 +341,16 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   pbs_mat* m = L.m;
   long long nblk = (hi - lo + kThreads - 1) / kThreads;
   int grid;
-  if (!m->stencil) {
+  if (!m->stencil && csr_engine_tpr()) {
+    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
+    if (csr_engine_tpr() == 2) {
+      grid = grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, true>, nblk);
+      csr_tpr_kernel<Epi, true><<<grid, kThreads, 0, L.s>>>(A, x, epi);
+    } else {
+      grid = grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, false>, nblk);
+      csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
+    }
+  } else if (!m->stencil) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
     int bslots, cstages, ctas, chunk;
     size_t smem;

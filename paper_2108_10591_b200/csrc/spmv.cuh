@@ -62,17 +62,17 @@ struct Dots9 {
 #pragma unroll
     for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
   }
-  // _safe_batch pairs (solvers.py:471-481), double-double accumulation
+  // _safe_batch pairs (solvers.py:471-481), compensated (Dot2) accumulation
   __device__ void add_row(double s, double y, double r, double r0s, double t) {
-    acc[DA] = dd_add(acc[DA], dd_prod(s, s));
-    acc[DB] = dd_add(acc[DB], dd_prod(y, y));
-    acc[DC] = dd_add(acc[DC], dd_prod(s, y));
-    acc[DD] = dd_add(acc[DD], dd_prod(s, r));
-    acc[DE] = dd_add(acc[DE], dd_prod(y, r));
-    acc[DF] = dd_add(acc[DF], dd_prod(r0s, r));
-    acc[DG] = dd_add(acc[DG], dd_prod(r0s, s));
-    acc[DH] = dd_add(acc[DH], dd_prod(r0s, t));
-    acc[DR] = dd_add(acc[DR], dd_prod(r, r));
+    acc[DA] = dot2_step(acc[DA], s, s);
+    acc[DB] = dot2_step(acc[DB], y, y);
+    acc[DC] = dot2_step(acc[DC], s, y);
+    acc[DD] = dot2_step(acc[DD], s, r);
+    acc[DE] = dot2_step(acc[DE], y, r);
+    acc[DF] = dot2_step(acc[DF], r0s, r);
+    acc[DG] = dot2_step(acc[DG], r0s, s);
+    acc[DH] = dot2_step(acc[DH], r0s, t);
+    acc[DR] = dot2_step(acc[DR], r, r);
   }
 };
 
@@ -558,6 +558,63 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
     }
   }
   e.template finish<kPipeRows, true>();
+}
+
+// ------------------------------------------- CSR thread-per-row engine
+
+// One thread per row at full occupancy (no shared memory, so L1 keeps the
+// matrix sectors a warp's strided row loads share): each thread loads its
+// row's epilogue inputs first, then its nonzeros in batches of U (values,
+// col_idx, x gathers all in flight), and accumulates in ascending column
+// order — bitwise the reference's row sum.
+template <class Epi, bool LATE>
+__global__ void __launch_bounds__(kThreads, LATE ? 4 : 1) csr_tpr_kernel(CsrView A, const double* __restrict__ x,
+                                                                       Epi epi) {
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    go = epi.active();
+    if (!go && blockIdx.x == 0) epi.on_skip();
+  }
+  __syncthreads();
+  if (!go) return;
+  Epi e = epi;
+  e.init();
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = A.row_lo + (long long)blockIdx.x * kThreads + threadIdx.x; i < A.row_hi; i += stride) {
+    double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+    if (!LATE) {
+#pragma unroll
+      for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][i];
+    }
+    const long long s0 = __ldg(A.rp + i), s1 = __ldg(A.rp + i + 1);
+    const int len = (int)(s1 - s0);
+    const double* __restrict__ vr = A.v + s0;
+    const int* __restrict__ cr = A.ci + s0;
+    double acc = 0.0;
+    constexpr int U = 8;
+    for (int k = 0; k < len; k += U) {
+      double vv[U], xv[U];
+      int cc[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < len) {
+          vv[u] = __ldcs(vr + k + u);
+          cc[u] = __ldcs(cr + k + u);
+        }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < len) xv[u] = __ldg(x + cc[u]);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < len) acc = add(acc, mul(vv[u], xv[u]));
+    }
+    if (LATE) {
+#pragma unroll
+      for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][i];
+    }
+    e.row(i, acc, inr);
+  }
+  e.template finish<kThreads, false>();
 }
 
 // ------------------------------------------------------ stencil engine

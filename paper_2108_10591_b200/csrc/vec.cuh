@@ -151,7 +151,7 @@ __global__ void dot_final_kernel(const double* partials, int nparts, double* out
   if (threadIdx.x == 0) *out = acc;
 }
 
-// batch of the 9 safe dots, double-double tree, into partials[blk*kPartStride]
+// batch of the 9 safe dots, compensated tree, into partials[blk*kPartStride]
 __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const double* s, const double* y,
                                                               const double* r, const double* r0s,
                                                               const double* t, double* partials,
@@ -163,15 +163,15 @@ __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
     const double sv = s[i], yv = y[i], rv = r[i], r0 = r0s[i], tv = t[i];
-    acc[DA] = dd_add(acc[DA], dd_prod(sv, sv));
-    acc[DB] = dd_add(acc[DB], dd_prod(yv, yv));
-    acc[DC] = dd_add(acc[DC], dd_prod(sv, yv));
-    acc[DD] = dd_add(acc[DD], dd_prod(sv, rv));
-    acc[DE] = dd_add(acc[DE], dd_prod(yv, rv));
-    acc[DF] = dd_add(acc[DF], dd_prod(r0, rv));
-    acc[DG] = dd_add(acc[DG], dd_prod(r0, sv));
-    acc[DH] = dd_add(acc[DH], dd_prod(r0, tv));
-    acc[DR] = dd_add(acc[DR], dd_prod(rv, rv));
+    acc[DA] = dot2_step(acc[DA], sv, sv);
+    acc[DB] = dot2_step(acc[DB], yv, yv);
+    acc[DC] = dot2_step(acc[DC], sv, yv);
+    acc[DD] = dot2_step(acc[DD], sv, rv);
+    acc[DE] = dot2_step(acc[DE], yv, rv);
+    acc[DF] = dot2_step(acc[DF], r0, rv);
+    acc[DG] = dot2_step(acc[DG], r0, sv);
+    acc[DH] = dot2_step(acc[DH], r0, tv);
+    acc[DR] = dot2_step(acc[DR], rv, rv);
   }
   block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
 }
