@@ -139,7 +139,7 @@ def run_reference(args):
     n = len(rp) - 1
     threads = os.cpu_count() or 1
     b = orc.spmv(rp, ci, v, np.ones(n))
-    window = 10
+    window = 60  # iterations per reference step (~1 s on 16 host cores)
     for _ in range(args.warmup):
         orc.solve(rp, ci, v, b, tol=1e-30, max_iters=2, workers=threads, threads=threads)
     t0 = time.perf_counter()
@@ -344,7 +344,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--cpu-iters", type=int, default=40)
+    ap.add_argument("--cpu-iters", type=int, default=600)  # ~10 s on a 16-core host
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
