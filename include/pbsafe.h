@@ -196,6 +196,28 @@ int pbs_k_dot_range(pbs_ctx* ctx, const double* x, const double* y, int64_t lo, 
 int pbs_k_lincomb(pbs_ctx* ctx, int32_t kind, int64_t n, double* out, const double* sc,
                   const double* a, const double* b, const double* c, const double* d);
 
+/* ---- multi-GPU row partition (one process per GPU) --------------------- */
+/* The row-partitioned path of SURVEY §8(e): each rank owns rows [lo, hi) of
+ * PartitionPlan.balanced(n, nranks) (reduction.py:55-87).  Its local CSR is
+ * uploaded with pbs_csr_upload using columns remapped to the extended space
+ * [left halo (hl) | own (hi-lo) | right halo (hr)]; pbs_mat_set_partition
+ * attaches the halo transfer plan.  Solves on a partitioned operator take
+ * and return the rank's own segments of b / x0 / x; the history, status and
+ * iteration count are identical on every rank.  NCCL is loaded at run time
+ * (libnccl.so.2, e.g. the copy torch already loaded). */
+typedef struct pbs_dist pbs_dist;
+int pbs_nccl_unique_id(void* out128);
+/* two NCCL communicators: halo exchange and the dot all-gather (they run on
+ * different streams concurrently, so they must not share a communicator) */
+int pbs_dist_init(pbs_ctx* ctx, int32_t nranks, int32_t rank, const void* id_halo128,
+                  const void* id_reduce128, pbs_dist** dist);
+int pbs_dist_destroy(pbs_dist* dist);
+/* sends: nsend triples (peer, offset within the own segment, length);
+ * recvs: nrecv triples (peer, extended-space offset, length) */
+int pbs_mat_set_partition(pbs_mat* mat, pbs_dist* dist, int64_t n_global, int64_t row_lo, int64_t hl,
+                          int64_t hr, int32_t nsend, const int64_t* sends, int32_t nrecv,
+                          const int64_t* recvs);
+
 /* ---- device batch reduction --------------------------------------------- */
 /* 9 dots of the safe batch over device vectors s y r r0s t, packed a..h,r */
 int pbs_dot_batch_dev(pbs_ctx* ctx, int64_t n, const double* d_s, const double* d_y,

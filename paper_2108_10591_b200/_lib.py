@@ -34,7 +34,8 @@ EXPORTS = (
     "pbs_init", "pbs_destroy", "pbs_last_error", "pbs_device_info", "pbs_set_stream",
     "pbs_csr_upload", "pbs_stencil_create", "pbs_mat_free", "pbs_mat_info", "pbs_spmv_dev",
     "pbs_solve", "pbs_solve_dev", "pbs_step_dev", "pbs_k_spmv_range", "pbs_k_dot_range",
-    "pbs_k_lincomb", "pbs_dot_batch_dev",
+    "pbs_k_lincomb", "pbs_dot_batch_dev", "pbs_nccl_unique_id", "pbs_dist_init", "pbs_dist_destroy",
+    "pbs_mat_set_partition",
 )
 
 
@@ -114,6 +115,10 @@ def load(build_if_missing: bool = True):
             "pbs_k_dot_range": ([p, p, p, i64, i64, C.POINTER(d)], C.c_int),
             "pbs_k_lincomb": ([p, i32, i64, p, p, p, p, p, p], C.c_int),
             "pbs_dot_batch_dev": ([p, i64, p, p, p, p, p, i32, i32, p], C.c_int),
+            "pbs_nccl_unique_id": ([p], C.c_int),
+            "pbs_dist_init": ([p, i32, i32, p, p, pp], C.c_int),
+            "pbs_dist_destroy": ([p], C.c_int),
+            "pbs_mat_set_partition": ([p, p, i64, i64, i64, i64, i32, p, i32, p], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

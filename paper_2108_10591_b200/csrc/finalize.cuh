@@ -151,6 +151,29 @@ __device__ void reduce_parts(const double* partials, int nparts, int chain, doub
   block_bar<NT, NAMED>();
 }
 
+// Multi-GPU local step: reduce this rank's CTA partial records to ONE record
+// of 9 compensated pairs (not rounded), the payload of the all-gather.
+__global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partials, int nparts, double* out) {
+  constexpr int T = 288 / kNumDots;
+  __shared__ Ddbl team[kNumDots][T];
+  const int t = threadIdx.x, j = t / T, l = t % T;
+  if (j < kNumDots) {
+    Ddbl acc{0.0, 0.0};
+    for (int b = l; b < nparts; b += T) {
+      const double* p = partials + (size_t)b * kPartStride + 2 * j;
+      acc = dd_add(acc, Ddbl{__ldcg(p), __ldcg(p + 1)});
+    }
+    team[j][l] = acc;
+  }
+  __syncthreads();
+  if (t < kNumDots) {
+    Ddbl acc = team[t][0];
+    for (int k = 1; k < T; ++k) acc = dd_add(acc, team[t][k]);
+    out[2 * t] = acc.hi;
+    out[2 * t + 1] = acc.lo;
+  }
+}
+
 // Run by every participating thread of each CTA after its block_reduce9:
 // the last CTA to arrive reduces all partials and performs the check.
 template <int NT, bool NAMED>

@@ -19,6 +19,9 @@
 #include <map>
 #include <thread>
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: libnccl.so.2 is loaded at run time
+
 #include "common.cuh"
 #include "spmv.cuh"
 #include "vec.cuh"
@@ -44,6 +47,71 @@ struct EventPool {
   ~EventPool() {
     for (auto e : ev) cudaEventDestroy(e);
   }
+};
+
+// ---- NCCL, loaded on first use (the copy torch loaded, or the system one)
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string err;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  if (api.tried) return api;
+  api.tried = true;
+  void* h = nullptr;
+  for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+    h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+    if (h) break;
+  }
+  if (!h) {
+    api.err = std::string("cannot load libnccl.so.2: ") + dlerror();
+    return api;
+  }
+#define PBS_SYM(field, sym)                                    \
+  api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, sym)); \
+  if (!api.field) {                                            \
+    api.err = std::string("libnccl lacks ") + sym;             \
+    return api;                                                \
+  }
+  PBS_SYM(GetUniqueId, "ncclGetUniqueId")
+  PBS_SYM(CommInitRank, "ncclCommInitRank")
+  PBS_SYM(CommDestroy, "ncclCommDestroy")
+  PBS_SYM(Send, "ncclSend")
+  PBS_SYM(Recv, "ncclRecv")
+  PBS_SYM(AllGather, "ncclAllGather")
+  PBS_SYM(GroupStart, "ncclGroupStart")
+  PBS_SYM(GroupEnd, "ncclGroupEnd")
+  PBS_SYM(GetErrorString, "ncclGetErrorString")
+#undef PBS_SYM
+  api.ok = true;
+  return api;
+}
+
+struct pbs_dist {
+  pbs_ctx* ctx = nullptr;
+  int nranks = 1, rank = 0;
+  ncclComm_t halo = nullptr, red = nullptr;
+  cudaStream_t comm = nullptr;  // all-gather + finalize, overlapping the As SpMV
+  cudaEvent_t ev_part = nullptr, ev_coef = nullptr;
+  double* sendbuf = nullptr;  // this rank's 9 compensated pairs
+  double* recvbuf = nullptr;  // all ranks' pairs, rank order
+};
+
+// row partition of an operator (see include/pbsafe.h)
+struct Partition {
+  pbs_dist* dist = nullptr;
+  long long n_global = 0, row_lo = 0, hl = 0, hr = 0;
+  std::vector<long long> sends, recvs;  // triples
 };
 
 struct Workspace;
@@ -73,6 +141,7 @@ struct pbs_mat {
   double* v = nullptr;
   StencilView sv{};
   XWin xwin{};  // x windows of the pipelined CSR engine (nwin = 0: gather x)
+  Partition part;  // multi-GPU row partition (part.dist == nullptr: single GPU)
   Workspace* ws = nullptr;
 };
 
@@ -115,7 +184,9 @@ struct Workspace {
   long long n = 0;
   size_t stride = 0;  // padded elements per vector
   double* base = nullptr;
-  VecPtrs V{};
+  VecPtrs V{};  // own segments (elementwise kernels, SpMV outputs, epilogue inputs)
+  VecPtrs X{};  // extended-space bases (SpMV inputs: [left halo | own | right halo])
+  long long n_ext = 0, own_off = 0;
   double* partials = nullptr;
   long long* plan_bounds = nullptr;
   int plan_workers = 0;
@@ -162,9 +233,16 @@ static int ensure_ws(pbs_mat* m, long long hist_slots) {
     ws = new Workspace();
     m->ws = ws;
     ws->n = m->n_rows;
-    ws->stride = ((size_t)ws->n + 2 + 31) / 32 * 32;  // +2: aligned bulk-copy over-read
+    ws->n_ext = m->part.dist ? m->n_cols : m->n_rows;
+    ws->own_off = m->part.dist ? m->part.hl + (m->part.hl & 1) : 0;  // even: 16-byte aligned
+    // +2: aligned bulk-copy over-read; even own offset keeps 16-byte alignment
+    ws->stride = ((size_t)ws->n_ext + 4 + 31) / 32 * 32;
     CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
-    for (int k = 0; k < kNumVecs; ++k) ws->V.v[k] = ws->base + ws->stride * k;
+    CK(cudaMemset(ws->base, 0, sizeof(double) * ws->stride * kNumVecs));
+    for (int k = 0; k < kNumVecs; ++k) {
+      ws->X.v[k] = ws->base + ws->stride * k;
+      ws->V.v[k] = ws->X.v[k] + ws->own_off;
+    }
     CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kPartStride));
     CK(cudaMalloc(&ws->st, sizeof(SolverState)));
     CK(cudaHostAlloc(&ws->mirror_h, sizeof(HostMirror), cudaHostAllocMapped));
@@ -507,13 +585,13 @@ static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int repl
 // s = A r (+ the batch of the next check); tree mode fuses the check into the
 // SpMV's last CTA, plan mode runs the plan chains + a separate finalize
 static void spmv_s_check(Launcher& L, Workspace* ws, const Mode& md, int kind, int spine, int replaced) {
-  spmv_launch(L, ws->V.v[VR], epi_dots(ws, md, spine, 1, replaced), 0, ws->n, kind);
+  spmv_launch(L, ws->X.v[VR], epi_dots(ws, md, spine, 1, replaced), 0, ws->n, kind);
   if (md.plan) finalize(L, ws, plan_dots(L, ws, KD), 1, replaced);
 }
 
 // setup of the pipelined methods (solvers.py:612-631) + check 0
 static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
-  spmv_launch(L, ws->V.v[VX], epi_resid(ws, true), 0, ws->n, KS);
+  spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, ws->n, KS);
   spmv_s_check(L, ws, md, KS, 0, 0);
 }
 
@@ -521,8 +599,8 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
 // (Aw + l g s + the fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  spmv_launch(L, V[VS], epi_k12(ws, md), 0, ws->n, KK1);
-  const int grid = spmv_launch(L, V[VW], epi_k3(ws, md, L.trace_cfg ? 0 : 1), 0, ws->n, KK3);
+  spmv_launch(L, ws->X.v[VS], epi_k12(ws, md), 0, ws->n, KK1);
+  const int grid = spmv_launch(L, ws->X.v[VW], epi_k3(ws, md, L.trace_cfg ? 0 : 1), 0, ws->n, KK3);
   if (md.plan) {
     int np = plan_dots(L, ws, KD);
     L.trace_point();
@@ -536,16 +614,16 @@ static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
 // residual-replacement iteration (solvers.py:676-713)
 static void iter_replace(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
+  spmv_launch(L, ws->X.v[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
   vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-  spmv_launch(L, V[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
-  spmv_launch(L, V[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
+  spmv_launch(L, ws->X.v[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
+  spmv_launch(L, ws->X.v[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
   vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-  spmv_launch(L, V[VX], epi_resid(ws, false), 0, ws->n, KRS);
-  spmv_launch(L, V[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
-  spmv_launch(L, V[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
+  spmv_launch(L, ws->X.v[VX], epi_resid(ws, false), 0, ws->n, KRS);
+  spmv_launch(L, ws->X.v[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
+  spmv_launch(L, ws->X.v[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
   if (L.trace_cfg) {
-    int np = spmv_launch(L, V[VR], epi_dots(ws, md, 0, 0, 1), 0, ws->n, KRS);
+    int np = spmv_launch(L, ws->X.v[VR], epi_dots(ws, md, 0, 0, 1), 0, ws->n, KRS);
     if (md.plan) np = plan_dots(L, ws, KD);
     L.trace_point();
     finalize(L, ws, np, md.plan, 1);
@@ -560,7 +638,7 @@ static void iter_ss(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
   spmv_s_check(L, ws, md, KK1, 1, 0);
   vec_launch(L, pou_kernel, ws->n, KK2, ws->V, ws->n, ws->st);
-  spmv_launch(L, V[VU], epi_ss3(ws), 0, ws->n, KK3);
+  spmv_launch(L, ws->X.v[VU], epi_ss3(ws), 0, ws->n, KK3);
   L.trace_point();
 }
 
@@ -611,6 +689,86 @@ static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const M
   return PBS_OK;
 }
 
+// ---------------------------------------------------------- multi-GPU schedule
+//
+// Per steady iteration j on every rank (stream s = compute, comm = reduction):
+//   s:    halo(s) -> K1 As = A s (spine)            || comm: all-gather of the
+//   s:    wait coefficients -> K2 updates              batch pairs of check j ->
+//   s:    halo(w) -> K3 (Aw + l g s + local partials)  finalize (check j)
+//   s:    reduce CTA partials -> this rank's 9 pairs -> record ev_part
+// The all-gather + check of iteration j overlaps the As SpMV: the pipelined
+// method's single reduction hides behind one SpMV.
+
+static void halo_exchange(Launcher& L, Workspace* ws, pbs_mat* m, int k) {
+  Partition& P = m->part;
+  pbs_dist* D = P.dist;
+  if (L.err || D->nranks == 1 || (P.sends.empty() && P.recvs.empty())) return;
+  NcclApi& A = nccl();
+  ncclResult_t r = A.GroupStart();
+  for (size_t i = 0; r == ncclSuccess && i < P.recvs.size(); i += 3)
+    r = A.Recv(ws->X.v[k] + P.recvs[i + 1], (size_t)P.recvs[i + 2], ncclDouble, (int)P.recvs[i], D->halo, L.s);
+  for (size_t i = 0; r == ncclSuccess && i < P.sends.size(); i += 3)
+    r = A.Send(ws->V.v[k] + P.sends[i + 1], (size_t)P.sends[i + 2], ncclDouble, (int)P.sends[i], D->halo, L.s);
+  ncclResult_t r2 = A.GroupEnd();
+  if (r == ncclSuccess) r = r2;
+  if (r != ncclSuccess) L.err = set_err(L.ctx, PBS_ERR_NCCL, std::string("halo exchange: ") + A.GetErrorString(r));
+}
+
+// this rank's pairs -> all-gather on the comm stream -> finalize (check)
+static void dist_check(Launcher& L, Workspace* ws, pbs_mat* m, int nparts, int replaced) {
+  pbs_dist* D = m->part.dist;
+  if (L.err) return;
+  reduce_pairs_kernel<<<1, 288, 0, L.s>>>(ws->partials, nparts, D->sendbuf);
+  L.done(KD);
+  cudaEventRecord(D->ev_part, L.s);
+  cudaStreamWaitEvent(D->comm, D->ev_part, 0);
+  ncclResult_t r = nccl().AllGather(D->sendbuf, D->recvbuf, kPartStride, ncclDouble, D->red, D->comm);
+  if (r != ncclSuccess) {
+    L.err = set_err(L.ctx, PBS_ERR_NCCL, std::string("all-gather: ") + nccl().GetErrorString(r));
+    return;
+  }
+  finalize_kernel<<<1, 288, 0, D->comm>>>(ws->st, D->recvbuf, D->nranks, 0, replaced);
+  L.done(KF);
+  cudaEventRecord(D->ev_coef, D->comm);
+}
+
+static void dist_setup(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md) {
+  halo_exchange(L, ws, m, VX);
+  spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, ws->n, KS);
+  halo_exchange(L, ws, m, VR);
+  int np = spmv_launch(L, ws->X.v[VR], epi_dots(ws, md, 0, 0, 0), 0, ws->n, KS);
+  dist_check(L, ws, m, np, 0);
+}
+
+static void dist_iter(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md, bool replace) {
+  pbs_dist* D = m->part.dist;
+  halo_exchange(L, ws, m, VS);
+  spmv_launch(L, ws->X.v[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
+  cudaStreamWaitEvent(L.s, D->ev_coef, 0);  // coefficients of this check
+  int np;
+  if (!replace) {
+    vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
+    halo_exchange(L, ws, m, VW);
+    np = spmv_launch(L, ws->X.v[VW], epi_k3(ws, md, 0), 0, ws->n, KK3);
+  } else {
+    vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+    halo_exchange(L, ws, m, VO);
+    spmv_launch(L, ws->X.v[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
+    halo_exchange(L, ws, m, VU);
+    spmv_launch(L, ws->X.v[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
+    vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
+    halo_exchange(L, ws, m, VX);
+    spmv_launch(L, ws->X.v[VX], epi_resid(ws, false), 0, ws->n, KRS);
+    halo_exchange(L, ws, m, VT);
+    spmv_launch(L, ws->X.v[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
+    halo_exchange(L, ws, m, VY);
+    spmv_launch(L, ws->X.v[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
+    halo_exchange(L, ws, m, VR);
+    np = spmv_launch(L, ws->X.v[VR], epi_dots(ws, md, 0, 0, 1), 0, ws->n, KRS);
+  }
+  dist_check(L, ws, m, np, replace ? 1 : 0);
+}
+
 // ------------------------------------------------------------------- solving
 
 static int validate_cfg(pbs_ctx* ctx, const pbs_config* cfg) {
@@ -624,8 +782,67 @@ static int validate_cfg(pbs_ctx* ctx, const pbs_config* cfg) {
   return PBS_OK;
 }
 
+// Device state -> pbs_result (+ the reference's SpMV tally)
+static int collect_result(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* res, Launcher& L,
+                          std::vector<std::pair<int, cudaEvent_t>>& marks, long long launched_graph_kernels) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  const bool pipelined = method != PBS_METHOD_SSBICGSAFE2;
+  const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
+  const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
+  SolverState out;
+  CK(cudaMemcpy(&out, ws->st, sizeof(out), cudaMemcpyDeviceToHost));
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
+  memset(res, 0, sizeof(*res));
+  res->device_ms = ms;
+  res->kernel_launches = L.launches + launched_graph_kernels;
+  if (L.timing) {
+    for (size_t k = 1; k < marks.size(); ++k) {
+      float d = 0.f;
+      cudaEventElapsedTime(&d, marks[k - 1].second, marks[k].second);
+      int kind = marks[k].first;
+      if (kind >= 0 && kind < PBS_NUM_KERNEL_KINDS) {
+        res->kernel_ms[kind] += d;
+        res->kernel_count[kind] += 1;
+      }
+    }
+  }
+  res->status = out.status;
+  res->breakdown = out.breakdown;
+  res->iterations = out.iterations;
+  res->failure_iter = out.failure_iter;
+  res->n_records = out.n_records;
+  res->r0_norm = out.r0_norm;
+  res->nonfinite_index = -1;
+  if (out.nf_row != (unsigned long long)kNoError) {
+    res->nonfinite_tag = out.nf_tag;
+    res->nonfinite_index = (long long)out.nf_row + (m->part.dist ? m->part.row_lo : 0);
+    return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output");
+  }
+  if (out.status < 0) return set_err(ctx, PBS_ERR_CUDA, "solver ended without a status");
+  // SpMV count as the reference tallies it (solvers.py:613-723, 530-569)
+  const long long reached = out.status == PBS_MAX_ITERS || out.iterations == cfg->max_iters
+                                ? cfg->max_iters
+                                : out.iterations + 1;
+  const long long completed = out.iterations;
+  long long nrep = 0;
+  if (rr)
+    for (long long i = 1; i < completed && i < cutoff; ++i)
+      if (i % cfg->rr_epoch == 0) ++nrep;
+  res->n_replacements = nrep;
+  if (pipelined)
+    res->n_spmv = 2 + reached + completed + 5 * nrep;
+  else
+    res->n_spmv = 1 + reached + completed;
+  return PBS_OK;
+}
+
 // Runs a solve with b / x0 already in the workspace (VB, VX).
+static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* res);
+
 static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* res) {
+  if (m->part.dist) return run_solve_dist(m, method, cfg, res);
   pbs_ctx* ctx = m->ctx;
   Workspace* ws = m->ws;
   const long long n = ws->n;
@@ -683,7 +900,7 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
     setup_pipelined(L, ws, md);
     if (L.err) return L.err;
   } else {
-    spmv_launch(L, ws->V.v[VX], epi_resid(ws, true), 0, n, KS);
+    spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, n, KS);
   }
   const long long lookahead = 6;
   long long launched_graph_kernels = 0;
@@ -732,52 +949,102 @@ loop_end:
   CK(cudaEventRecord(ws->ev1, s));
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());
-  SolverState out;
-  CK(cudaMemcpy(&out, ws->st, sizeof(out), cudaMemcpyDeviceToHost));
-  float ms = 0.f;
-  cudaEventElapsedTime(&ms, ws->ev0, ws->ev1);
-  memset(res, 0, sizeof(*res));
-  res->device_ms = ms;
-  res->kernel_launches = L.launches + launched_graph_kernels;
-  if (L.timing) {
-    for (size_t k = 1; k < marks.size(); ++k) {
-      float d = 0.f;
-      cudaEventElapsedTime(&d, marks[k - 1].second, marks[k].second);
-      int kind = marks[k].first;
-      if (kind >= 0 && kind < PBS_NUM_KERNEL_KINDS) {
-        res->kernel_ms[kind] += d;
-        res->kernel_count[kind] += 1;
-      }
+  return collect_result(m, method, cfg, res, L, marks, launched_graph_kernels);
+}
+
+
+// Multi-GPU solve: every rank launches the same sequence; at chunk
+// boundaries the ranks agree (all-gather of two flags) on whether any rank
+// hit a non-finite SpMV output or the solve stopped, so the NCCL call
+// sequence stays identical on every rank.
+static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* res) {
+  pbs_ctx* ctx = m->ctx;
+  Workspace* ws = m->ws;
+  pbs_dist* D = m->part.dist;
+  if (method == PBS_METHOD_SSBICGSAFE2)
+    return set_err(ctx, PBS_ERR_UNSUPPORTED, "ssBiCGSafe2 has no multi-GPU schedule yet");
+  if (cfg->reduce_mode != PBS_REDUCE_TREE)
+    return set_err(ctx, PBS_ERR_UNSUPPORTED, "multi-GPU solves use the compensated tree reduction");
+  if (cfg->trace_fn) return set_err(ctx, PBS_ERR_UNSUPPORTED, "trace_hook is single-GPU only");
+  Mode md;
+  cudaStream_t s = ctx->stream;
+  SolverState h{};
+  h.tol = cfg->tol;
+  h.max_iters = cfg->max_iters;
+  h.record_history = cfg->record_history ? 1 : 0;
+  h.run_all = 1;
+  h.run_spine = 1;
+  h.status = -1;
+  h.failure_iter = -1;
+  h.nf_row = (unsigned long long)kNoError;
+  h.hist_rel = ws->hist_rel;
+  h.hist_flags = ws->hist_flags;
+  h.hist_coef = ws->hist_coef;
+  h.mirror = nullptr;
+  CK(cudaMemcpyAsync(ws->st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+  const int zero_slots[] = {VP, VU, VT, VY, VZ, VG, VL, VW};
+  for (int k : zero_slots) CK(cudaMemsetAsync(ws->X.v[k], 0, sizeof(double) * ws->n_ext, s));
+  std::vector<std::pair<int, cudaEvent_t>> marks;
+  ctx->events.reset();
+  Launcher L{ctx, m, s};
+  L.timing = cfg->timing != 0;
+  L.marks = &marks;
+  const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
+  const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
+  int* flags = nullptr;  // [2] local, [2*nranks] gathered
+  CK(cudaMalloc(&flags, sizeof(int) * 2 * (D->nranks + 1)));
+  CK(cudaEventRecord(ws->ev0, s));
+  if (L.timing) marks.push_back({-1, ws->ev0});
+  dist_setup(L, ws, m, md);
+  const long long chunk = 8;
+  long long j = 0;
+  int rc = PBS_OK;
+  bool any_err = false;
+  while (!L.err) {
+    const long long jend = j + chunk < cfg->max_iters ? j + chunk : cfg->max_iters;
+    for (; j < jend && !L.err; ++j) {
+      const bool replace = rr && (j % cfg->rr_epoch == 0) && 0 < j && j < cutoff;
+      dist_iter(L, ws, m, md, replace);
     }
+    if (L.err) break;
+    // agreement: every rank contributes (error, stopped); the reduction
+    // communicator is only ever driven from the comm stream
+    CK(cudaStreamSynchronize(s));
+    CK(cudaStreamSynchronize(D->comm));
+    SolverState st;
+    CK(cudaMemcpy(&st, ws->st, sizeof(st), cudaMemcpyDeviceToHost));
+    int mine[2] = {st.nf_row != (unsigned long long)kNoError ? 1 : 0, st.run_all ? 0 : 1};
+    CK(cudaMemcpyAsync(flags, mine, sizeof(mine), cudaMemcpyHostToDevice, D->comm));
+    ncclResult_t r = nccl().AllGather(flags, flags + 2, 2, ncclInt32, D->red, D->comm);
+    if (r != ncclSuccess) {
+      rc = set_err(ctx, PBS_ERR_NCCL, std::string("agreement: ") + nccl().GetErrorString(r));
+      break;
+    }
+    std::vector<int> all(2 * D->nranks);
+    CK(cudaMemcpyAsync(all.data(), flags + 2, sizeof(int) * 2 * D->nranks, cudaMemcpyDeviceToHost, D->comm));
+    CK(cudaStreamSynchronize(D->comm));
+    bool stop = true;
+    for (int q = 0; q < D->nranks; ++q) {
+      any_err = any_err || all[2 * q];
+      stop = stop && all[2 * q + 1];
+    }
+    if (any_err || stop || j >= cfg->max_iters) break;
   }
-  res->status = out.status;
-  res->breakdown = out.breakdown;
-  res->iterations = out.iterations;
-  res->failure_iter = out.failure_iter;
-  res->n_records = out.n_records;
-  res->r0_norm = out.r0_norm;
-  res->nonfinite_index = -1;
-  if (out.nf_row != (unsigned long long)kNoError) {
-    res->nonfinite_tag = out.nf_tag;
-    res->nonfinite_index = (long long)out.nf_row;
-    return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output");
+  cudaFree(flags);
+  if (L.err) return L.err;
+  if (rc) return rc;
+  CK(cudaStreamWaitEvent(s, D->ev_coef, 0));
+  CK(cudaEventRecord(ws->ev1, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaStreamSynchronize(D->comm));
+  CK(cudaGetLastError());
+  rc = collect_result(m, method, cfg, res, L, marks, 0);
+  if (rc == PBS_OK && any_err) {  // another rank raised: raise here too
+    res->nonfinite_tag = PBS_TAG_AS;
+    res->nonfinite_index = -1;
+    return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output on another rank");
   }
-  if (out.status < 0) return set_err(ctx, PBS_ERR_CUDA, "solver ended without a status");
-  // SpMV count as the reference tallies it (solvers.py:613-723, 530-569)
-  const long long reached = out.status == PBS_MAX_ITERS || out.iterations == cfg->max_iters
-                                ? cfg->max_iters
-                                : out.iterations + 1;
-  const long long completed = out.iterations;
-  long long nrep = 0;
-  if (rr)
-    for (long long i = 1; i < completed && i < cutoff; ++i)
-      if (i % cfg->rr_epoch == 0) ++nrep;
-  res->n_replacements = nrep;
-  if (pipelined)
-    res->n_spmv = 2 + reached + completed + 5 * nrep;
-  else
-    res->n_spmv = 1 + reached + completed;
-  return PBS_OK;
+  return rc;
 }
 
 static int copy_history(pbs_mat* m, const pbs_result* res, double* hist_rel, uint8_t* hist_flags,
@@ -1127,7 +1394,7 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
 static int solve_common(pbs_mat* m, int32_t method, const pbs_config* cfg) {
   pbs_ctx* ctx = m ? m->ctx : nullptr;
   if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
-  if (m->n_rows != m->n_cols) return set_err(ctx, PBS_ERR_INVALID, "solver needs a square operator");
+  if (!m->part.dist && m->n_rows != m->n_cols) return set_err(ctx, PBS_ERR_INVALID, "solver needs a square operator");
   if (method < 0 || method > 2) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
   int rc = validate_cfg(ctx, cfg);
   if (rc) return rc;
@@ -1231,21 +1498,21 @@ PBS_EXPORT int pbs_step_dev(pbs_mat* m, double* const* d_state, const double* in
     auto& V = ws->V.v;
     Mode nm = md;  // the step's batch comes first; the body's partials are not needed
     if (in[5] != 0.0) {
-      spmv_launch(L, V[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
+      spmv_launch(L, ws->X.v[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
       vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-      spmv_launch(L, V[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
-      spmv_launch(L, V[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VO], epi_store(ws, VQ, PBS_TAG_AO, 0), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VU], epi_store(ws, VW, PBS_TAG_AU, 0), 0, ws->n, KRS);
       vec_launch(L, tzyx_kernel, ws->n, KR, ws->V, ws->n, ws->st);
-      spmv_launch(L, V[VX], epi_resid(ws, false), 0, ws->n, KRS);
-      spmv_launch(L, V[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
-      spmv_launch(L, V[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VX], epi_resid(ws, false), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VT], epi_store(ws, VL, PBS_TAG_AT, 0), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VY], epi_store(ws, VG, PBS_TAG_AY, 0), 0, ws->n, KRS);
       nm.plan = 1;  // no partials
-      spmv_launch(L, V[VR], epi_dots(ws, nm, 0, 0, 0), 0, ws->n, KRS);
+      spmv_launch(L, ws->X.v[VR], epi_dots(ws, nm, 0, 0, 0), 0, ws->n, KRS);
     } else {
       nm.plan = 1;
       nm.store_temps = 1;
-      spmv_launch(L, V[VS], epi_k12(ws, nm), 0, ws->n, KK1);
-      spmv_launch(L, V[VW], epi_k3(ws, nm, 0), 0, ws->n, KK3);
+      spmv_launch(L, ws->X.v[VS], epi_k12(ws, nm), 0, ws->n, KK1);
+      spmv_launch(L, ws->X.v[VW], epi_k3(ws, nm, 0), 0, ws->n, KK3);
     }
   }
   if (L.err) return L.err;
@@ -1431,5 +1698,93 @@ PBS_EXPORT int pbs_dot_batch_dev(pbs_ctx* ctx, int64_t n, const double* d_s, con
   CK(cudaStreamSynchronize(s));
   cudaFree(d_bounds);
   CK(cudaGetLastError());
+  return PBS_OK;
+}
+
+// ------------------------------------------------------------ multi-GPU C-ABI
+
+PBS_EXPORT int pbs_nccl_unique_id(void* out) {
+  NcclApi& A = nccl();
+  if (!A.ok) return set_err(nullptr, PBS_ERR_NCCL, A.err);
+  ncclUniqueId id;
+  ncclResult_t r = A.GetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(nullptr, PBS_ERR_NCCL, A.GetErrorString(r));
+  memcpy(out, &id, sizeof(id));
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_dist_init(pbs_ctx* ctx, int32_t nranks, int32_t rank, const void* id_halo,
+                             const void* id_red, pbs_dist** out) {
+  if (!ctx || !out) return set_err(ctx, PBS_ERR_INVALID, "NULL argument");
+  if (nranks < 1 || rank < 0 || rank >= nranks) return set_err(ctx, PBS_ERR_INVALID, "bad rank / nranks");
+  NcclApi& A = nccl();
+  if (!A.ok) return set_err(ctx, PBS_ERR_NCCL, A.err);
+  CK(cudaSetDevice(ctx->device));
+  pbs_dist* d = new pbs_dist();
+  d->ctx = ctx;
+  d->nranks = nranks;
+  d->rank = rank;
+  ncclUniqueId a, b;
+  memcpy(&a, id_halo, sizeof(a));
+  memcpy(&b, id_red, sizeof(b));
+  ncclResult_t r = A.CommInitRank(&d->halo, nranks, a, rank);
+  if (r == ncclSuccess) r = A.CommInitRank(&d->red, nranks, b, rank);
+  if (r != ncclSuccess) {
+    delete d;
+    return set_err(ctx, PBS_ERR_NCCL, std::string("ncclCommInitRank: ") + A.GetErrorString(r));
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, hi));  // reduction first
+  CK(cudaEventCreateWithFlags(&d->ev_part, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d->ev_coef, cudaEventDisableTiming));
+  CK(cudaMalloc(&d->sendbuf, sizeof(double) * kPartStride));
+  CK(cudaMalloc(&d->recvbuf, sizeof(double) * kPartStride * nranks));
+  *out = d;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_dist_destroy(pbs_dist* d) {
+  if (!d) return PBS_OK;
+  cudaSetDevice(d->ctx->device);
+  cudaStreamSynchronize(d->comm);
+  if (d->halo) nccl().CommDestroy(d->halo);
+  if (d->red) nccl().CommDestroy(d->red);
+  cudaStreamDestroy(d->comm);
+  cudaEventDestroy(d->ev_part);
+  cudaEventDestroy(d->ev_coef);
+  cudaFree(d->sendbuf);
+  cudaFree(d->recvbuf);
+  delete d;
+  return PBS_OK;
+}
+
+PBS_EXPORT int pbs_mat_set_partition(pbs_mat* m, pbs_dist* dist, int64_t n_global, int64_t row_lo, int64_t hl,
+                                     int64_t hr, int32_t nsend, const int64_t* sends, int32_t nrecv,
+                                     const int64_t* recvs) {
+  if (!m || !dist) return set_err(nullptr, PBS_ERR_INVALID, "NULL argument");
+  pbs_ctx* ctx = m->ctx;
+  if (m->stencil) return set_err(ctx, PBS_ERR_UNSUPPORTED, "partitioned operators are CSR slabs");
+  const long long pad = hl & 1;
+  if (m->n_cols != pad + hl + m->n_rows + hr)
+    return set_err(ctx, PBS_ERR_INVALID, "n_cols must equal pad + hl + n_own + hr (extended space)");
+  if (m->ws) {  // the workspace layout depends on the partition
+    free_ws(m->ws);
+    m->ws = nullptr;
+  }
+  Partition& P = m->part;
+  P.dist = dist;
+  P.n_global = n_global;
+  P.row_lo = row_lo;
+  P.hl = hl;
+  P.hr = hr;
+  P.sends.assign(sends, sends + 3 * (size_t)nsend);
+  P.recvs.assign(recvs, recvs + 3 * (size_t)nrecv);
+  for (size_t i = 0; i < P.sends.size(); i += 3)
+    if (P.sends[i + 1] < 0 || P.sends[i + 1] + P.sends[i + 2] > m->n_rows)
+      return set_err(ctx, PBS_ERR_INVALID, "halo send outside the own segment");
+  for (size_t i = 0; i < P.recvs.size(); i += 3)
+    if (P.recvs[i + 1] < 0 || P.recvs[i + 1] + P.recvs[i + 2] > m->n_cols)
+      return set_err(ctx, PBS_ERR_INVALID, "halo receive outside the extended space");
   return PBS_OK;
 }

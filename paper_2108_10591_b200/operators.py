@@ -36,7 +36,7 @@ class DeviceMatrix:
     @classmethod
     def from_csr(cls, A: CsrMatrix | tuple, device: int | None = None, ctx=None) -> "DeviceMatrix":
         """Upload a CsrMatrix (or (row_ptr, col_idx, values[, n_cols]) arrays)."""
-        if isinstance(A, CsrMatrix):
+        if isinstance(A, CsrMatrix) or hasattr(A, "row_ptr"):  # ours or the reference's CsrMatrix
             rp, ci, v, n_rows, n_cols = A.row_ptr, A.col_idx, A.values, A.n_rows, A.n_cols
         else:
             rp, ci, v = A[:3]
