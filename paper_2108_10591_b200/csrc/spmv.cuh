@@ -130,7 +130,7 @@ struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
 
 struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   static constexpr int kIn = 4;
-  static constexpr int kGatherBatch = 4;  // x gathers in flight per row
+  static constexpr int kGatherBatch = 2;  // x gathers in flight per row
   double* s;
   SolverState* st;
   int tag;
@@ -204,7 +204,7 @@ struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local
 
 struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
   static constexpr int kIn = 8;
-  static constexpr int kGatherBatch = 4;  // x gathers in flight per row
+  static constexpr int kGatherBatch = 2;  // x gathers in flight per row
   double *l, *g, *s;
   double* q_out;  // nullable (single-step parity: expose q)
   SolverState* st;
@@ -429,10 +429,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       if (lane == 0) {
         bulk_g2s(bst + BL.rp, A.rp + r0a, brp, &bfull[bs]);
       } else if (lane <= W.nwin) {
-        const int c = lane - 1;
+        // lane 1+c copies window c (static indexing keeps wlo/wbytes in registers)
         int soff = 0;
-        for (int cc = 0; cc < c; ++cc) soff += W.cap[cc];
-        if (wbytes[c]) bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[c], wbytes[c], &bfull[bs]);
+#pragma unroll
+        for (int cc = 0; cc < kMaxWin; ++cc) {
+          if (cc == lane - 1 && wbytes[cc])
+            bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
+          soff += cc < W.nwin ? W.cap[cc] : 0;
+        }
       } else if (lane >= 8 && lane < 8 + Epi::kIn) {
         const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
