@@ -141,6 +141,7 @@ struct pbs_mat {
   double* v = nullptr;
   StencilView sv{};
   XWin xwin{};  // x windows of the pipelined CSR engine (nwin = 0: gather x)
+  long long blk_nnz_max = 0;  // most nonzeros in one 256-row block (chunk sizing)
   Partition part;  // multi-GPU row partition (part.dist == nullptr: single GPU)
   Workspace* ws = nullptr;
 };
@@ -362,8 +363,8 @@ static int pipe_ctas_per_sm() {
   static int v = env_int("PBS_PIPE_CTAS", 2, 1, 4);
   return v;
 }
-static int pipe_chunk() {
-  static int v = env_int("PBS_PIPE_CHUNK", 1024, 256, kPipeChunkMax) & ~3;
+static int pipe_chunk_cap() {
+  static int v = env_int("PBS_PIPE_CHUNK", 2048, 256, kPipeChunkMax) & ~3;
   return v;
 }
 static int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-row CSR engine
@@ -378,16 +379,24 @@ static int pipe_slots_cap() {
   static int v = env_int("PBS_PIPE_SLOTS", 2, 2, kMaxStages);
   return v;
 }
+static int pipe_extra_chunks() {  // chunk stages beyond the block slots
+  static int v = env_int("PBS_PIPE_XCHUNK", 0, 0, 4);
+  return v;
+}
 
 template <class Epi>
-static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, size_t* smem, int* ctas,
-                       int* chunk) {
+static int pipe_config(pbs_ctx* ctx, const XWin& W, long long blk_nnz_max, int* bslots, int* cstages,
+                       size_t* smem, int* ctas, int* chunk) {
   const BlockLayout BL(W.total, Epi::kIn);
-  const ChunkLayout CL(pipe_chunk());
+  // one chunk per row block when the densest block fits the cap (stencils:
+  // ~7 or ~27 nonzeros per row), else cap-sized chunks
+  int ch = pipe_chunk_cap();
+  if (blk_nnz_max > 0 && blk_nnz_max < ch) ch = (int)((blk_nnz_max + 3) & ~3LL);
+  const ChunkLayout CL(ch);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  int n = 0, c = pipe_ctas_per_sm();
+  int n = 0, c = pipe_ctas_per_sm(), xc = 0;
   for (; c >= 1; --c) {
     // per-CTA budget: the SM's shared memory split between the resident CTAs,
     // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
@@ -396,14 +405,20 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, int* cstages, s
     budget -= kPipeBarrierBytes;
     n = (int)(budget / (BL.bytes + CL.bytes));
     if (n > pipe_slots_cap()) n = pipe_slots_cap();
-    if (n >= 2) break;
+    if (n < 2) continue;
+    // extra chunk stages so the next block's nonzeros stream while the
+    // current block's chunks are consumed
+    xc = (int)((budget - (size_t)n * (BL.bytes + CL.bytes)) / CL.bytes);
+    if (xc > pipe_extra_chunks()) xc = pipe_extra_chunks();
+    if (n + xc > kMaxStages) xc = kMaxStages - n;
+    break;
   }
   if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
   *ctas = c;
   *bslots = n;
-  *cstages = n;
-  *chunk = pipe_chunk();
-  *smem = kPipeBarrierBytes + (size_t)n * (BL.bytes + CL.bytes);
+  *cstages = n + xc;
+  *chunk = ch;
+  *smem = kPipeBarrierBytes + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
   const void* k = (const void*)csr_pipe_kernel<Epi>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
@@ -432,7 +447,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
     int bslots, cstages, ctas, chunk;
     size_t smem;
-    int rc = pipe_config<Epi>(L.ctx, m->xwin, &bslots, &cstages, &smem, &ctas, &chunk);
+    int rc = pipe_config<Epi>(L.ctx, m->xwin, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk);
     if (rc) {
       L.err = rc;
       return 0;
@@ -1281,6 +1296,11 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
     }
   }
   CK(cudaStreamSynchronize(s));
+  for (long long r0 = 0; r0 < n_rows; r0 += kPipeRows) {
+    const long long r1 = r0 + kPipeRows < n_rows ? r0 + kPipeRows : n_rows;
+    const long long bn = row_ptr[r1] - row_ptr[r0];
+    if (bn > m->blk_nnz_max) m->blk_nnz_max = bn;
+  }
   int rc = compute_xwin(ctx, m);
   if (rc) {
     pbs_mat_free(m);
