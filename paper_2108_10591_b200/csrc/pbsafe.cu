@@ -159,6 +159,18 @@ static int set_err(pbs_ctx* ctx, int code, const std::string& msg) {
       return set_err(ctx, PBS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
+// Large buffers come from the device's stream-ordered memory pool, which keeps
+// freed memory cached (release threshold = max): a solve on a host CsrMatrix
+// uploads and frees its operator and workspace every call, and plain
+// cudaFree of hundreds of MB can stall for hundreds of ms.
+template <class T>
+static cudaError_t pool_alloc(pbs_ctx* ctx, T** p, size_t bytes) {
+  return cudaMallocAsync((void**)p, bytes, ctx->stream);
+}
+static void pool_free(pbs_ctx* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
 static int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int cap_per_sm = 8) {
   auto it = ctx->occ.find(kernel);
   int per_sm;
@@ -182,6 +194,7 @@ constexpr int kMaxParts = 148 * 16;
 // ------------------------------------------------------------------ workspace
 
 struct Workspace {
+  pbs_ctx* ctx = nullptr;
   long long n = 0;
   size_t stride = 0;  // padded elements per vector
   double* base = nullptr;
@@ -213,14 +226,15 @@ static void free_graphs(Workspace* ws) {
 static void free_ws(Workspace* ws) {
   if (!ws) return;
   free_graphs(ws);
-  cudaFree(ws->base);
-  cudaFree(ws->partials);
-  cudaFree(ws->plan_bounds);
-  cudaFree(ws->st);
+  pbs_ctx* ctx = ws->ctx;
+  pool_free(ctx, ws->base);
+  pool_free(ctx, ws->partials);
+  pool_free(ctx, ws->plan_bounds);
+  pool_free(ctx, ws->st);
   if (ws->mirror_h) cudaFreeHost(ws->mirror_h);
-  cudaFree(ws->hist_rel);
-  cudaFree(ws->hist_flags);
-  cudaFree(ws->hist_coef);
+  pool_free(ctx, ws->hist_rel);
+  pool_free(ctx, ws->hist_flags);
+  pool_free(ctx, ws->hist_coef);
   if (ws->ev0) cudaEventDestroy(ws->ev0);
   if (ws->ev1) cudaEventDestroy(ws->ev1);
   if (ws->trace_host) cudaFreeHost(ws->trace_host);
@@ -232,33 +246,34 @@ static int ensure_ws(pbs_mat* m, long long hist_slots) {
   Workspace* ws = m->ws;
   if (!ws) {
     ws = new Workspace();
+    ws->ctx = ctx;
     m->ws = ws;
     ws->n = m->n_rows;
     ws->n_ext = m->part.dist ? m->n_cols : m->n_rows;
     ws->own_off = m->part.dist ? m->part.hl + (m->part.hl & 1) : 0;  // even: 16-byte aligned
     // +2: aligned bulk-copy over-read; even own offset keeps 16-byte alignment
     ws->stride = ((size_t)ws->n_ext + 4 + 31) / 32 * 32;
-    CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
-    CK(cudaMemset(ws->base, 0, sizeof(double) * ws->stride * kNumVecs));
+    CK(pool_alloc(ctx, &ws->base, sizeof(double) * ws->stride * kNumVecs));
+    CK(cudaMemsetAsync(ws->base, 0, sizeof(double) * ws->stride * kNumVecs, ctx->stream));
     for (int k = 0; k < kNumVecs; ++k) {
       ws->X.v[k] = ws->base + ws->stride * k;
       ws->V.v[k] = ws->X.v[k] + ws->own_off;
     }
-    CK(cudaMalloc(&ws->partials, sizeof(double) * kMaxParts * kPartStride));
-    CK(cudaMalloc(&ws->st, sizeof(SolverState)));
+    CK(pool_alloc(ctx, &ws->partials, sizeof(double) * kMaxParts * kPartStride));
+    CK(pool_alloc(ctx, &ws->st, sizeof(SolverState)));
     CK(cudaHostAlloc(&ws->mirror_h, sizeof(HostMirror), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ws->mirror_d, ws->mirror_h, 0));
     CK(cudaEventCreate(&ws->ev0));
     CK(cudaEventCreate(&ws->ev1));
   }
   if (hist_slots > ws->hist_cap) {
-    cudaFree(ws->hist_rel);
-    cudaFree(ws->hist_flags);
-    cudaFree(ws->hist_coef);
+    pool_free(ctx, ws->hist_rel);
+    pool_free(ctx, ws->hist_flags);
+    pool_free(ctx, ws->hist_coef);
     long long cap = hist_slots < 1024 ? 1024 : hist_slots;
-    CK(cudaMalloc(&ws->hist_rel, sizeof(double) * cap));
-    CK(cudaMalloc(&ws->hist_flags, cap));
-    CK(cudaMalloc(&ws->hist_coef, sizeof(double) * 4 * cap));
+    CK(pool_alloc(ctx, &ws->hist_rel, sizeof(double) * cap));
+    CK(pool_alloc(ctx, &ws->hist_flags, cap));
+    CK(pool_alloc(ctx, &ws->hist_coef, sizeof(double) * 4 * cap));
     ws->hist_cap = cap;
     free_graphs(ws);  // graphs capture the state pointer only, but keep it simple
   }
@@ -287,9 +302,10 @@ static int ensure_plan(pbs_mat* m, int workers) {
   std::vector<long long> b;
   int w = plan_balanced(ws->n, workers, b);
   if (w > kMaxParts) return set_err(ctx, PBS_ERR_INVALID, "plan_workers too large for the device plan");
-  cudaFree(ws->plan_bounds);
-  CK(cudaMalloc(&ws->plan_bounds, sizeof(long long) * (w + 1)));
-  CK(cudaMemcpy(ws->plan_bounds, b.data(), sizeof(long long) * (w + 1), cudaMemcpyHostToDevice));
+  pool_free(ctx, ws->plan_bounds);
+  CK(pool_alloc(ctx, &ws->plan_bounds, sizeof(long long) * (w + 1)));
+  CK(cudaMemcpyAsync(ws->plan_bounds, b.data(), sizeof(long long) * (w + 1), cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
   ws->plan_workers = workers;
   ws->plan_w_actual = w;
   free_graphs(ws);
@@ -1103,6 +1119,12 @@ PBS_EXPORT int pbs_init(int device, pbs_ctx** out) {
   }
   CK(cudaStreamCreateWithFlags(&ctx->own, cudaStreamNonBlocking));
   ctx->stream = ctx->own;
+  {
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = UINT64_MAX;  // keep freed blocks cached for the next upload
+    CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   CK(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * kPartStride));
   CK(cudaMalloc(&ctx->tmp_state, sizeof(SolverState)));
   *out = ctx;
@@ -1187,9 +1209,9 @@ static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   if (m->n_rows == 0 || m->nnz == 0 || m->n_cols > 0x7fffffffLL) return PBS_OK;
   cudaStream_t s = ctx->stream;
   int *bmin = nullptr, *bmax = nullptr, *wide = nullptr;
-  CK(cudaMalloc(&bmin, sizeof(int) * 2 * kBins));
-  CK(cudaMalloc(&bmax, sizeof(int) * 2 * kBins));
-  CK(cudaMalloc(&wide, sizeof(int)));
+  CK(pool_alloc(ctx, &bmin, sizeof(int) * 2 * kBins));
+  CK(pool_alloc(ctx, &bmax, sizeof(int) * 2 * kBins));
+  CK(pool_alloc(ctx, &wide, sizeof(int)));
   std::vector<int> hmin(2 * kBins, 0x7fffffff), hmax(2 * kBins, (int)0x80000000);
   CK(cudaMemcpyAsync(bmin, hmin.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(bmax, hmax.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
@@ -1200,9 +1222,9 @@ static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   CK(cudaMemcpyAsync(hmax.data(), bmax, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  cudaFree(bmin);
-  cudaFree(bmax);
-  cudaFree(wide);
+  pool_free(ctx, bmin);
+  pool_free(ctx, bmax);
+  pool_free(ctx, wide);
   if (hwide) return PBS_OK;
   std::vector<std::pair<int, int>> cl;  // [min, max] offsets
   for (int b = 0; b < 2 * kBins; ++b) {
@@ -1259,9 +1281,9 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
   m->nnz = nnz;
   cudaStream_t s = ctx->stream;
   // padding: the pipelined SpMV bulk-copies 16-byte-aligned windows
-  CK(cudaMalloc(&m->rp, sizeof(long long) * (n_rows + 4)));
-  CK(cudaMalloc(&m->ci, sizeof(int) * (nnz + 8)));
-  CK(cudaMalloc(&m->v, sizeof(double) * (nnz + 4)));
+  CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n_rows + 4)));
+  CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
+  CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
   CK(cudaMemsetAsync(m->rp + n_rows + 1, 0, sizeof(long long) * 3, s));
   CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
   CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
@@ -1275,8 +1297,8 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
       const long long chunk = 1LL << 24;
       long long* tmp = nullptr;
       int* bad = nullptr;
-      CK(cudaMalloc(&tmp, sizeof(long long) * (nnz < chunk ? nnz : chunk)));
-      CK(cudaMalloc(&bad, sizeof(int)));
+      CK(pool_alloc(ctx, &tmp, sizeof(long long) * (nnz < chunk ? nnz : chunk)));
+      CK(pool_alloc(ctx, &bad, sizeof(int)));
       CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
       for (long long off = 0; off < nnz; off += chunk) {
         long long len = nnz - off < chunk ? nnz - off : chunk;
@@ -1287,8 +1309,8 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
       int hbad = 0;
       CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      cudaFree(tmp);
-      cudaFree(bad);
+      pool_free(ctx, tmp);
+      pool_free(ctx, bad);
       if (hbad) {
         pbs_mat_free(m);
         return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
@@ -1366,9 +1388,9 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
   free_ws(m->ws);
-  cudaFree(m->rp);
-  cudaFree(m->ci);
-  cudaFree(m->v);
+  pool_free(m->ctx, m->rp);
+  pool_free(m->ctx, m->ci);
+  pool_free(m->ctx, m->v);
   delete m;
   return PBS_OK;
 }
