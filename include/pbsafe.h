@@ -155,6 +155,11 @@ int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
  * coeffs f64[npts].  npts <= 27. */
 int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t npts,
                        const int32_t* offsets, const double* coeffs, pbs_mat** mat);
+/* CSR of a stencil operator built on the device (rows in C order, columns
+ * ascending, out-of-grid neighbours dropped) — the same arrays as
+ * problems.stencil_csr builds on the host, without the host round trip
+ * (config 4's 1.5e9 nonzeros). */
+int pbs_stencil_to_csr(pbs_mat* stencil, pbs_mat** csr);
 int pbs_mat_free(pbs_mat* mat);
 int pbs_mat_info(pbs_mat* mat, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
                  int32_t* is_stencil);

@@ -35,7 +35,7 @@ EXPORTS = (
     "pbs_csr_upload", "pbs_stencil_create", "pbs_mat_free", "pbs_mat_info", "pbs_spmv_dev",
     "pbs_solve", "pbs_solve_dev", "pbs_step_dev", "pbs_k_spmv_range", "pbs_k_dot_range",
     "pbs_k_lincomb", "pbs_dot_batch_dev", "pbs_nccl_unique_id", "pbs_dist_init", "pbs_dist_destroy",
-    "pbs_mat_set_partition",
+    "pbs_mat_set_partition", "pbs_stencil_to_csr",
 )
 
 
@@ -119,6 +119,7 @@ def load(build_if_missing: bool = True):
             "pbs_dist_init": ([p, i32, i32, p, p, pp], C.c_int),
             "pbs_dist_destroy": ([p], C.c_int),
             "pbs_mat_set_partition": ([p, p, i64, i64, i64, i64, i32, p, i32, p], C.c_int),
+            "pbs_stencil_to_csr": ([p, pp], C.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -19,6 +19,7 @@
 #include <map>
 #include <thread>
 
+#include <cub/device/device_scan.cuh>
 #include <dlfcn.h>
 #include <nccl.h>  // types only: libnccl.so.2 is loaded at run time
 
@@ -1379,6 +1380,117 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
     nnz += cnt;
   }
   m->nnz = nnz;
+  *out = m;
+  return PBS_OK;
+}
+
+
+// ---- stencil -> CSR on the device
+__device__ __forceinline__ bool stencil_in(const StencilView& S, long long i, int p) {
+  int c[3] = {0, 0, 0};
+  if (S.dim == 3) {
+    const long long z = i / S.k2, rem = i - z * S.k2, yy = rem / S.k;
+    c[0] = (int)z;
+    c[1] = (int)yy;
+    c[2] = (int)(rem - yy * S.k);
+  } else if (S.dim == 2) {
+    const long long yy = i / S.k;
+    c[1] = (int)yy;
+    c[2] = (int)(i - yy * S.k);
+  } else {
+    c[2] = (int)i;
+  }
+  bool ok = true;
+  for (int a = 3 - S.dim; a < 3; ++a) {
+    const int cc = c[a] + S.off[p][a];
+    ok = ok && cc >= 0 && cc < S.k;
+  }
+  return ok;
+}
+
+__global__ void stencil_count_kernel(const __grid_constant__ StencilView S, long long* counts) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.n; i += stride) {
+    long long c = 0;
+    for (int p = 0; p < S.npts; ++p) c += stencil_in(S, i, p);
+    counts[i + 1] = c;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = 0;
+}
+
+__global__ void stencil_fill_kernel(const __grid_constant__ StencilView S, const long long* rp, int* ci,
+                                    double* v) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.n; i += stride) {
+    long long k = rp[i];
+    for (int p = 0; p < S.npts; ++p)
+      if (stencil_in(S, i, p)) {
+        ci[k] = (int)(i + S.foff[p]);
+        v[k] = S.coef[p];
+        ++k;
+      }
+  }
+}
+
+// most nonzeros in one kPipeRows-row block (chunk sizing of the CSR engine)
+__global__ void block_nnz_max_kernel(const long long* rp, long long n, unsigned long long* out) {
+  const long long nb = (n + kPipeRows - 1) / kPipeRows;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long b = (long long)blockIdx.x * blockDim.x + threadIdx.x; b < nb; b += stride) {
+    const long long r0 = b * kPipeRows, r1 = r0 + kPipeRows < n ? r0 + kPipeRows : n;
+    atomicMax(out, (unsigned long long)(rp[r1] - rp[r0]));
+  }
+}
+
+static int compute_xwin(pbs_ctx* ctx, pbs_mat* m);
+
+PBS_EXPORT int pbs_stencil_to_csr(pbs_mat* st, pbs_mat** out) {
+  if (!st || !out || !st->stencil) return set_err(st ? st->ctx : nullptr, PBS_ERR_INVALID, "need a stencil operator");
+  pbs_ctx* ctx = st->ctx;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t s = ctx->stream;
+  const long long n = st->n_rows, nnz = st->nnz;
+  if (nnz > 0x7fffffffffffLL) return set_err(ctx, PBS_ERR_INVALID, "too many nonzeros");
+  pbs_mat* m = new pbs_mat();
+  m->ctx = ctx;
+  m->n_rows = m->n_cols = n;
+  m->nnz = nnz;
+  CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n + 4)));
+  CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
+  CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
+  CK(cudaMemsetAsync(m->rp + n + 1, 0, sizeof(long long) * 3, s));
+  CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
+  CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
+  StencilView S = st->sv;
+  stencil_count_kernel<<<ctx->sms * 8, 256, 0, s>>>(S, m->rp);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, m->rp, m->rp, n + 1, s);
+  void* tmp = nullptr;
+  CK(pool_alloc(ctx, &tmp, tmp_bytes));
+  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, m->rp, m->rp, n + 1, s);
+  pool_free(ctx, tmp);
+  stencil_fill_kernel<<<ctx->sms * 8, 256, 0, s>>>(S, m->rp, m->ci, m->v);
+  unsigned long long* bmax = nullptr;
+  CK(pool_alloc(ctx, &bmax, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), s));
+  block_nnz_max_kernel<<<ctx->sms * 4, 256, 0, s>>>(m->rp, n, bmax);
+  unsigned long long hb = 0;
+  long long last = 0;
+  CK(cudaMemcpyAsync(&hb, bmax, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&last, m->rp + n, sizeof(last), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pool_free(ctx, bmax);
+  CK(cudaGetLastError());
+  if (last != nnz) {
+    pbs_mat_free(m);
+    return set_err(ctx, PBS_ERR_CUDA, "stencil CSR nonzero count mismatch");
+  }
+  m->blk_nnz_max = (long long)hb;
+  int rc = compute_xwin(ctx, m);
+  if (rc) {
+    pbs_mat_free(m);
+    return rc;
+  }
   *out = m;
   return PBS_OK;
 }

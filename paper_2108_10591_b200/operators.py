@@ -80,6 +80,14 @@ class DeviceMatrix:
         _lib.load().pbs_mat_info(h, C.byref(nr), C.byref(nc), C.byref(nnz), C.byref(st))
         return cls(h, ctx, nr.value, nc.value, nnz.value, True, f"stencil{spec.dim}d:{spec.npts}pt")
 
+    def to_csr(self) -> "DeviceMatrix":
+        """CSR of a stencil operator, built on the device (== problems.stencil_csr)."""
+        if not self.stencil:
+            raise ValueError("to_csr needs a stencil operator")
+        h = C.c_void_p()
+        _lib.check(_lib.load().pbs_stencil_to_csr(self.handle, C.byref(h)), self.ctx.handle)
+        return DeviceMatrix(h, self.ctx, self.n_rows, self.n_cols, self.nnz, False, self.source + "->csr")
+
     def spmv_dev(self, x_ptr: int, y_ptr: int) -> int:
         """y = A x on device pointers; returns the first non-finite row or -1."""
         bad = C.c_int64()

@@ -369,3 +369,27 @@ def test_c2_solve_converges_with_certificate(pb, c2):
         true = np.linalg.norm(b - orc.spmv(rp, ci, v, out.x)) / out.r0_norm
         assert true <= 1e-8, (method, true)
     dm.free()
+
+
+def test_device_stencil_csr_equals_host_generator(pb):
+    import torch  # noqa: F401
+
+    from paper_2108_10591_b200 import problems
+    from paper_2108_10591_b200.operators import DeviceMatrix
+
+    for st in (problems.config_stencil("c1"), problems.convdiff_stencil(3, 20, (100.0, 50.0, 25.0)),
+               problems.convdiff27_stencil(14, (1.0, 0.5, 0.25))):
+        rp, ci, v = problems.stencil_csr(st)
+        n = len(rp) - 1
+        csr = DeviceMatrix.from_stencil(st).to_csr()
+        assert csr.nnz == rp[-1]
+        # compare through SpMV on a random vector (bitwise) and b = A*1
+        x = np.random.default_rng(9).standard_normal(n)
+        import torch
+
+        xd = torch.from_numpy(x).cuda()
+        yd = torch.empty(n, dtype=torch.float64, device="cuda")
+        csr.spmv_dev(xd.data_ptr(), yd.data_ptr())
+        torch.cuda.synchronize()
+        assert np.array_equal(yd.cpu().numpy(), orc.spmv(rp, ci, v, x))
+        csr.free()
