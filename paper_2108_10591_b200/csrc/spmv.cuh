@@ -513,11 +513,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       const unsigned char* st = chk0 + (size_t)cs * CL.bytes;
       const ChunkHdr h = *reinterpret_cast<const ChunkHdr*>(st);
       if (t < nr) {
-        const double* vs = reinterpret_cast<const double*>(st + CL.v) + h.dv - h.c0;
-        const int* cis = reinterpret_cast<const int*>(st + CL.ci) + h.dci - h.c0;
-        const long long lo = max(my_s, h.c0), hi = min(my_e, h.c1);
+        // chunk-local indices: smem addressing stays 32-bit for any nnz
+        const double* vs = reinterpret_cast<const double*>(st + CL.v) + h.dv;
+        const int* cis = reinterpret_cast<const int*>(st + CL.ci) + h.dci;
+        const int lo = (int)(max(my_s, h.c0) - h.c0), hi = (int)(min(my_e, h.c1) - h.c0);
         constexpr int U = Epi::kGatherBatch;
-        for (long long k = lo; k < hi; k += U) {
+        for (int k = lo; k < hi; k += U) {
           double vv[U], xv[U];
 #pragma unroll
           for (int u = 0; u < U; ++u)
