@@ -1536,7 +1536,17 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
   e.y = d_y;
   e.st = ctx->tmp_state;
   e.tag = PBS_TAG_AX;
-  spmv_launch(L, d_x, e, 0, m->n_rows, KS);
+  const double* xin = d_x;
+  if (!m->stencil && m->xwin.nwin) {
+    // staged x windows are copied in 16-byte units and may read one element
+    // past the end of x: stage a caller's x into a padded buffer
+    double* xs = nullptr;
+    CK(pool_alloc(ctx, &xs, sizeof(double) * (m->n_cols + 4)));
+    CK(cudaMemcpyAsync(xs, d_x, sizeof(double) * m->n_cols, cudaMemcpyDeviceToDevice, ctx->stream));
+    xin = xs;
+  }
+  spmv_launch(L, xin, e, 0, m->n_rows, KS);
+  if (xin != d_x) pool_free(ctx, const_cast<double*>(xin));
   if (L.err) return L.err;
   unsigned long long row = 0;
   CK(cudaMemcpyAsync(&row, &ctx->tmp_state->nf_row, sizeof(row), cudaMemcpyDeviceToHost, ctx->stream));

@@ -404,11 +404,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
           long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
           if (lo < 0) lo = 0;
           if (hi > A.n_cols) hi = A.n_cols;
-          if (hi < lo) hi = lo;
-          const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
-          wlo[c] = loa;
-          wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
-          total += wbytes[c];
+          if (hi > lo) {  // an empty window (past either end of x) copies nothing
+            const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
+            wlo[c] = loa;
+            wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
+            total += wbytes[c];
+          } else {
+            wlo[c] = lo & ~1LL;
+          }
         }
       }
       mbar_wait(&bempty[bs], bph ^ 1);
