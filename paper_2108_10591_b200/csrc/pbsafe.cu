@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 #include <map>
+#include <algorithm>
 #include <thread>
 
 #include <cub/device/device_scan.cuh>
@@ -141,7 +142,8 @@ struct pbs_mat {
   int* ci = nullptr;
   double* v = nullptr;
   StencilView sv{};
-  XWin xwin{};  // x windows of the pipelined CSR engine (nwin = 0: gather x)
+  XWin xwin{};  // x windows of the pipelined engines (nwin = 0: gather x)
+  StencilWin swin{};  // stencil point -> window
   long long blk_nnz_max = 0;  // most nonzeros in one 256-row block (chunk sizing)
   Partition part;  // multi-GPU row partition (part.dist == nullptr: single GPU)
   Workspace* ws = nullptr;
@@ -446,6 +448,56 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, long long blk_nnz_max, int* 
   return PBS_OK;
 }
 
+static int stencil_engine_pipe() {  // PBS_STENCIL_ENGINE=direct: thread-per-row direct loads
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PBS_STENCIL_ENGINE");
+    v = (e && std::string(e) == "direct") ? 0 : 1;
+  }
+  return v;
+}
+
+template <class Epi, int DIM, int NP>
+static int stencil_pipe_set_smem(pbs_ctx* ctx, size_t smem) {
+  const void* k = (const void*)stencil_pipe_kernel<Epi, DIM, NP>;
+  auto it = ctx->occ.find(k);
+  if (it == ctx->occ.end() || (size_t)it->second < smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    ctx->occ[k] = (int)smem;
+  }
+  return PBS_OK;
+}
+
+template <class Epi>
+static int stencil_pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, size_t* smem, int* ctas) {
+  const BlockLayout BL(W.total, Epi::kIn);
+  int per_sm = 0, optin = 0;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  int n = 0, c = pipe_ctas_per_sm();
+  for (; c >= 1; --c) {
+    size_t budget = (size_t)per_sm / c - 1024 - 2048;
+    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
+    budget -= kPipeBarrierBytes;
+    n = (int)(budget / BL.bytes);
+    if (n > 4) n = 4;
+    if (n >= 2) break;
+  }
+  if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the stencil pipeline");
+  *ctas = c;
+  *bslots = n;
+  *smem = kPipeBarrierBytes + (size_t)n * BL.bytes;
+  int rc = stencil_pipe_set_smem<Epi, 3, 7>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 3, 27>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 3, 0>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 2, 5>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 2, 0>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 1, 3>(ctx, *smem);
+  if (!rc) rc = stencil_pipe_set_smem<Epi, 1, 0>(ctx, *smem);
+  return rc;
+}
+
 template <class Epi>
 static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long long hi, int kind) {
   pbs_mat* m = L.m;
@@ -472,6 +524,29 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages, chunk);
+  } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe()) {
+    StencilView S = m->sv;
+    S.row_lo = lo;
+    S.row_hi = hi;
+    int bslots, ctas;
+    size_t smem;
+    int rc = stencil_pipe_config<Epi>(L.ctx, m->xwin, &bslots, &smem, &ctas);
+    if (rc) {
+      L.err = rc;
+      return 0;
+    }
+    const long long cap = (long long)L.ctx->sms * ctas;
+    grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
+#define PBS_SPIPE(D, NP)                                                                                  \
+  stencil_pipe_kernel<Epi, D, NP><<<grid, kPipeThreads, smem, L.s>>>(S, x, epi, m->xwin, m->swin, bslots);
+    if (S.dim == 3 && S.npts == 7) PBS_SPIPE(3, 7)
+    else if (S.dim == 3 && S.npts == 27) PBS_SPIPE(3, 27)
+    else if (S.dim == 3) PBS_SPIPE(3, 0)
+    else if (S.dim == 2 && S.npts == 5) PBS_SPIPE(2, 5)
+    else if (S.dim == 2) PBS_SPIPE(2, 0)
+    else if (S.dim == 1 && S.npts == 3) PBS_SPIPE(1, 3)
+    else PBS_SPIPE(1, 0)
+#undef PBS_SPIPE
   } else {
     StencilView S = m->sv;
     S.row_lo = lo;
@@ -1380,6 +1455,38 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
     nnz += cnt;
   }
   m->nnz = nnz;
+  // x windows: cluster the flattened offsets like compute_xwin does for CSR
+  {
+    std::vector<std::pair<long long, int>> offs;
+    for (int q = 0; q < npts; ++q) offs.push_back({S.foff[q], q});
+    std::sort(offs.begin(), offs.end());
+    std::vector<std::pair<long long, long long>> cl;
+    std::vector<int> owner(npts);
+    for (auto& o : offs) {
+      if (!cl.empty() && o.first - cl.back().second <= kPipeRows + 4)
+        cl.back().second = o.first;
+      else
+        cl.push_back({o.first, o.first});
+      owner[o.second] = (int)cl.size() - 1;
+    }
+    XWin W{};
+    long long total = 0;
+    if (cl.size() <= (size_t)kMaxWin) {
+      for (size_t c = 0; c < cl.size(); ++c) {
+        W.wmin[c] = (int)cl[c].first;
+        W.wmax[c] = (int)cl[c].second;
+        long long cap = ((long long)kPipeRows + cl[c].second - cl[c].first + 4 + 1) & ~1LL;
+        W.cap[c] = (int)cap;
+        total += cap;
+      }
+      if (total <= kMaxWinElems) {
+        W.nwin = (int)cl.size();
+        W.total = (int)total;
+        m->xwin = W;
+        for (int q = 0; q < npts; ++q) m->swin.pw[q] = owner[q];
+      }
+    }
+  }
   *out = m;
   return PBS_OK;
 }
@@ -1537,7 +1644,7 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
   e.st = ctx->tmp_state;
   e.tag = PBS_TAG_AX;
   const double* xin = d_x;
-  if (!m->stencil && m->xwin.nwin) {
+  if (m->xwin.nwin) {
     // staged x windows are copied in 16-byte units and may read one element
     // past the end of x: stage a caller's x into a padded buffer
     double* xs = nullptr;

@@ -568,6 +568,179 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   e.template finish<kPipeRows, true>();
 }
 
+// ---------------------------------------------- stencil pipelined engine
+
+// Matrix-free counterpart of csr_pipe_kernel: the producer warp stages, per
+// 256-row block, the x windows the stencil reaches (one per offset cluster:
+// the z-1 / z / z+1 plane slices of a 3D stencil) and the epilogue inputs
+// into a ring of block slots with bulk async copies; consumers compute their
+// row from shared memory, neighbours in ascending flattened offset (the CSR
+// column order), so the result is bitwise the CSR engine's.
+struct StencilWin {
+  int pw[kMaxStencil];  // window of each stencil point
+};
+
+template <class Epi, int DIM, int NP>
+__global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __grid_constant__ StencilView S,
+                                                                       const double* __restrict__ x, Epi epi,
+                                                                       XWin W, StencilWin SW, int bslots) {
+  __shared__ int go;
+  if (threadIdx.x == 0) {
+    go = epi.active();
+    if (!go && blockIdx.x == 0) epi.on_skip();
+  }
+  __syncthreads();
+  if (!go) return;
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* bempty = bfull + kMaxStages;
+  const BlockLayout BL(W.total, Epi::kIn);
+  unsigned char* blk0 = smem + kPipeBarrierBytes;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < bslots; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const long long nrows = S.row_hi - S.row_lo;
+  const long long nblk = (nrows + kPipeRows - 1) / kPipeRows;
+  if (warp == kConsumerWarps) {
+    int bs = 0;
+    uint32_t bph = 0;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+      const long long r0 = S.row_lo + blk * kPipeRows;
+      const long long r0a = r0 & ~1LL;
+      const int nr = (int)min((long long)kPipeRows, S.row_hi - r0);
+      const int dr = (int)(r0 - r0a);
+      const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
+      long long wlo[kMaxWin];
+      uint32_t wbytes[kMaxWin];
+      uint32_t total = Epi::kIn * bin;
+#pragma unroll
+      for (int c = 0; c < kMaxWin; ++c) {
+        wlo[c] = 0x7fffffff;
+        wbytes[c] = 0;
+        if (c < W.nwin) {
+          long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
+          if (lo < 0) lo = 0;
+          if (hi > S.n) hi = S.n;
+          if (hi > lo) {
+            const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
+            wlo[c] = loa;
+            wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
+            total += wbytes[c];
+          } else {
+            wlo[c] = lo & ~1LL;
+          }
+        }
+      }
+      mbar_wait(&bempty[bs], bph ^ 1);
+      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+      if (lane == 0) {
+        BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
+        bh->r0 = r0;
+        bh->nr = nr;
+        bh->dr = dr;
+#pragma unroll
+        for (int c = 0; c < kMaxWin; ++c) bh->ws[c] = wlo[c];
+        mbar_arrive_expect_tx(&bfull[bs], total);
+      }
+      __syncwarp();
+      if (lane >= 1 && lane <= W.nwin) {
+        int soff = 0;
+#pragma unroll
+        for (int cc = 0; cc < kMaxWin; ++cc) {
+          if (cc == lane - 1 && wbytes[cc])
+            bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
+          soff += cc < W.nwin ? W.cap[cc] : 0;
+        }
+      } else if (lane >= 8 && lane < 8 + Epi::kIn) {
+        const int e = lane - 8;
+        bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
+      }
+      if (total == 0 && lane == 0) mbar_arrive(&bfull[bs]);  // unreachable with kIn > 0 or windows
+      if (++bs == bslots) {
+        bs = 0;
+        bph ^= 1;
+      }
+    }
+    return;
+  }
+  Epi e = epi;
+  e.init();
+  const int t = threadIdx.x;
+  int bs = 0;
+  uint32_t bph = 0;
+  const int npts = NP > 0 ? NP : S.npts;
+  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+    mbar_wait(&bfull[bs], bph);
+    const unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+    const BlockHdr* bhp = reinterpret_cast<const BlockHdr*>(bst);
+    const int nr = bhp->nr, dr = bhp->dr;
+    const long long r0 = bhp->r0;
+    if (t < nr) {
+      const long long i = r0 + t;
+      int c[3] = {0, 0, 0};
+      if (DIM == 3) {
+        const long long z = i / S.k2;
+        const long long rem = i - z * S.k2;
+        const long long yy = rem / S.k;
+        c[0] = (int)z;
+        c[1] = (int)yy;
+        c[2] = (int)(rem - yy * S.k);
+      } else if (DIM == 2) {
+        const long long yy = i / S.k;
+        c[1] = (int)yy;
+        c[2] = (int)(i - yy * S.k);
+      } else {
+        c[2] = (int)i;
+      }
+      // window base per cluster: x[col] = xw[col - wsb[w]]
+      const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
+      int wsb[kMaxWin];
+      {
+        int soff = 0;
+#pragma unroll
+        for (int cc = 0; cc < kMaxWin; ++cc) {
+          wsb[cc] = cc < W.nwin ? (int)bhp->ws[cc] - soff : 0;
+          soff += cc < W.nwin ? W.cap[cc] : 0;
+        }
+      }
+      const int km1 = (int)S.k - 1;
+      double acc = 0.0;
+#pragma unroll
+      for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
+        if (NP == 0 && p >= npts) break;
+        bool ok = true;
+#pragma unroll
+        for (int a = 3 - DIM; a < 3; ++a) {
+          const int cc = c[a] + S.off[p][a];
+          ok = ok && cc >= 0 && cc <= km1;
+        }
+        if (ok) {
+          const int col = (int)(i + S.foff[p]);
+          acc = add(acc, mul(S.coef[p], xw[col - wsb[SW.pw[p]]]));
+        }
+      }
+      double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+      const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
+#pragma unroll
+      for (int k = 0; k < Epi::kIn; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+      e.row(i, acc, inr);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bempty[bs]);
+    if (++bs == bslots) {
+      bs = 0;
+      bph ^= 1;
+    }
+  }
+  e.template finish<kPipeRows, true>();
+}
+
 // ------------------------------------------- CSR thread-per-row engine
 
 // One thread per row at full occupancy (no shared memory, so L1 keeps the
