@@ -448,13 +448,17 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, long long blk_nnz_max, int* 
   return PBS_OK;
 }
 
-static int stencil_engine_pipe() {  // PBS_STENCIL_ENGINE=direct: thread-per-row direct loads
+// PBS_STENCIL_ENGINE=direct|pipe forces one stencil engine; default: per
+// epilogue (Epi::kStencilPipe — the staged engine for the dot-carrying K3,
+// the L1-cached direct engine for the streaming K12)
+template <class Epi>
+static bool stencil_engine_pipe() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PBS_STENCIL_ENGINE");
-    v = (e && std::string(e) == "direct") ? 0 : 1;
+    v = (e && std::string(e) == "direct") ? 0 : ((e && std::string(e) == "pipe") ? 1 : 2);
   }
-  return v;
+  return v == 2 ? Epi::kStencilPipe : v == 1;
 }
 
 template <class Epi, int DIM, int NP>
@@ -524,7 +528,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages, chunk);
-  } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe()) {
+  } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>()) {
     StencilView S = m->sv;
     S.row_lo = lo;
     S.row_hi = hi;
@@ -1468,6 +1472,21 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
       else
         cl.push_back({o.first, o.first});
       owner[o.second] = (int)cl.size() - 1;
+    }
+    while (cl.size() > (size_t)kMaxWin) {  // merge across the smallest gap (plane rows -> planes)
+      size_t best = 0;
+      long long gap = -1;
+      for (size_t q = 0; q + 1 < cl.size(); ++q) {
+        long long g = cl[q + 1].first - cl[q].second;
+        if (gap < 0 || g < gap) {
+          gap = g;
+          best = q;
+        }
+      }
+      cl[best].second = cl[best + 1].second;
+      cl.erase(cl.begin() + best + 1);
+      for (auto& o : owner)
+        if (o > (int)best) --o;
     }
     XWin W{};
     long long total = 0;

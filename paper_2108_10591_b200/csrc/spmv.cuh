@@ -91,6 +91,8 @@ struct DotSink {
 
 struct EpiStore {
   static constexpr int kIn = 0;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double* y;
   SolverState* st;
@@ -110,6 +112,8 @@ struct EpiStore {
 
 struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
   static constexpr int kIn = 1;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double* r;
   double* r0s;  // nullable: also r0s = r (solvers.py:617)
@@ -130,6 +134,8 @@ struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
 
 struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   static constexpr int kIn = 4;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 2;  // x gathers in flight per row
   double* s;
   SolverState* st;
@@ -152,6 +158,8 @@ struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
 
 struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local K2 updates)
   static constexpr int kIn = 11;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double* as;  // As is kept for K3
   double *p, *u, *w, *t, *z, *y, *x, *r;
@@ -204,6 +212,8 @@ struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local
 
 struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
   static constexpr int kIn = 8;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 2;  // x gathers in flight per row
   double *l, *g, *s;
   double* q_out;  // nullable (single-step parity: expose q)
@@ -244,6 +254,8 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
 
 struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:569-580)
   static constexpr int kIn = 8;
+  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double *w, *t, *z, *y, *x, *r;
   SolverState* st;
@@ -802,7 +814,7 @@ __global__ void __launch_bounds__(kThreads, LATE ? 4 : 1) csr_tpr_kernel(CsrView
 
 // NP > 0: compile-time point count (fully unrolled); NP == 0: runtime npts
 template <class Epi, int DIM, int NP>
-__global__ void __launch_bounds__(kThreads) stencil_spmv_kernel(const __grid_constant__ StencilView S,
+__global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel(const __grid_constant__ StencilView S,
                                                                 const double* __restrict__ x, Epi epi) {
   __shared__ int go;
   if (threadIdx.x == 0) {

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--graphs", action="store_true")
     ap.add_argument("--repeat", type=int, default=1)
     ap.add_argument("--timing", action="store_true", help="per-kernel CUDA-event breakdown")
+    ap.add_argument("--reduce", default="tree", choices=("tree", "plan"))
+    ap.add_argument("--workers", type=int, default=1)
     args = ap.parse_args()
     import torch
 
@@ -47,7 +49,8 @@ def main():
     cfg = pb.SolverConfig(tol=1e-30, max_iters=args.iters)
     for _ in range(args.repeat):
         out = pb.solve(dm, bh, method=args.method, config=cfg,
-                       engine=pb.DeviceEngine(use_graphs=args.graphs, timing=args.timing))
+                       engine=pb.DeviceEngine(use_graphs=args.graphs, timing=args.timing,
+                                              reduce=args.reduce, workers=args.workers))
     extra = ""
     if args.timing:
         kc = out.device["kernel_count"]
