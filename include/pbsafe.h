@@ -111,6 +111,13 @@ typedef struct {
   int32_t pad;
   pbs_trace_fn trace_fn; /* NULL: no tracing */
   void* trace_user;
+  /* schedule evidence (multi-GPU schedule, timing mode): records of
+   * (iter, kind, tag, t_ms) as 4 doubles, kind 0 reduce_start 1 reduce_end
+   * 2 spmv_start 3 spmv_end 4 coeff_ready, tag = PBS_TAG_* (spmv) or 0;
+   * t_ms from the solve's first event.  NULL: off. */
+  double* events_out;
+  int64_t events_cap;
+  int64_t* events_count;
 } pbs_config;
 
 #define PBS_NUM_KERNEL_KINDS 8 /* K1 As, K2 update, K3 Aw+epilogue, F finalize,

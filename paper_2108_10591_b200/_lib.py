@@ -58,6 +58,7 @@ class Config(C.Structure):
         ("rr_cutoff", C.c_int64), ("record_history", C.c_int32), ("reduce_mode", C.c_int32),
         ("plan_workers", C.c_int32), ("use_graphs", C.c_int32), ("timing", C.c_int32),
         ("pad", C.c_int32), ("trace_fn", TRACE_FN), ("trace_user", C.c_void_p),
+        ("events_out", C.c_void_p), ("events_cap", C.c_int64), ("events_count", C.POINTER(C.c_int64)),
     ]
 
 

@@ -333,6 +333,19 @@ struct Launcher {
   long long iter = 0;
   int trace_rc = 0;
   int err = 0;  // first launch-configuration failure (sticky)
+  // schedule evidence: (iter, kind, tag, event) — resolved to times at the end
+  struct Ev {
+    long long iter;
+    int kind, tag;
+    cudaEvent_t e;
+  };
+  std::vector<Ev>* evidence = nullptr;
+  void mark(cudaStream_t st, long long it, int kind, int tag) {
+    if (!evidence) return;
+    cudaEvent_t e = ctx->events.get();
+    cudaEventRecord(e, st);
+    evidence->push_back({it, kind, tag, e});
+  }
   void trace_point();
   void done(int kind) {
     ++launches;
@@ -833,6 +846,7 @@ static void dist_check(Launcher& L, Workspace* ws, pbs_mat* m, int nparts, int r
   L.done(KD);
   cudaEventRecord(D->ev_part, L.s);
   cudaStreamWaitEvent(D->comm, D->ev_part, 0);
+  L.mark(D->comm, L.iter, 0, 0);  // reduce_start
   ncclResult_t r = nccl().AllGather(D->sendbuf, D->recvbuf, kPartStride, ncclDouble, D->red, D->comm);
   if (r != ncclSuccess) {
     L.err = set_err(L.ctx, PBS_ERR_NCCL, std::string("all-gather: ") + nccl().GetErrorString(r));
@@ -840,6 +854,8 @@ static void dist_check(Launcher& L, Workspace* ws, pbs_mat* m, int nparts, int r
   }
   finalize_kernel<<<1, 288, 0, D->comm>>>(ws->st, D->recvbuf, D->nranks, 0, replaced);
   L.done(KF);
+  L.mark(D->comm, L.iter, 1, 0);  // reduce_end
+  L.mark(D->comm, L.iter, 4, 0);  // coeff_ready
   cudaEventRecord(D->ev_coef, D->comm);
 }
 
@@ -854,13 +870,17 @@ static void dist_setup(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md) {
 static void dist_iter(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md, bool replace) {
   pbs_dist* D = m->part.dist;
   halo_exchange(L, ws, m, VS);
+  L.mark(L.s, L.iter, 2, PBS_TAG_AS);
   spmv_launch(L, ws->X.v[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
+  L.mark(L.s, L.iter, 3, PBS_TAG_AS);
   cudaStreamWaitEvent(L.s, D->ev_coef, 0);  // coefficients of this check
   int np;
   if (!replace) {
     vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
     halo_exchange(L, ws, m, VW);
+    L.mark(L.s, L.iter, 2, PBS_TAG_AW);
     np = spmv_launch(L, ws->X.v[VW], epi_k3(ws, md, 0), 0, ws->n, KK3);
+    L.mark(L.s, L.iter, 3, PBS_TAG_AW);
   } else {
     vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
     halo_exchange(L, ws, m, VO);
@@ -877,7 +897,9 @@ static void dist_iter(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md, bo
     halo_exchange(L, ws, m, VR);
     np = spmv_launch(L, ws->X.v[VR], epi_dots(ws, md, 0, 0, 1), 0, ws->n, KRS);
   }
+  ++L.iter;  // this batch / check is iteration j+1's (solvers.py:641)
   dist_check(L, ws, m, np, replace ? 1 : 0);
+  --L.iter;
 }
 
 // ------------------------------------------------------------------- solving
@@ -1100,6 +1122,8 @@ static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
   Launcher L{ctx, m, s};
   L.timing = cfg->timing != 0;
   L.marks = &marks;
+  std::vector<Launcher::Ev> evidence;
+  if (cfg->events_out && cfg->events_cap > 0) L.evidence = &evidence;
   const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
   const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
   int* flags = nullptr;  // [2] local, [2*nranks] gathered
@@ -1115,6 +1139,7 @@ static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
     const long long jend = j + chunk < cfg->max_iters ? j + chunk : cfg->max_iters;
     for (; j < jend && !L.err; ++j) {
       const bool replace = rr && (j % cfg->rr_epoch == 0) && 0 < j && j < cutoff;
+      L.iter = j;
       dist_iter(L, ws, m, md, replace);
     }
     if (L.err) break;
@@ -1149,6 +1174,20 @@ static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
   CK(cudaStreamSynchronize(s));
   CK(cudaStreamSynchronize(D->comm));
   CK(cudaGetLastError());
+  if (L.evidence) {
+    long long k = 0;
+    for (auto& ev : evidence) {
+      if (k >= cfg->events_cap) break;
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ws->ev0, ev.e);
+      cfg->events_out[4 * k + 0] = (double)ev.iter;
+      cfg->events_out[4 * k + 1] = ev.kind;
+      cfg->events_out[4 * k + 2] = ev.tag;
+      cfg->events_out[4 * k + 3] = t;
+      ++k;
+    }
+    if (cfg->events_count) *cfg->events_count = k;
+  }
   rc = collect_result(m, method, cfg, res, L, marks, 0);
   if (rc == PBS_OK && any_err) {  // another rank raised: raise here too
     res->nonfinite_tag = PBS_TAG_AS;

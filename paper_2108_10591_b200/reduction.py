@@ -103,3 +103,45 @@ class EventLog:
                 row = json.loads(line)
                 log._events.append(ExecutionEvent(row["seq"], row["iter"], row["kind"], row.get("tag")))
         return log
+
+
+_KINDS = {0: REDUCE_START, 1: REDUCE_END, 2: SPMV_START, 3: SPMV_END, 4: COEFF_READY}
+_TAGS = {0: None, 1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay"}
+
+
+def events_to_log(records) -> EventLog:
+    """Device schedule records (iter, kind, tag, t_ms) -> the reference's EventLog.
+
+    seq follows the CUDA-event timestamps (ties keep issue order), so the
+    reference's verify_phase_order (reduction.py:486-563) can be re-run on it.
+    """
+    recs = [(float(t), k, int(i), int(kind), int(tag)) for k, (i, kind, tag, t) in enumerate(records)]
+    recs.sort(key=lambda r: (r[0], r[1]))
+    log = EventLog()
+    for t, _, i, kind, tag in recs:
+        log.append(i, _KINDS[kind], _TAGS.get(tag))
+    return log
+
+
+def overlap_report(records) -> dict:
+    """Per iteration: the reduction's [start, end] vs the As SpMV's [start, end]
+    (CUDA-event ms).  overlapped = the intervals intersect, i.e. the
+    all-gather + check really ran while A s was computed."""
+    per: dict[int, dict] = {}
+    for i, kind, tag, t in records:
+        d = per.setdefault(int(i), {})
+        if kind == 0:
+            d["r0"] = t
+        elif kind == 1:
+            d["r1"] = t
+        elif kind == 2 and int(tag) == 3:
+            d["a0"] = t
+        elif kind == 3 and int(tag) == 3:
+            d["a1"] = t
+    out = {}
+    for i, d in sorted(per.items()):
+        if {"r0", "r1", "a0", "a1"} <= d.keys():
+            inter = min(d["r1"], d["a1"]) - max(d["r0"], d["a0"])
+            out[i] = {"reduce_ms": d["r1"] - d["r0"], "as_ms": d["a1"] - d["a0"],
+                      "overlap_ms": max(inter, 0.0), "overlapped": inter > 0}
+    return out

@@ -124,6 +124,7 @@ class DeviceEngine:
     workers: int = 1
     use_graphs: bool = True
     timing: bool = False
+    evidence: bool = False  # record the schedule as an EventLog (multi-GPU schedule)
 
     def __post_init__(self):
         if self.reduce not in ("tree", "plan"):
@@ -191,7 +192,15 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
         cfg.reduce_mode = _lib.REDUCE_PLAN if eng.reduce == "plan" else _lib.REDUCE_TREE
         cfg.plan_workers = eng.workers
         cfg.use_graphs = 1 if eng.use_graphs else 0
-        cfg.timing = 1 if eng.timing else 0
+        cfg.timing = 1 if (eng.timing or eng.evidence) else 0
+        ev_buf = ev_cnt = None
+        if eng.evidence:
+            ev_cap = 8 * (config.max_iters + 2)
+            ev_buf = np.zeros((ev_cap, 4))
+            ev_cnt = C.c_int64(0)
+            cfg.events_out = ev_buf.ctypes.data_as(C.c_void_p)
+            cfg.events_cap = ev_cap
+            cfg.events_count = C.pointer(ev_cnt)
         cb_keep = None
         if trace_hook is not None:
             def _cb(i, vecs, _user):
@@ -245,6 +254,8 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
         "kernel_count": {name: int(res.kernel_count[j]) for j, name in enumerate(_lib.KERNEL_KINDS)},
         "reduce": eng.reduce,
     }
+    if ev_buf is not None:
+        device["events"] = ev_buf[: ev_cnt.value].copy()
     return SolveOutcome(
         status=status,
         iterations=iterations,

@@ -58,3 +58,46 @@ def test_partitioned_nonfinite_raises():
             sysd.solve(np.ones(n))
     finally:
         sysd.close()
+
+
+def test_overlap_evidence_in_reference_event_format():
+    """the schedule as the reference's EventLog, plus real overlap.
+
+    Per iteration >= 1 the reference's verifier requires exactly one
+    reduce_start and reduce_start before the end of the As product
+    (reduction.py:486-563, test_acceptance.py:248-288).  CUDA-event times
+    also show the all-gather + check interval intersecting the As interval.
+    """
+    import paper_2108_10591_b200 as pb
+    from paper_2108_10591_b200 import problems
+    from paper_2108_10591_b200.distributed import DistributedSystem
+    from paper_2108_10591_b200.reduction import REDUCE_START, SPMV_END, events_to_log, overlap_report
+
+    st = problems.convdiff_stencil(3, 96, (1.0, 0.5, 0.25))
+    rp, ci, v = problems.stencil_csr(st)
+    n = len(rp) - 1
+    b = orc.spmv(rp, ci, v, np.ones(n))
+    sysd = DistributedSystem(rp, ci, v, n)
+    try:
+        out = sysd.solve(b, config=pb.SolverConfig(tol=1e-30, max_iters=40),
+                         engine=pb.DeviceEngine(evidence=True))
+    finally:
+        sysd.close()
+    recs = out.device["events"]
+    log = events_to_log(recs)
+    by_iter = {}
+    for ev in log.events():
+        by_iter.setdefault(ev.iter, []).append(ev)
+    checked = 0
+    for it, evs in sorted(by_iter.items()):
+        starts = [e.seq for e in evs if e.kind == REDUCE_START]
+        as_end = [e.seq for e in evs if e.kind == SPMV_END and e.tag == "As"]
+        if not as_end:
+            continue  # the final check has no As product
+        assert len(starts) == 1, (it, starts)
+        assert starts[0] < as_end[0], it
+        checked += 1
+    assert checked >= 39
+    rep = overlap_report(recs)
+    frac = sum(r["overlapped"] for r in rep.values()) / max(len(rep), 1)
+    assert frac >= 0.5, rep
