@@ -662,6 +662,41 @@ static EpiK12 epi_k12(Workspace* ws, const Mode& md) {
   return e;
 }
 
+static EpiK3n epi_k3n(Workspace* ws, const Mode& md) {
+  EpiK3n e{};
+  auto& V = ws->V.v;
+  e.l = V[VL];
+  e.g = V[VG];
+  e.s = V[VS];
+  e.q_out = md.store_temps ? V[VQ] : nullptr;
+  e.st = ws->st;
+  const int in[4] = {VAS, VL, VG, VS};
+  for (int k = 0; k < 4; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+// K3's batch as a separate kernel (PBS_K3_DOTS=split, the default) or fused
+// into K3's epilogue (=fused)
+static bool k3_dots_split() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PBS_K3_DOTS");
+    v = (e && std::string(e) == "fused") ? 0 : 1;
+  }
+  return v;
+}
+
+// the next check's batch as a streaming kernel; returns nparts
+static int dots_check(Launcher& L, Workspace* ws, int fuse, int replaced) {
+  auto& V = ws->V.v;
+  long long nblk = (ws->n + kThreads - 1) / kThreads;
+  int np = grid_for(L.ctx, (const void*)dots9_check_kernel, nblk);
+  dots9_check_kernel<<<np, kThreads, 0, L.s>>>(ws->n, V[VS], V[VY], V[VR], V[VR0S], V[VT], ws->partials,
+                                               ws->st, fuse, replaced);
+  L.done(KD);
+  return np;
+}
+
 static EpiK3 epi_k3(Workspace* ws, const Mode& md, int fuse) {
   EpiK3 e{};
   auto& V = ws->V.v;
@@ -724,6 +759,15 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
   spmv_launch(L, ws->X.v[VS], epi_k12(ws, md), 0, ws->n, KK1);
+  if (!md.plan && k3_dots_split()) {
+    spmv_launch(L, ws->X.v[VW], epi_k3n(ws, md), 0, ws->n, KK3);
+    const int np = dots_check(L, ws, L.trace_cfg ? 0 : 1, 0);
+    if (L.trace_cfg) {
+      L.trace_point();
+      finalize(L, ws, np, 0, 0);
+    }
+    return;
+  }
   const int grid = spmv_launch(L, ws->X.v[VW], epi_k3(ws, md, L.trace_cfg ? 0 : 1), 0, ws->n, KK3);
   if (md.plan) {
     int np = plan_dots(L, ws, KD);

@@ -210,8 +210,11 @@ struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local
   __device__ void finish() {}
 };
 
-struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
-  static constexpr int kIn = 8;
+// block 2 of the pipelined iteration; DOTS: also the next iteration's batch
+// (else a separate streaming kernel computes it, and K3 needs 4 fewer inputs)
+template <bool DOTS>
+struct EpiK3T {
+  static constexpr int kIn = DOTS ? 8 : 4;
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 2;  // x gathers in flight per row
@@ -219,7 +222,7 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
   double* q_out;  // nullable (single-step parity: expose q)
   SolverState* st;
   DotSink sink;
-  const double* in[kIn];  // As l g s y r r0s t
+  const double* in[8];  // As l g s (y r r0s t)
   double alpha, beta, zeta, eta;
   Dots9 d;
   __device__ bool active() const { return gate_all(st); }
@@ -229,7 +232,7 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
     if (!dev_err(st) && !st->run_all) st->run_spine = 0;
   }
   __device__ void init() {
-    d.zero();
+    if (DOTS) d.zero();
     alpha = st->alpha;
     beta = st->beta;
     zeta = st->zeta;
@@ -246,11 +249,16 @@ struct EpiK3 {  // block 2 of the pipelined iteration, fused with the next batch
     g[i] = gv;
     s[i] = sv;
     if (q_out) q_out[i] = q;
-    if (sink.partials) d.add_row(sv, v[4], v[5], v[6], v[7]);
+    if (DOTS && sink.partials) d.add_row(sv, v[4], v[5], v[6], v[7]);
   }
   template <int NT, bool NAMED>
-  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+  __device__ void finish() {
+    if (DOTS) sink.finish<NT, NAMED>(d, st);
+  }
 };
+using EpiK3 = EpiK3T<true>;
+using EpiK3n = EpiK3T<false>;
+
 
 struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:569-580)
   static constexpr int kIn = 8;

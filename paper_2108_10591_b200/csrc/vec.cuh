@@ -176,6 +176,39 @@ __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const
   block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
 }
 
+// The batch of the next check as its own streaming kernel (s y r r0s t ->
+// 9 compensated dots), with the check fused into the last CTA's tail.
+__global__ void __launch_bounds__(kThreads) dots9_check_kernel(long long n, const double* __restrict__ s,
+                                                               const double* __restrict__ y,
+                                                               const double* __restrict__ r,
+                                                               const double* __restrict__ r0s,
+                                                               const double* __restrict__ t, double* partials,
+                                                               SolverState* st, int fuse, int replaced) {
+  __shared__ int go;
+  if (threadIdx.x == 0) go = gate_all(st);
+  __syncthreads();
+  if (!go) return;
+  Ddbl acc[kNumDots];
+#pragma unroll
+  for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double sv = __ldcs(s + i), yv = __ldcs(y + i), rv = __ldcs(r + i), r0 = __ldcs(r0s + i),
+                 tv = __ldcs(t + i);
+    acc[DA] = dot2_step(acc[DA], sv, sv);
+    acc[DB] = dot2_step(acc[DB], yv, yv);
+    acc[DC] = dot2_step(acc[DC], sv, yv);
+    acc[DD] = dot2_step(acc[DD], sv, rv);
+    acc[DE] = dot2_step(acc[DE], yv, rv);
+    acc[DF] = dot2_step(acc[DF], r0, rv);
+    acc[DG] = dot2_step(acc[DG], r0, sv);
+    acc[DH] = dot2_step(acc[DH], r0, tv);
+    acc[DR] = dot2_step(acc[DR], rv, rv);
+  }
+  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
+  if (fuse) finalize_tail<kThreads, false>(st, partials, gridDim.x, replaced);
+}
+
 // PartitionPlan chains (reduction.py:282-283 with kernels.py:103-107): block w
 // handles range [bounds[w], bounds[w+1]); thread j < 9 sums pair j
 // sequentially in ascending index order -> partials[w*kPartStride + 2j].
