@@ -675,13 +675,14 @@ static EpiK3n epi_k3n(Workspace* ws, const Mode& md) {
   return e;
 }
 
-// K3's batch as a separate kernel (PBS_K3_DOTS=split, the default) or fused
-// into K3's epilogue (=fused)
+// K3's batch fused into K3's epilogue (default) or as a separate streaming
+// kernel (PBS_K3_DOTS=split; slower on B200: the compensated FP64 batch hides
+// better under K3's memory traffic, profiles/r1_engine_sweep.log)
 static bool k3_dots_split() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PBS_K3_DOTS");
-    v = (e && std::string(e) == "fused") ? 0 : 1;
+    v = (e && std::string(e) == "split") ? 1 : 0;
   }
   return v;
 }
