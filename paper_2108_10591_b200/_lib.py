@@ -78,7 +78,8 @@ _lock = threading.Lock()
 
 
 def lib_path() -> str:
-    return _build.LIB
+    # PBS_LIB: an alternative build of the same library (engine sweeps)
+    return os.environ.get("PBS_LIB") or _build.LIB
 
 
 def load(build_if_missing: bool = True):

@@ -19,7 +19,8 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpbsafe.so")
 SOURCES = [os.path.join(CSRC, "pbsafe.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "spmv.cuh", "vec.cuh")] + [
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "spmv.cuh", "vec.cuh", "finalize.cuh",
+                                                  "ptx.cuh")] + [
     os.path.join(ROOT, "include", "pbsafe.h")]
 
 

@@ -19,11 +19,21 @@ constexpr int kThreads = 256;          // CTA size of every streaming kernel
 constexpr int kChunk = 2048;           // CSR products staged per smem chunk (16 KiB)
 constexpr int kNumDots = 9;            // a b c d e f g h r  (reduction.py:32)
 constexpr int kPartStride = 2 * kNumDots;  // doubles per partial record (double-double)
+// Partial-record buffers hold up to kMaxParts records stored field-major:
+// field f of record b at p[f * kMaxParts + b], so a warp reading one field of
+// consecutive records is coalesced.
+constexpr int kMaxParts = 148 * 16;
 constexpr int kMaxStencil = 27;
 constexpr long long kNoError = 0x7fffffffffffffffLL;
 
 // dot slots in BATCH_LABELS order; _safe_batch pairs (solvers.py:467-482)
 enum Dot { DA = 0, DB, DC, DD, DE, DF, DG, DH, DR };
+// dot subsets: the s-independent dots (b e f h r) are final after K12's
+// row-local updates, so K12 carries them and K3 only the four that need the
+// new s (a c d g)
+constexpr unsigned kAllDots = (1u << kNumDots) - 1;
+constexpr unsigned kDotsK12 = (1u << DB) | (1u << DE) | (1u << DF) | (1u << DH) | (1u << DR);
+constexpr unsigned kDotsK3 = kAllDots & ~kDotsK12;
 
 // Host-visible mirror, written by the finalize kernel through mapped pinned
 // memory so the host can stop launching without a device sync.
@@ -87,6 +97,11 @@ __device__ __forceinline__ void report_nonfinite(SolverState* st, int tag, long 
   st->nf_tag = tag;
   if (st->mirror) st->mirror->err = 1;  // lets the host stop launching at once
 }
+
+// release/acquire fence (the patterns here — publish a record, then take a
+// ticket; take the ticket, then read every record — need no more than
+// acq_rel; __threadfence() is the stronger, slower fence.sc)
+__device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
@@ -157,29 +172,32 @@ __device__ __forceinline__ Ddbl dd_shfl_xor(Ddbl v, int o) {
   return Ddbl{__shfl_xor_sync(0xffffffffu, v.hi, o), __shfl_xor_sync(0xffffffffu, v.lo, o)};
 }
 
-// Block-level reduction of 9 per-thread compensated partials into
-// out[2*j], out[2*j+1] (threads 0..8 write, then __threadfence so a last-CTA
+// Block-level reduction of 9 per-thread compensated partials into fields
+// 2j, 2j+1 of the CTA's record, out = partials + blockIdx.x (field-major;
+// threads 0..8 write, then a release fence so a last-CTA
 // reader sees them).  Fixed shape (xor-butterfly in warps, then warps in
 // index order): the result depends only on the data-to-thread mapping.
-template <int NT, bool NAMED>
+// Only the dots in M are reduced and written.
+template <int NT, bool NAMED, unsigned M = kAllDots>
 __device__ __forceinline__ void block_reduce9(Ddbl (&acc)[kNumDots], double* out) {
   __shared__ Ddbl red[NT / 32][kNumDots];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
   for (int j = 0; j < kNumDots; ++j) {
+    if (!((M >> j) & 1u)) continue;
     Ddbl v = acc[j];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v = dd_add(v, dd_shfl_xor(v, o));
     if (lane == 0) red[warp][j] = v;
   }
   block_bar<NT, NAMED>();
-  if (threadIdx.x < kNumDots) {
+  if (threadIdx.x < kNumDots && ((M >> threadIdx.x) & 1u)) {
     Ddbl v = red[0][threadIdx.x];
 #pragma unroll
     for (int w = 1; w < NT / 32; ++w) v = dd_add(v, red[w][threadIdx.x]);
-    out[2 * threadIdx.x] = v.hi;
-    out[2 * threadIdx.x + 1] = v.lo;
-    __threadfence();
+    out[(size_t)(2 * threadIdx.x) * kMaxParts] = v.hi;
+    out[(size_t)(2 * threadIdx.x + 1) * kMaxParts] = v.lo;
+    fence_gpu();
   }
 }
 

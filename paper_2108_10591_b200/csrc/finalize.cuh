@@ -8,22 +8,95 @@
 
 namespace pbs {
 
-// Coefficient step + bookkeeping for check j.  One thread.
 __device__ __forceinline__ bool guard(double q, double scale) {
   return !isfinite(q) || fabs(q) <= mul(1e-14, scale);
 }
 
-__device__ void check_iteration(SolverState* st, long long j, const double* d, int replaced) {
-  const bool first = j == 0;
-  if (first) st->r0_norm = sqrt(d[DR]);
+// The check's three independent computations, one thread each so their
+// division / square-root chains run side by side: the relative residual
+// (_Run.rel_of), compute_alpha_beta_safe, compute_zeta_eta_safe.  The commit
+// then applies the reference's control flow to them (a breakdown in
+// alpha/beta wins over one in zeta/eta, as the reference raises it first).
+struct CheckVals {
+  double r0_norm, rel;
+  double alpha, beta;
+  int q_ab;
+  double zeta, eta;
+  int q_ze;
+  double f;  // this check's f, the next check's f_prev
+};
+
+__device__ __forceinline__ void check_rel(const SolverState* st, bool first, const double* d, CheckVals* cv) {
+  const double r0n = first ? sqrt(d[DR]) : st->r0_norm;
   // _Run.rel_of (solvers.py:176-179): Python max(rr, 0.0) keeps rr unless 0.0 > rr
   double rel;
-  if (st->r0_norm == 0.0) {
+  if (r0n == 0.0) {
     rel = 0.0;
   } else {
     const double m = (0.0 > d[DR]) ? 0.0 : d[DR];
-    rel = sqrt(m) / st->r0_norm;
+    rel = sqrt(m) / r0n;
   }
+  cv->r0_norm = r0n;
+  cv->rel = rel;
+}
+
+// compute_alpha_beta_safe (coefficients.py:60-84)
+__device__ __forceinline__ void check_ab(const SolverState* st, bool first, const double* d, CheckVals* cv) {
+  const double f = d[DF], g = d[DG], h = first ? 0.0 : d[DH];
+  double alpha = 0.0, beta = 0.0;
+  int q = PBS_BD_NONE;
+  if (first) {
+    if (guard(g, fabs(g))) q = PBS_BD_INITIAL_ALPHA;
+    alpha = f / g;
+    beta = 0.0;
+  } else {
+    const double denom_beta = mul(st->zeta, st->f_prev);
+    if (guard(denom_beta, fabs(denom_beta))) {
+      q = PBS_BD_BETA;
+    } else {
+      beta = mul(st->alpha, f) / denom_beta;
+      const double bh = mul(beta, h);
+      const double denom_alpha = add(g, bh);
+      if (guard(denom_alpha, add(fabs(g), fabs(bh)))) q = PBS_BD_ALPHA;
+      alpha = f / denom_alpha;
+    }
+  }
+  cv->alpha = alpha;
+  cv->beta = beta;
+  cv->q_ab = q;
+  cv->f = f;
+}
+
+// compute_zeta_eta_safe (coefficients.py:87-106)
+__device__ __forceinline__ void check_ze(bool first, const double* d, CheckVals* cv) {
+  double zeta = 0.0, eta = 0.0;
+  int q = PBS_BD_NONE;
+  const double a = d[DA], b = first ? 0.0 : d[DB], c = first ? 0.0 : d[DC], dd = d[DD], e = first ? 0.0 : d[DE];
+  if (first || (b == 0.0 && c == 0.0 && e == 0.0)) {
+    if (guard(a, fabs(a))) q = PBS_BD_ZETA;
+    zeta = dd / a;
+    eta = 0.0;
+  } else {
+    const double ab = mul(a, b), cc = mul(c, c);
+    const double det = sub(ab, cc);
+    if (guard(det, add(fabs(ab), cc))) {
+      q = PBS_BD_ZETA_ETA;
+    } else {
+      zeta = sub(mul(b, dd), mul(c, e)) / det;
+      eta = sub(mul(a, e), mul(c, dd)) / det;
+    }
+  }
+  cv->zeta = zeta;
+  cv->eta = eta;
+  cv->q_ze = q;
+}
+
+// Bookkeeping of check j (solvers.py:645-674, 736-739) on precomputed values.
+// One thread.
+__device__ void check_commit(SolverState* st, long long j, const CheckVals& cv, int replaced) {
+  const bool first = j == 0;
+  if (first) st->r0_norm = cv.r0_norm;
+  const double rel = cv.rel;
   long long slot = st->n_records;
   if (st->record_history) {
     st->hist_rel[slot] = rel;
@@ -44,111 +117,153 @@ __device__ void check_iteration(SolverState* st, long long j, const double* d, i
   }
   if (!isfinite(rel)) return stop(PBS_NON_FINITE, j, true);
   if (rel <= st->tol) return stop(PBS_CONVERGED, j, false);
-  // compute_alpha_beta_safe (coefficients.py:60-84)
-  const double f = d[DF], g = d[DG], h = first ? 0.0 : d[DH];
-  double alpha, beta;
-  int q = PBS_BD_NONE;
-  if (first) {
-    if (guard(g, fabs(g))) q = PBS_BD_INITIAL_ALPHA;
-    alpha = f / g;
-    beta = 0.0;
-  } else {
-    const double denom_beta = mul(st->zeta, st->f_prev);
-    if (guard(denom_beta, fabs(denom_beta))) {
-      q = PBS_BD_BETA;
-    } else {
-      beta = mul(st->alpha, f) / denom_beta;
-      const double bh = mul(beta, h);
-      const double denom_alpha = add(g, bh);
-      if (guard(denom_alpha, add(fabs(g), fabs(bh)))) q = PBS_BD_ALPHA;
-      alpha = f / denom_alpha;
-    }
-  }
-  // compute_zeta_eta_safe (coefficients.py:87-106)
-  double zeta = 0.0, eta = 0.0;
-  if (q == PBS_BD_NONE) {
-    const double a = d[DA], b = first ? 0.0 : d[DB], c = first ? 0.0 : d[DC], dd = d[DD],
-                 e = first ? 0.0 : d[DE];
-    if (first || (b == 0.0 && c == 0.0 && e == 0.0)) {
-      if (guard(a, fabs(a))) q = PBS_BD_ZETA;
-      zeta = dd / a;
-      eta = 0.0;
-    } else {
-      const double ab = mul(a, b), cc = mul(c, c);
-      const double det = sub(ab, cc);
-      if (guard(det, add(fabs(ab), cc))) {
-        q = PBS_BD_ZETA_ETA;
-      } else {
-        zeta = sub(mul(b, dd), mul(c, e)) / det;
-        eta = sub(mul(a, e), mul(c, dd)) / det;
-      }
-    }
-  }
+  const int q = cv.q_ab != PBS_BD_NONE ? cv.q_ab : cv.q_ze;
   if (q != PBS_BD_NONE) {
     st->breakdown = q;
     return stop(PBS_BREAKDOWN, j, true);
   }
-  st->alpha = alpha;
-  st->beta = beta;
-  st->zeta = zeta;
-  st->eta = eta;
-  st->f_prev = f;
+  st->alpha = cv.alpha;
+  st->beta = cv.beta;
+  st->zeta = cv.zeta;
+  st->eta = cv.eta;
+  st->f_prev = cv.f;
   if (st->record_history) {
-    st->hist_coef[4 * slot + 0] = alpha;
-    st->hist_coef[4 * slot + 1] = beta;
-    st->hist_coef[4 * slot + 2] = zeta;
-    st->hist_coef[4 * slot + 3] = eta;
+    st->hist_coef[4 * slot + 0] = cv.alpha;
+    st->hist_coef[4 * slot + 1] = cv.beta;
+    st->hist_coef[4 * slot + 2] = cv.zeta;
+    st->hist_coef[4 * slot + 3] = cv.eta;
     st->hist_flags[slot] |= PBS_HIST_HAS_COEF;
   }
-  if (!(isfinite(alpha) && isfinite(beta) && isfinite(zeta) && isfinite(eta)))
+  if (!(isfinite(cv.alpha) && isfinite(cv.beta) && isfinite(cv.zeta) && isfinite(cv.eta)))
     return stop(PBS_NON_FINITE, j, true);
 }
 
+// The check's working copy of the state.  The check is one thread's chain of
+// dependent reads and writes; run against global memory every read after a
+// write is another L2 round trip.  Instead the CTA loads the state into
+// shared memory in one round (overlapping the partials' reduction), thread 0
+// edits the copy, and the block the check owns (carried scalars .. n_records)
+// is written back.
+constexpr int kStateWords = (int)(sizeof(SolverState) / 8);
 
-__device__ __forceinline__ void publish(SolverState* st, long long next_iter) {
-  st->iter = next_iter;
-  if (st->mirror) {
-    st->mirror->iter = next_iter;
-    st->mirror->run_all = st->run_all;
-    st->mirror->err = dev_err(st) ? 1 : 0;
-    __threadfence_system();
+template <int NT>
+__device__ __forceinline__ void state_load(const SolverState* st, SolverState* ss) {
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(st);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(ss);
+  for (int k = threadIdx.x; k < kStateWords; k += NT) dst[k] = __ldcg(src + k);
+}
+
+__device__ __forceinline__ void state_store(SolverState* st, const SolverState* ss) {
+  constexpr int w0 = (int)(offsetof(SolverState, alpha) / 8), w1 = (int)(offsetof(SolverState, nf_row) / 8);
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(ss);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(st);
+#pragma unroll
+  for (int k = w0; k < w1; ++k) dst[k] = src[k];
+}
+
+// check j on the shared copy (its three computations in threads 0, 32, 64),
+// write back, mirror to the host.  Called by all NT threads after the copy
+// and dots are visible.
+template <int NT, bool NAMED>
+__device__ __forceinline__ void check_and_publish(SolverState* st, SolverState* ss, const double* dots,
+                                                  int replaced) {
+  __shared__ CheckVals cv;
+  const long long j = ss->iter;
+  const bool first = j == 0;
+  const bool work = !dev_err(ss) && ss->run_all;
+  if (work) {
+    if (threadIdx.x == 0) check_rel(ss, first, dots, &cv);
+    else if (threadIdx.x == 32) check_ab(ss, first, dots, &cv);
+    else if (threadIdx.x == 64) check_ze(first, dots, &cv);
+  }
+  block_bar<NT, NAMED>();
+  if (threadIdx.x != 0) return;
+  if (work) {
+    for (int k = 0; k < kNumDots; ++k) ss->dots[k] = dots[k];
+    check_commit(ss, j, cv, replaced);
+  } else if (!dev_err(ss)) {
+    ss->run_spine = 0;  // the stop iteration's spine product has run
+  }
+  ss->iter = j + 1;
+  state_store(st, ss);
+  // host mirror: posted stores, no fence (a stale field only delays the host's
+  // stop by one poll; every launch is gated on the device state anyway)
+  if (ss->mirror) {
+    ss->mirror->iter = j + 1;
+    ss->mirror->run_all = ss->run_all;
+    ss->mirror->err = dev_err(ss) ? 1 : 0;
   }
 }
 
 // Reduce partial records (kPartStride doubles each: hi/lo per dot) -> dots[9]
-// with NT threads, fixed shape: dot j is summed in double-double by a team of
-// T = NT/9 threads (strided, sequential per thread), then the team's values
-// in order, then rounded once.  chain: the reference's left-to-right combine
-// of plain per-range values (reduction.py:285-294 _combine), one thread per dot.
+// with NT threads, fixed shape: one warp per dot, each lane summing a strided
+// subset of the records in double-double (pairwise, 16 records per pass),
+// then the warp's xor butterfly, rounded once.  Dots in
+// mask2 come from a second record set (partials2, nparts2): the
+// s-independent dots K12 produced.  chain: the reference's left-to-right
+// combine of plain per-range values (reduction.py:285-294 _combine), one
+// thread per dot.
 template <int NT, bool NAMED>
-__device__ void reduce_parts(const double* partials, int nparts, int chain, double* dots) {
-  constexpr int T = NT / kNumDots;
-  __shared__ Ddbl team[kNumDots][T];
+__device__ void reduce_parts(const double* partials, int nparts, int chain, double* dots,
+                             const double* partials2 = nullptr, int nparts2 = 0, unsigned mask2 = 0,
+                             int rs = 1, int fs = kMaxParts) {
   const int t = threadIdx.x;
   if (chain) {
     if (t < kNumDots) {
-      double acc = __ldcg(partials + 2 * t);
-      for (int b = 1; b < nparts; ++b) acc = add(acc, __ldcg(partials + (size_t)b * kPartStride + 2 * t));
+      double acc = __ldcg(partials + (size_t)(2 * t) * fs);
+      const double* p = partials + (size_t)(2 * t) * fs;
+      for (int b = 1; b < nparts; ++b) acc = add(acc, __ldcg(p + (size_t)b * rs));
       dots[t] = acc;
     }
-  } else {
-    const int j = t / T, l = t % T;
-    if (j < kNumDots) {
-      Ddbl acc{0.0, 0.0};
-      for (int b = l; b < nparts; b += T) {
-        const double* p = partials + (size_t)b * kPartStride + 2 * j;
-        acc = dd_add(acc, Ddbl{__ldcg(p), __ldcg(p + 1)});
-      }
-      team[j][l] = acc;
-    }
     block_bar<NT, NAMED>();
-    if (t < kNumDots) {
-      Ddbl acc = team[t][0];
-      for (int k = 1; k < T; ++k) acc = dd_add(acc, team[t][k]);
-      dots[t] = add(acc.hi, acc.lo);
+    return;
+  }
+  // warp w sums dots w, w + NW, ...: lane l takes records l, l + 32, ... in
+  // order (eight records' loads in flight per round), then the xor butterfly
+  constexpr int NW = NT / 32;
+  const int lane = t & 31, warp = t >> 5;
+#ifdef PBS_TAIL_CLOCKS
+  const long long q0 = clock64();
+  long long q1 = 0, q2 = 0, q3 = 0;
+#endif
+  for (int j = warp; j < kNumDots; j += NW) {
+    const bool second = (mask2 >> j) & 1u;
+    const double* src = (second ? partials2 : partials) + (size_t)(2 * j) * fs;
+    const int np = second ? nparts2 : nparts;
+    Ddbl acc{0.0, 0.0};
+    constexpr int U = 16;  // records per lane per pass: all loads in flight, then a pairwise tree
+    for (int b0 = lane; b0 < np; b0 += 32 * U) {
+      Ddbl v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + 32 * u;
+        v[u] = b < np ? Ddbl{__ldcg(src + (size_t)b * rs), __ldcg(src + (size_t)b * rs + fs)}
+                      : Ddbl{0.0, 0.0};
+      }
+#ifdef PBS_TAIL_CLOCKS
+      if (v[U - 1].hi == 12345.0) acc.lo += 1.0;  // force the loads to land
+      q1 = clock64();
+#endif
+#pragma unroll
+      for (int w = 1; w < U; w *= 2)
+#pragma unroll
+        for (int u = 0; u < U; u += 2 * w) v[u] = dd_add(v[u], v[u + w]);
+      acc = dd_add(acc, v[0]);
     }
+#ifdef PBS_TAIL_CLOCKS
+    q2 = clock64();
+#endif
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = dd_add(acc, dd_shfl_xor(acc, o));
+    if (lane == 0) dots[j] = add(acc.hi, acc.lo);
+#ifdef PBS_TAIL_CLOCKS
+    q3 = clock64();
+#endif
   }
   block_bar<NT, NAMED>();
+#ifdef PBS_TAIL_CLOCKS
+  if (t == 0) printf("reduce parts: loads %lld tree %lld butterfly %lld\n", q1 - q0, q2 - q1, q3 - q2);
+#endif
 }
 
 // Multi-GPU local step: reduce this rank's CTA partial records to ONE record
@@ -160,8 +275,8 @@ __global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partial
   if (j < kNumDots) {
     Ddbl acc{0.0, 0.0};
     for (int b = l; b < nparts; b += T) {
-      const double* p = partials + (size_t)b * kPartStride + 2 * j;
-      acc = dd_add(acc, Ddbl{__ldcg(p), __ldcg(p + 1)});
+      const double* p = partials + (size_t)(2 * j) * kMaxParts + b;
+      acc = dd_add(acc, Ddbl{__ldcg(p), __ldcg(p + kMaxParts)});
     }
     team[j][l] = acc;
   }
@@ -177,49 +292,49 @@ __global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partial
 // Run by every participating thread of each CTA after its block_reduce9:
 // the last CTA to arrive reduces all partials and performs the check.
 template <int NT, bool NAMED>
-__device__ void finalize_tail(SolverState* st, const double* partials, int nparts, int replaced) {
+__device__ void finalize_tail(SolverState* st, const double* partials, int nparts, int replaced,
+                              const double* partials2 = nullptr, int nparts2 = 0, unsigned mask2 = 0) {
   __shared__ int last;
   __shared__ double dots[kNumDots];
   block_bar<NT, NAMED>();
   if (threadIdx.x == 0) {
-    __threadfence();
+    fence_gpu();
     const unsigned int ticket = atomicAdd(&st->done_ctas, 1u);
     last = ticket == (unsigned int)nparts - 1;
   }
   block_bar<NT, NAMED>();
   if (!last) return;
-  __threadfence();
-  reduce_parts<NT, NAMED>(partials, nparts, 0, dots);
-  if (threadIdx.x == 0) {
-    st->done_ctas = 0;
-    const long long j = st->iter;
-    if (!dev_err(st) && st->run_all) {
-      for (int k = 0; k < kNumDots; ++k) st->dots[k] = dots[k];
-      check_iteration(st, j, dots, replaced);
-    }
-    publish(st, j + 1);
-  }
+  fence_gpu();
+  __shared__ SolverState ss;
+  state_load<NT>(st, &ss);
+  reduce_parts<NT, NAMED>(partials, nparts, 0, dots, partials2, nparts2, mask2);  // ends with a barrier
+  if (threadIdx.x == 0) st->done_ctas = 0;
+  check_and_publish<NT, NAMED>(st, &ss, dots, replaced);
 }
 
 // Standalone finalize (1 CTA, 288 threads): reduce (tree or plan chain), then
 // the check for j = st->iter, then advance st->iter.
 __global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const double* partials, int nparts,
-                                                       int chain, int replaced) {
+                                                       int chain, int replaced, const double* partials2 = nullptr,
+                                                       int nparts2 = 0, unsigned mask2 = 0, int rs = 1,
+                                                       int fs = kMaxParts) {
   __shared__ double dots[kNumDots];
-  __shared__ int work;
-  if (threadIdx.x == 0) work = !dev_err(st) && st->run_all;
-  __syncthreads();
-  const long long j = st->iter;
-  if (work) {
-    reduce_parts<288, false>(partials, nparts, chain, dots);
-    if (threadIdx.x == 0) {
-      for (int k = 0; k < kNumDots; ++k) st->dots[k] = dots[k];
-      check_iteration(st, j, dots, replaced);
-    }
-  } else if (threadIdx.x == 0 && !dev_err(st)) {
-    st->run_spine = 0;  // the stop iteration's spine product has run
+  __shared__ SolverState ss;
+#ifdef PBS_TAIL_CLOCKS
+  long long c0 = clock64();
+#endif
+  state_load<288>(st, &ss);
+  reduce_parts<288, false>(partials, nparts, chain, dots, partials2, nparts2, mask2, rs, fs);  // ends with a barrier
+#ifdef PBS_TAIL_CLOCKS
+  long long c1 = clock64();
+#endif
+  check_and_publish<288, false>(st, &ss, dots, replaced);
+#ifdef PBS_TAIL_CLOCKS
+  if (threadIdx.x == 0) {
+    long long c2 = clock64();
+    printf("tail clocks: reduce %lld check+publish %lld\n", c1 - c0, c2 - c1);
   }
-  if (threadIdx.x == 0) publish(st, j + 1);
+#endif
 }
 
 }  // namespace pbs

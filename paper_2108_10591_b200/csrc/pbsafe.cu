@@ -141,6 +141,7 @@ struct pbs_mat {
   long long* rp = nullptr;
   int* ci = nullptr;
   double* v = nullptr;
+  unsigned short* wc = nullptr;  // window-local column per nonzero (staged engine; null: col_idx)
   StencilView sv{};
   XWin xwin{};  // x windows of the pipelined engines (nwin = 0: gather x)
   StencilWin swin{};  // stencil point -> window
@@ -192,7 +193,6 @@ static int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int
   return (int)g;
 }
 
-constexpr int kMaxParts = 148 * 16;
 
 // ------------------------------------------------------------------ workspace
 
@@ -205,6 +205,7 @@ struct Workspace {
   VecPtrs X{};  // extended-space bases (SpMV inputs: [left halo | own | right halo])
   long long n_ext = 0, own_off = 0;
   double* partials = nullptr;
+  double* partials12 = nullptr;  // K12's records of the s-independent dots
   long long* plan_bounds = nullptr;
   int plan_workers = 0;
   int plan_w_actual = 0;
@@ -232,6 +233,7 @@ static void free_ws(Workspace* ws) {
   pbs_ctx* ctx = ws->ctx;
   pool_free(ctx, ws->base);
   pool_free(ctx, ws->partials);
+  pool_free(ctx, ws->partials12);
   pool_free(ctx, ws->plan_bounds);
   pool_free(ctx, ws->st);
   if (ws->mirror_h) cudaFreeHost(ws->mirror_h);
@@ -263,6 +265,7 @@ static int ensure_ws(pbs_mat* m, long long hist_slots) {
       ws->V.v[k] = ws->X.v[k] + ws->own_off;
     }
     CK(pool_alloc(ctx, &ws->partials, sizeof(double) * kMaxParts * kPartStride));
+    CK(pool_alloc(ctx, &ws->partials12, sizeof(double) * kMaxParts * kPartStride));
     CK(pool_alloc(ctx, &ws->st, sizeof(SolverState)));
     CK(cudaHostAlloc(&ws->mirror_h, sizeof(HostMirror), cudaHostAllocMapped));
     CK(cudaHostGetDevicePointer((void**)&ws->mirror_d, ws->mirror_h, 0));
@@ -417,14 +420,14 @@ static int pipe_extra_chunks() {  // chunk stages beyond the block slots
 }
 
 template <class Epi>
-static int pipe_config(pbs_ctx* ctx, const XWin& W, long long blk_nnz_max, int* bslots, int* cstages,
+static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_max, int* bslots, int* cstages,
                        size_t* smem, int* ctas, int* chunk) {
-  const BlockLayout BL(W.total, Epi::kIn);
+  const BlockLayout BL(W.total, Epi::kInStaged);
   // one chunk per row block when the densest block fits the cap (stencils:
   // ~7 or ~27 nonzeros per row), else cap-sized chunks
   int ch = pipe_chunk_cap();
   if (blk_nnz_max > 0 && blk_nnz_max < ch) ch = (int)((blk_nnz_max + 3) & ~3LL);
-  const ChunkLayout CL(ch);
+  const ChunkLayout CL(ch, colb);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
@@ -488,7 +491,7 @@ static int stencil_pipe_set_smem(pbs_ctx* ctx, size_t smem) {
 
 template <class Epi>
 static int stencil_pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, size_t* smem, int* ctas) {
-  const BlockLayout BL(W.total, Epi::kIn);
+  const BlockLayout BL(W.total, Epi::kInStaged);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
@@ -521,7 +524,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   long long nblk = (hi - lo + kThreads - 1) / kThreads;
   int grid;
   if (!m->stencil && csr_engine_tpr()) {
-    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
+    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, nullptr};
     if (csr_engine_tpr() == 2) {
       grid = grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, true>, nblk);
       csr_tpr_kernel<Epi, true><<<grid, kThreads, 0, L.s>>>(A, x, epi);
@@ -530,17 +533,20 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
   } else if (!m->stencil) {
-    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols};
+    // window-local columns describe the row blocks of a launch starting at row 0
+    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, lo == 0 ? m->wc : nullptr};
+    // staged x windows need the window-local columns; otherwise gather x
+    const XWin W = A.wc ? m->xwin : XWin{};
     int bslots, cstages, ctas, chunk;
     size_t smem;
-    int rc = pipe_config<Epi>(L.ctx, m->xwin, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk);
+    int rc = pipe_config<Epi>(L.ctx, W, A.wc ? 2 : 4, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk);
     if (rc) {
       L.err = rc;
       return 0;
     }
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
-    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, m->xwin, bslots, cstages, chunk);
+    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, W, bslots, cstages, chunk);
   } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>()) {
     StencilView S = m->sv;
     S.row_lo = lo;
@@ -642,8 +648,9 @@ static EpiDots epi_dots(Workspace* ws, const Mode& md, int spine, int fuse, int 
   return e;
 }
 
-static EpiK12 epi_k12(Workspace* ws, const Mode& md) {
-  EpiK12 e{};
+template <class E>
+static E epi_k12_fill(Workspace* ws, const Mode& md) {
+  E e{};
   auto& V = ws->V.v;
   e.as = V[VAS];
   e.p = V[VP];
@@ -657,8 +664,16 @@ static EpiK12 epi_k12(Workspace* ws, const Mode& md) {
   e.o_out = md.store_temps ? V[VO] : nullptr;
   e.q_out = md.store_temps ? V[VQ] : nullptr;
   e.st = ws->st;
-  const int in[11] = {VR, VP, VU, VS, VT, VY, VL, VG, VW, VZ, VX};
-  for (int k = 0; k < 11; ++k) e.in[k] = V[in[k]];
+  const int in[12] = {VR, VP, VU, VS, VT, VY, VL, VG, VW, VZ, VX, VR0S};
+  for (int k = 0; k < E::kIn; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+static EpiK12 epi_k12(Workspace* ws, const Mode& md) { return epi_k12_fill<EpiK12>(ws, md); }
+
+static EpiK12d epi_k12d(Workspace* ws, const Mode& md) {
+  EpiK12d e = epi_k12_fill<EpiK12d>(ws, md);
+  e.parts = ws->partials12;
   return e;
 }
 
@@ -712,6 +727,41 @@ static EpiK3 epi_k3(Workspace* ws, const Mode& md, int fuse) {
   return e;
 }
 
+// K3 carrying only the dots that need the new s; the check also reduces
+// K12's records (np12 of them) for the other five
+static EpiK3s epi_k3s(Workspace* ws, const Mode& md, int fuse, int np12) {
+  EpiK3s e{};
+  auto& V = ws->V.v;
+  e.l = V[VL];
+  e.g = V[VG];
+  e.s = V[VS];
+  e.q_out = md.store_temps ? V[VQ] : nullptr;
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, fuse, 0);
+  e.sink.partials2 = ws->partials12;
+  e.sink.nparts2 = np12;
+  e.sink.mask2 = kDotsK12;
+  const int in[7] = {VAS, VL, VG, VS, VY, VR, VR0S};
+  for (int k = 0; k < 7; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+// the batch split between K12 (b e f h r) and K3 (a c d g): default on for
+// CSR (the staged K12 has the registers to spare); the direct stencil K12
+// loses occupancy to the accumulators, so stencils keep all nine in K3.
+// PBS_K12_DOTS=0 keeps all nine in K3 for CSR too.
+// PBS_FUSE_CHECK=0: the check as its own 1-CTA kernel instead of the last
+// K3 CTA's tail (A/B of the tail's cost)
+static bool fuse_check() {
+  static int v = env_int("PBS_FUSE_CHECK", 1, 0, 1);
+  return v;
+}
+
+static bool k12_dots() {
+  static int v = env_int("PBS_K12_DOTS", 1, 0, 1);
+  return v;
+}
+
 static EpiSS3 epi_ss3(Workspace* ws) {
   EpiSS3 e{};
   auto& V = ws->V.v;
@@ -737,8 +787,9 @@ static int plan_dots(Launcher& L, Workspace* ws, int kind) {
   return ws->plan_w_actual;
 }
 
-static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int replaced) {
-  finalize_kernel<<<1, 288, 0, L.s>>>(ws->st, ws->partials, nparts, chain, replaced);
+static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int replaced, int np12 = 0) {
+  finalize_kernel<<<1, 288, 0, L.s>>>(ws->st, ws->partials, nparts, chain, replaced, ws->partials12, np12,
+                                      np12 ? kDotsK12 : 0u);
   L.done(KF);
 }
 
@@ -759,6 +810,16 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
 // (Aw + l g s + the fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
+  if (!md.plan && !k3_dots_split() && k12_dots() && !L.m->stencil) {
+    const int fuse = L.trace_cfg || !fuse_check() ? 0 : 1;
+    const int np12 = spmv_launch(L, ws->X.v[VS], epi_k12d(ws, md), 0, ws->n, KK1);
+    const int grid = spmv_launch(L, ws->X.v[VW], epi_k3s(ws, md, fuse, np12), 0, ws->n, KK3);
+    if (!fuse) {
+      L.trace_point();
+      finalize(L, ws, grid, 0, 0, np12);
+    }
+    return;
+  }
   spmv_launch(L, ws->X.v[VS], epi_k12(ws, md), 0, ws->n, KK1);
   if (!md.plan && k3_dots_split()) {
     spmv_launch(L, ws->X.v[VW], epi_k3n(ws, md), 0, ws->n, KK3);
@@ -897,7 +958,8 @@ static void dist_check(Launcher& L, Workspace* ws, pbs_mat* m, int nparts, int r
     L.err = set_err(L.ctx, PBS_ERR_NCCL, std::string("all-gather: ") + nccl().GetErrorString(r));
     return;
   }
-  finalize_kernel<<<1, 288, 0, D->comm>>>(ws->st, D->recvbuf, D->nranks, 0, replaced);
+  // the gathered pairs are one row-major record per rank
+  finalize_kernel<<<1, 288, 0, D->comm>>>(ws->st, D->recvbuf, D->nranks, 0, replaced, nullptr, 0, 0u, kPartStride, 1);
   L.done(KF);
   L.mark(D->comm, L.iter, 1, 0);  // reduce_end
   L.mark(D->comm, L.iter, 4, 0);  // coeff_ready
@@ -1367,6 +1429,78 @@ __global__ void offset_bins_kernel(const long long* rp, const int* ci, long long
   (void)r_first;
 }
 
+// Window-local column of every nonzero: the staged offset of x[col] in its
+// row block's x windows, by the rule the staged engine's producer and
+// consumers use (csr_pipe_kernel: window c spans [r0 + wmin[c], r0 + nr - 1 +
+// wmax[c]] clamped to x and aligned down to even, staged at the sum of the
+// earlier caps; a column belongs to the last window starting at or before it).
+// *bad = 1 when a column falls outside its window (the engine then keeps
+// col_idx).
+__global__ void window_cols_kernel(const long long* rp, const int* ci, long long n_rows, long long n_cols, XWin W,
+                                   unsigned short* wc, int* bad) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride) {
+    const long long r0 = i / kPipeRows * kPipeRows;
+    const long long nr = min((long long)kPipeRows, n_rows - r0);
+    long long wlo[kMaxWin], whi[kMaxWin];
+    int soff[kMaxWin];
+    int acc = 0;
+#pragma unroll
+    for (int c = 0; c < kMaxWin; ++c) {
+      wlo[c] = 0x7fffffff;
+      whi[c] = 0;
+      soff[c] = acc;
+      if (c < W.nwin) {
+        long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
+        if (lo < 0) lo = 0;
+        if (hi > n_cols) hi = n_cols;
+        wlo[c] = lo & ~1LL;
+        whi[c] = hi > lo ? ((hi + 1) & ~1LL) : wlo[c];
+        acc += W.cap[c];
+      }
+    }
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+      const long long col = ci[k];
+      int c = 0;
+#pragma unroll
+      for (int cc = 1; cc < kMaxWin; ++cc)
+        if (col >= wlo[cc]) c = cc;
+      const long long off = col - wlo[c];
+      if (off < 0 || col >= whi[c] || off + soff[c] >= W.total) {
+        *bad = 1;
+        wc[k] = 0;
+      } else {
+        wc[k] = (unsigned short)(off + soff[c]);
+      }
+    }
+  }
+}
+
+static int build_window_cols(pbs_ctx* ctx, pbs_mat* m) {
+  if (m->wc) {
+    pool_free(ctx, m->wc);
+    m->wc = nullptr;
+  }
+  if (!m->xwin.nwin || m->nnz == 0 || m->xwin.total > 65535) return PBS_OK;
+  cudaStream_t s = ctx->stream;
+  int* bad = nullptr;
+  CK(pool_alloc(ctx, &m->wc, sizeof(unsigned short) * (m->nnz + 16)));
+  CK(pool_alloc(ctx, &bad, sizeof(int)));
+  CK(cudaMemsetAsync(m->wc + m->nnz, 0, sizeof(unsigned short) * 16, s));
+  CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
+  window_cols_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->rp, m->ci, m->n_rows, m->n_cols, m->xwin, m->wc, bad);
+  int hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  pool_free(ctx, bad);
+  if (hbad || env_int("PBS_NO_WINDOW_COLS", 0, 0, 1)) {  // 1: keep col_idx (A/B sweeps)
+    pool_free(ctx, m->wc);
+    m->wc = nullptr;
+  }
+  return PBS_OK;
+}
+
 // clusters of row offsets -> x windows (<= kMaxWin, <= kMaxWinElems staged)
 static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   m->xwin = XWin{};
@@ -1425,7 +1559,7 @@ static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   W.nwin = (int)cl.size();
   W.total = (int)total;
   m->xwin = W;
-  return PBS_OK;
+  return m->stencil ? PBS_OK : build_window_cols(ctx, m);
 }
 
 PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
@@ -1713,6 +1847,7 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   pool_free(m->ctx, m->rp);
   pool_free(m->ctx, m->ci);
   pool_free(m->ctx, m->v);
+  pool_free(m->ctx, m->wc);
   delete m;
   return PBS_OK;
 }

@@ -37,12 +37,24 @@
 
 namespace pbs {
 
+// staged-window products in flight per row for the dot-carrying epilogues
+// (register-bound; -D overrides for sweeps)
+#ifndef PBS_WCB_K12D
+#define PBS_WCB_K12D 2
+#endif
+#ifndef PBS_WCB_K3S
+#define PBS_WCB_K3S 4
+#endif
+
 struct CsrView {
   const long long* rp;
   const int* ci;
   const double* v;
   long long row_lo, row_hi;
   long long n_cols;
+  // nullable: per-nonzero index into its row block's staged x windows (built
+  // at upload for row_lo == 0); replaces col_idx in the staged engine
+  const unsigned short* wc;
 };
 
 struct StencilView {
@@ -56,41 +68,53 @@ struct StencilView {
 
 // ---------------------------------------------------------------- epilogues
 
-struct Dots9 {
+template <unsigned M>
+struct DotsT {
   Ddbl acc[kNumDots];
   __device__ void zero() {
 #pragma unroll
     for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
   }
-  // _safe_batch pairs (solvers.py:471-481), compensated (Dot2) accumulation
+  __device__ __forceinline__ void step(int j, double a, double b) {
+    if ((M >> j) & 1u) acc[j] = dot2_step(acc[j], a, b);
+  }
+  // _safe_batch pairs (solvers.py:471-481), compensated (Dot2) accumulation;
+  // only the dots in M
   __device__ void add_row(double s, double y, double r, double r0s, double t) {
-    acc[DA] = dot2_step(acc[DA], s, s);
-    acc[DB] = dot2_step(acc[DB], y, y);
-    acc[DC] = dot2_step(acc[DC], s, y);
-    acc[DD] = dot2_step(acc[DD], s, r);
-    acc[DE] = dot2_step(acc[DE], y, r);
-    acc[DF] = dot2_step(acc[DF], r0s, r);
-    acc[DG] = dot2_step(acc[DG], r0s, s);
-    acc[DH] = dot2_step(acc[DH], r0s, t);
-    acc[DR] = dot2_step(acc[DR], r, r);
+    step(DA, s, s);
+    step(DB, y, y);
+    step(DC, s, y);
+    step(DD, s, r);
+    step(DE, y, r);
+    step(DF, r0s, r);
+    step(DG, r0s, s);
+    step(DH, r0s, t);
+    step(DR, r, r);
   }
 };
+using Dots9 = DotsT<kAllDots>;
 
 // dot-partial sink shared by the epilogues that carry the batch
 struct DotSink {
   double* partials;  // nullptr: no partials (PBS_REDUCE_PLAN computes them separately)
   int fuse;          // last CTA runs finalize_tail (check + coefficients)
   int replaced;      // the record this check writes follows a replacement
-  template <int NT, bool NAMED>
-  __device__ void finish(Dots9& d, SolverState* st) {
+  // the dots this kernel does not carry: K12's records (mask2 = kDotsK12)
+  const double* partials2;
+  int nparts2;
+  unsigned mask2;
+  template <int NT, bool NAMED, unsigned M>
+  __device__ void finish(DotsT<M>& d, SolverState* st) {
     if (!partials) return;
-    block_reduce9<NT, NAMED>(d.acc, partials + (size_t)blockIdx.x * kPartStride);
-    if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced);
+    block_reduce9<NT, NAMED, M>(d.acc, partials + blockIdx.x);
+    if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced, partials2, nparts2, mask2);
   }
 };
 
 struct EpiStore {
   static constexpr int kIn = 0;
+  static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  static constexpr int kWcBatch = 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
@@ -112,6 +136,8 @@ struct EpiStore {
 
 struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
   static constexpr int kIn = 1;
+  static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  static constexpr int kWcBatch = 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
@@ -134,6 +160,8 @@ struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
 
 struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   static constexpr int kIn = 4;
+  static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  static constexpr int kWcBatch = 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 2;  // x gathers in flight per row
@@ -156,22 +184,30 @@ struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
 };
 
-struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local K2 updates)
-  static constexpr int kIn = 11;
+// DOTS: also the partials of the s-independent dots of the next check (b e f
+// h r: y, r, t are final here), with r0s read directly, not staged
+template <bool DOTS>
+struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-local K2 updates)
+  static constexpr int kIn = DOTS ? 12 : 11;
+  static constexpr int kInStaged = 11;  // r0s (DOTS) is loaded by the consumer thread
+  static constexpr int kWcBatch = DOTS ? PBS_WCB_K12D : 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
-  static constexpr int kGatherBatch = 8;  // x gathers in flight per row
+  static constexpr int kGatherBatch = DOTS ? 4 : 8;  // x gathers in flight per row
   double* as;  // As is kept for K3
   double *p, *u, *w, *t, *z, *y, *x, *r;
   double *o_out, *q_out;  // nullable (single-step parity)
+  double* parts;          // DOTS: partial records of the s-independent dots (kDotsK12)
   SolverState* st;
-  const double* in[kIn];  // r p u s t y l g w z x
+  const double* in[kIn];  // r p u s t y l g w z x r0s
   double alpha, beta, zeta, eta;
   int full;  // 0: the check stopped the solve; only the spine product runs
+  DotsT<kDotsK12> d;
   __device__ bool active() const { return gate_spine(st); }
   __device__ void on_skip() const {}
   __device__ void init() {
     full = gate_all(st);
+    if (DOTS) d.zero();
     alpha = st->alpha;
     beta = st->beta;
     zeta = st->zeta;
@@ -205,16 +241,24 @@ struct EpiK12 {  // K1 (As = A s) fused with block 1 of the iteration (row-local
       o_out[i] = o;
       q_out[i] = q;
     }
+    if constexpr (DOTS) d.add_row(0.0, yn, rn, v[kIn - 1], tn);  // next check's b e f h r
   }
   template <int NT, bool NAMED>
-  __device__ void finish() {}
+  __device__ void finish() {
+    if constexpr (DOTS) block_reduce9<NT, NAMED, kDotsK12>(d.acc, parts + blockIdx.x);
+  }
 };
+using EpiK12 = EpiK12T<false>;
+using EpiK12d = EpiK12T<true>;
 
-// block 2 of the pipelined iteration; DOTS: also the next iteration's batch
-// (else a separate streaming kernel computes it, and K3 needs 4 fewer inputs)
-template <bool DOTS>
+// block 2 of the pipelined iteration with the dot partials in M of the next
+// check's batch: all 9 (kAllDots), the 4 that need the new s (kDotsK3; K12
+// carried the rest), or none (0: a separate streaming kernel computes them)
+template <unsigned M>
 struct EpiK3T {
-  static constexpr int kIn = DOTS ? 8 : 4;
+  static constexpr int kIn = M == kAllDots ? 8 : (M ? 7 : 4);
+  static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  static constexpr int kWcBatch = M == kAllDots ? 2 : PBS_WCB_K3S;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 2;  // x gathers in flight per row
@@ -222,9 +266,9 @@ struct EpiK3T {
   double* q_out;  // nullable (single-step parity: expose q)
   SolverState* st;
   DotSink sink;
-  const double* in[8];  // As l g s (y r r0s t)
+  const double* in[8];  // As l g s (y r r0s (t))
   double alpha, beta, zeta, eta;
-  Dots9 d;
+  DotsT<M> d;
   __device__ bool active() const { return gate_all(st); }
   // the stop iteration's spine product (K12) has run: close the spine gate for
   // iterations the host launched ahead
@@ -232,7 +276,7 @@ struct EpiK3T {
     if (!dev_err(st) && !st->run_all) st->run_spine = 0;
   }
   __device__ void init() {
-    if (DOTS) d.zero();
+    if (M) d.zero();
     alpha = st->alpha;
     beta = st->beta;
     zeta = st->zeta;
@@ -249,19 +293,26 @@ struct EpiK3T {
     g[i] = gv;
     s[i] = sv;
     if (q_out) q_out[i] = q;
-    if (DOTS && sink.partials) d.add_row(sv, v[4], v[5], v[6], v[7]);
+    if constexpr (M == kAllDots) {
+      if (sink.partials) d.add_row(sv, v[4], v[5], v[6], v[7]);
+    } else if constexpr (M != 0) {
+      if (sink.partials) d.add_row(sv, v[4], v[5], v[6], 0.0);
+    }
   }
   template <int NT, bool NAMED>
   __device__ void finish() {
-    if (DOTS) sink.finish<NT, NAMED>(d, st);
+    if constexpr (M != 0) sink.finish<NT, NAMED>(d, st);
   }
 };
-using EpiK3 = EpiK3T<true>;
-using EpiK3n = EpiK3T<false>;
+using EpiK3 = EpiK3T<kAllDots>;
+using EpiK3n = EpiK3T<0>;
+using EpiK3s = EpiK3T<kDotsK3>;
 
 
 struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:569-580)
   static constexpr int kIn = 8;
+  static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  static constexpr int kWcBatch = 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
@@ -337,13 +388,14 @@ struct BlockLayout {
   }
 };
 
-// chunk stage: header, values, col_idx (ch nonzeros)
+// chunk stage: header, values, column stream (ch nonzeros; int32 col_idx or
+// u16 window-local columns, colb bytes each, 16-byte-aligned copy slack)
 struct ChunkLayout {
   size_t v, ci, bytes;
-  __host__ __device__ ChunkLayout(int ch) {
+  __host__ __device__ ChunkLayout(int ch, int colb) {
     v = 128;
     ci = v + align128(sizeof(double) * (ch + 2));
-    bytes = ci + align128(sizeof(int) * (ch + 4));
+    bytes = ci + align128((size_t)colb * (ch + 32 / colb));
   }
 };
 constexpr size_t kPipeBarrierBytes = 512;
@@ -364,8 +416,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   uint64_t* cempty = cfull + kMaxStages;
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
-  const BlockLayout BL(W.total, Epi::kIn);
-  const ChunkLayout CL(chunk);
+  const BlockLayout BL(W.total, Epi::kInStaged);
+  const ChunkLayout CL(chunk, A.wc ? 2 : 4);
   unsigned char* blk0 = smem + kPipeBarrierBytes;
   unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -415,7 +467,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       // x windows of this block (every lane computes them; lane 1+c copies window c)
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = brp + Epi::kIn * bin;
+      uint32_t total = brp + Epi::kInStaged * bin;
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0x7fffffff;
@@ -460,7 +512,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
             bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
           soff += cc < W.nwin ? W.cap[cc] : 0;
         }
-      } else if (lane >= 8 && lane < 8 + Epi::kIn) {
+      } else if (lane >= 8 && lane < 8 + Epi::kInStaged) {
         const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
       }
@@ -475,9 +527,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         const long long c0 = base + c * chunk;
         const long long c1 = min(end, c0 + chunk);
         const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
-        const long long c0b = c0 & ~3LL, c1b = (c1 + 3) & ~3LL;
+        // column stream: window-local u16 indices (8 per 16 bytes) or int32
+        const long long cal = A.wc ? 7 : 3;
+        const long long c0b = c0 & ~cal, c1b = (c1 + cal) & ~cal;
         const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
-        const uint32_t bc = (uint32_t)((c1b - c0b) * sizeof(int));
+        const uint32_t bc = (uint32_t)((c1b - c0b) * (A.wc ? sizeof(unsigned short) : sizeof(int)));
         if (lane == 0) {
           ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
           h->c0 = c0;
@@ -489,7 +543,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         }
         __syncwarp();
         if (lane == 0 && bv) bulk_g2s(st + CL.v, A.v + c0a, bv, &cfull[cs]);
-        if (lane == 1 && bc) bulk_g2s(st + CL.ci, A.ci + c0b, bc, &cfull[cs]);
+        if (lane == 1 && bc)
+          bulk_g2s(st + CL.ci, A.wc ? (const void*)(A.wc + c0b) : (const void*)(A.ci + c0b), bc, &cfull[cs]);
         if (++cs == cstages) {
           cs = 0;
           cph ^= 1;
@@ -512,24 +567,17 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
     const int nr = bhp->nr, dr = bhp->dr;
     const long long r0 = bhp->r0;
     long long my_s = 0, my_e = 0;
+    double inr[Epi::kIn > 0 ? Epi::kIn : 1];
     if (t < nr) {
       const long long* rps = reinterpret_cast<const long long*>(bst + BL.rp);
       my_s = rps[t + dr];
       my_e = rps[t + dr + 1];
-    }
-    // x lookup: window c holds x[ws[c] ...] at staged offset soff[c], so
-    // x[col] = xw[col - wsb[c]] for the last window with ws[c] <= col
-    const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
-    int wsv[kMaxWin], wsb[kMaxWin];
-    {
-      int soff = 0;
+      // inputs the producer does not stage: in flight during the row's products
 #pragma unroll
-      for (int c = 0; c < kMaxWin; ++c) {
-        wsv[c] = c < W.nwin ? (int)bhp->ws[c] : 0x7fffffff;
-        wsb[c] = c < W.nwin ? (int)bhp->ws[c] - soff : 0;
-        soff += c < W.nwin ? W.cap[c] : 0;
-      }
+      for (int k = Epi::kInStaged; k < Epi::kIn; ++k) inr[k] = __ldg(e.in[k] + r0 + t);
     }
+    // staged x windows, addressed by the window-local column stream
+    const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
     double acc = 0.0;
     for (long long c = 0;; ++c) {
       mbar_wait(&cfull[cs], cph);
@@ -538,29 +586,39 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       if (t < nr) {
         // chunk-local indices: smem addressing stays 32-bit for any nnz
         const double* vs = reinterpret_cast<const double*>(st + CL.v) + h.dv;
-        const int* cis = reinterpret_cast<const int*>(st + CL.ci) + h.dci;
         const int lo = (int)(max(my_s, h.c0) - h.c0), hi = (int)(min(my_e, h.c1) - h.c0);
-        constexpr int U = Epi::kGatherBatch;
-        for (int k = lo; k < hi; k += U) {
-          double vv[U], xv[U];
+        if (A.wc) {
+          // staged window index per nonzero: no window search, half the bytes
+          const unsigned short* wcs = reinterpret_cast<const unsigned short*>(st + CL.ci) + h.dci;
+          constexpr int U = Epi::kWcBatch;
+          for (int k = lo; k < hi; k += U) {
+            double vv[U], xv[U];
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (k + u < hi) {
-              const int col = cis[k + u];
-              vv[u] = vs[k + u];
-              if (W.nwin) {
-                int b = wsb[0];
-#pragma unroll
-                for (int cc = 1; cc < kMaxWin; ++cc)
-                  if (col >= wsv[cc]) b = wsb[cc];
-                xv[u] = xw[col - b];
-              } else {
-                xv[u] = __ldg(x + col);
+            for (int u = 0; u < U; ++u)
+              if (k + u < hi) {
+                vv[u] = vs[k + u];
+                xv[u] = xw[wcs[k + u]];
               }
-            }
 #pragma unroll
-          for (int u = 0; u < U; ++u)
-            if (k + u < hi) acc = add(acc, mul(vv[u], xv[u]));
+            for (int u = 0; u < U; ++u)
+              if (k + u < hi) acc = add(acc, mul(vv[u], xv[u]));
+          }
+        } else {
+          // no windows: x gathered from global memory (L2)
+          const int* cis = reinterpret_cast<const int*>(st + CL.ci) + h.dci;
+          constexpr int U = Epi::kGatherBatch;
+          for (int k = lo; k < hi; k += U) {
+            double vv[U], xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (k + u < hi) {
+                vv[u] = vs[k + u];
+                xv[u] = __ldg(x + cis[k + u]);
+              }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+              if (k + u < hi) acc = add(acc, mul(vv[u], xv[u]));
+          }
         }
       }
       __syncwarp();
@@ -572,10 +630,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       if (h.last) break;
     }
     if (t < nr) {
-      double inr[Epi::kIn > 0 ? Epi::kIn : 1];
       const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
 #pragma unroll
-      for (int k = 0; k < Epi::kIn; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+      for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
       e.row(r0 + t, acc, inr);
     }
     __syncwarp();
@@ -614,7 +671,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bfull = reinterpret_cast<uint64_t*>(smem);
   uint64_t* bempty = bfull + kMaxStages;
-  const BlockLayout BL(W.total, Epi::kIn);
+  const BlockLayout BL(W.total, Epi::kInStaged);
   unsigned char* blk0 = smem + kPipeBarrierBytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -638,7 +695,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
       const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = Epi::kIn * bin;
+      uint32_t total = Epi::kInStaged * bin;
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0x7fffffff;
@@ -677,7 +734,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
             bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
           soff += cc < W.nwin ? W.cap[cc] : 0;
         }
-      } else if (lane >= 8 && lane < 8 + Epi::kIn) {
+      } else if (lane >= 8 && lane < 8 + Epi::kInStaged) {
         const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
       }
@@ -746,9 +803,11 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
         }
       }
       double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+#pragma unroll
+      for (int k = Epi::kInStaged; k < Epi::kIn; ++k) inr[k] = __ldg(e.in[k] + i);
       const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
 #pragma unroll
-      for (int k = 0; k < Epi::kIn; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+      for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
       e.row(i, acc, inr);
     }
     __syncwarp();

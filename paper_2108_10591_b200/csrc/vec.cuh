@@ -151,7 +151,7 @@ __global__ void dot_final_kernel(const double* partials, int nparts, double* out
   if (threadIdx.x == 0) *out = acc;
 }
 
-// batch of the 9 safe dots, compensated tree, into partials[blk*kPartStride]
+// batch of the 9 safe dots, compensated tree, into record blk of partials
 __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const double* s, const double* y,
                                                               const double* r, const double* r0s,
                                                               const double* t, double* partials,
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const
     acc[DH] = dot2_step(acc[DH], r0, tv);
     acc[DR] = dot2_step(acc[DR], rv, rv);
   }
-  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
+  block_reduce9<kThreads, false>(acc, partials + blockIdx.x);
 }
 
 // The batch of the next check as its own streaming kernel (s y r r0s t ->
@@ -205,13 +205,13 @@ __global__ void __launch_bounds__(kThreads) dots9_check_kernel(long long n, cons
     acc[DH] = dot2_step(acc[DH], r0, tv);
     acc[DR] = dot2_step(acc[DR], rv, rv);
   }
-  block_reduce9<kThreads, false>(acc, partials + (size_t)blockIdx.x * kPartStride);
+  block_reduce9<kThreads, false>(acc, partials + blockIdx.x);
   if (fuse) finalize_tail<kThreads, false>(st, partials, gridDim.x, replaced);
 }
 
 // PartitionPlan chains (reduction.py:282-283 with kernels.py:103-107): block w
 // handles range [bounds[w], bounds[w+1]); thread j < 9 sums pair j
-// sequentially in ascending index order -> partials[w*kPartStride + 2j].
+// sequentially in ascending index order -> field 2j of record w.
 __global__ void dots9_plan_kernel(const long long* bounds, const double* s, const double* y,
                                   const double* r, const double* r0s, const double* t,
                                   double* partials, const SolverState* st) {
@@ -225,8 +225,8 @@ __global__ void dots9_plan_kernel(const long long* bounds, const double* s, cons
   const long long lo = bounds[blockIdx.x], hi = bounds[blockIdx.x + 1];
   double acc = 0.0;
   for (long long k = lo; k < hi; ++k) acc = add(acc, mul(xa[k], ya[k]));
-  partials[(size_t)blockIdx.x * kPartStride + 2 * j] = acc;
-  partials[(size_t)blockIdx.x * kPartStride + 2 * j + 1] = 0.0;
+  partials[(size_t)(2 * j) * kMaxParts + blockIdx.x] = acc;
+  partials[(size_t)(2 * j + 1) * kMaxParts + blockIdx.x] = 0.0;
 }
 
 }  // namespace pbs

@@ -1,0 +1,42 @@
+"""Build alternative libpbsafe.so variants (extra -D flags) for A/B sweeps.
+
+    python tools/build_variants.py NAME=-DFOO=1,-DBAR=2 ...
+
+Writes paper_2108_10591_b200/variants/libpbsafe_NAME.so (git-ignored; travels
+with the gpurun snapshot) and prints each variant's csr_pipe register/spill
+lines.  Select one at run time with PBS_LIB=<path>.
+"""
+
+import os
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2108_10591_b200 import build as B  # noqa: E402
+
+OUT = os.path.join(B.HERE, "variants")
+
+
+def one(spec):
+    name, _, defs = spec.partition("=")
+    out = os.path.join(OUT, f"libpbsafe_{name}.so")
+    cmd = [B.nvcc(), *B.flags(), *[d for d in defs.split(",") if d], "-o", out, *B.SOURCES]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode:
+        return name, "FAILED\n" + p.stderr[-2000:]
+    lines, cur = [], None
+    for ln in p.stderr.splitlines():
+        if "Compiling entry function" in ln and "csr_pipe" in ln:
+            cur = subprocess.run(["c++filt", ln.split("'")[1]], capture_output=True, text=True).stdout.strip()[:48]
+        elif cur and "spill" in ln:
+            lines.append(f"  {cur:48s} {ln.split('info    :')[-1].strip()}")
+            cur = None
+    return name, out + "\n" + "\n".join(lines)
+
+
+if __name__ == "__main__":
+    os.makedirs(OUT, exist_ok=True)
+    with ThreadPoolExecutor(4) as ex:
+        for name, info in ex.map(one, sys.argv[1:]):
+            print(name, info)

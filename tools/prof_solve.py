@@ -35,12 +35,16 @@ def main():
     from paper_2108_10591_b200.operators import DeviceMatrix
 
     torch.cuda.set_device(0)
-    st = problems.config_stencil(args.config)
-    if args.operator == "csr":
+    if problems.CONFIGS[args.config]["kind"] == "random":
+        c = problems.CONFIGS[args.config]
+        rp, ci, v, _ = problems.random_banded_csr(c["n"], seed=c["seed"], col_dtype=np.int32)
+        dm = DeviceMatrix.from_csr((rp, ci, v))
+    elif args.operator == "csr":
+        st = problems.config_stencil(args.config)
         rp, ci, v = problems.stencil_csr(st, col_dtype=np.int32)
         dm = DeviceMatrix.from_csr((rp, ci, v))
     else:
-        dm = DeviceMatrix.from_stencil(st)
+        dm = DeviceMatrix.from_stencil(problems.config_stencil(args.config))
     n = dm.n_rows
     ones = torch.ones(n, dtype=torch.float64, device="cuda")
     b = torch.empty_like(ones)

@@ -1,7 +1,8 @@
-run() { echo "$1 $2: $(env $1 timeout 300 python tools/prof_solve.py --iters 60 --timing --repeat 2 $2 2>&1 | tail -1)"; }
-run "PBS_K3_DOTS=fused" ""
-run "PBS_K3_DOTS=split" ""
-run "PBS_K3_DOTS=fused" "--operator stencil"
-run "PBS_K3_DOTS=split" "--operator stencil"
-run "PBS_K3_DOTS=fused" "--operator stencil --config c4 --iters 20"
-run "PBS_K3_DOTS=split" "--operator stencil --config c4 --iters 20"
+# A/B sweep over env knobs
+run() { echo "$1 $2: $(env $1 timeout 300 python tools/prof_solve.py --iters 60 --timing --repeat 3 $2 2>&1 | tail -1)"; }
+for rep in 1 2; do
+run "PBS_FUSE_CHECK=1" ""
+run "PBS_FUSE_CHECK=0" ""
+done
+run "PBS_FUSE_CHECK=1" "--config c1 --iters 200"
+run "PBS_FUSE_CHECK=1" "--operator stencil"
