@@ -250,11 +250,13 @@ def run_ours(args):
         total_ms = float(t.item())
     iters_per_s = total_it / (total_ms / 1e3)  # iterations of the one global solve
 
-    # roofline of the dominant kernel (K3: Aw SpMV + l,g,s epilogue + 9 dot partials)
+    # roofline of the dominant kernel.  Matrix bytes at SURVEY 8(d)'s 12 B per
+    # nonzero (f64 value + int32 column) + row_ptr; the staged engine actually
+    # streams 10 B (u16 window-local columns), so `traffic` can sit below it.
     peak, peak_src = peaks()
     m_a = 12 * nnz + 8 * (n + 1)
-    k3_bytes = m_a + 12 * 8 * n     # w gather, As l g s y r r0s t reads, l g s writes
-    k12_bytes = m_a + 20 * 8 * n    # s gather, r p u t y l g w z x reads, As p u w t z y x r writes
+    k3_bytes = m_a + 11 * 8 * n     # w gather, As l g s y r r0s reads, l g s writes (+ dots a c d g)
+    k12_bytes = m_a + 21 * 8 * n    # s gather, r p u t y l g w z x r0s reads, As p u w t z y x r writes (+ b e f h r)
     it_bytes = 2 * m_a + 34 * 8 * n  # SURVEY 8(d) three-phase minimum (K1, K2, K3)
     it_bytes_fused = 2 * m_a + 32 * 8 * n  # this schedule: K1+K2 fused (As not re-read)
     kms = {name: sum(r.kernel_ms[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
@@ -264,15 +266,17 @@ def run_ours(args):
     k12_avg = kms["K1_As"] / max(kcnt["K1_As"], 1)
     k12_gbs = k12_bytes / (k12_avg * 1e-3) / 1e9
     if kms["K1_As"] > kms["K3_Aw_epilogue"]:  # dominant kernel = larger share of the step
-        dom = ("K12 (As CSR SpMV + fused p u w t z y x r updates)", k12_bytes, k12_avg, k12_gbs)
+        dom = ("K12 (As CSR SpMV + fused p u w t z y x r updates + dots b e f h r)", k12_bytes, k12_avg,
+               k12_gbs, "K1_As")
     else:
-        dom = ("K3 (Aw CSR SpMV + l,g,s updates + next 9-dot partials + fused check)", k3_bytes, k3_avg, k3_gbs)
+        dom = ("K3 (Aw CSR SpMV + l,g,s updates + dots a c d g + fused check)", k3_bytes, k3_avg, k3_gbs,
+               "K3_Aw_epilogue")
     tim_ms = sum(r.device_ms for r in tres)
     traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "k3_dram_bytes.json")
+    tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")  # from the committed ncu --set full capture
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("dram_bytes_per_launch")
+            traffic = json.load(open(tr_path)).get(dom[4], {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     kernels = {}
