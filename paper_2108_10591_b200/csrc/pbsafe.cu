@@ -410,6 +410,15 @@ static int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-row CSR
   }
   return v;
 }
+// Programmatic dependent launch per engine, PBS_PDL bitmask (A/B sweeps):
+// 1 staged CSR, 2 staged stencil, 4 direct stencil.  Default 1: the staged
+// CSR engine gains (its producer streams matrix chunks before the wait);
+// the direct stencil engine loses (profiles/sweeps/r1_pdl.log).
+enum { kPdlCsrPipe = 1, kPdlStencilPipe = 2, kPdlStencilDirect = 4 };
+static bool use_pdl(int engine) {
+  static int v = env_int("PBS_PDL", kPdlCsrPipe, 0, 7);
+  return (v & engine) != 0;
+}
 static int pipe_slots_cap() {
   static int v = env_int("PBS_PIPE_SLOTS", 2, 2, kMaxStages);
   return v;
@@ -518,6 +527,30 @@ static int stencil_pipe_config(pbs_ctx* ctx, const XWin& W, int* bslots, size_t*
   return rc;
 }
 
+// Launch with the programmatic-dependent-launch attribute when PBS_PDL is on
+// (kernels launched this way call griddep_wait before reading anything the
+// previous kernel wrote).
+template <class... KArgs, class... Args>
+static void launch_pdl(Launcher& L, int engine, void (*kernel)(KArgs...), int grid, int block, size_t smem,
+                       Args... args) {
+  if (!use_pdl(engine)) {
+    kernel<<<grid, block, smem, L.s>>>(args...);
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = L.s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (e != cudaSuccess) L.err = set_err(L.ctx, PBS_ERR_CUDA, std::string("PDL launch: ") + cudaGetErrorString(e));
+}
+
 template <class Epi>
 static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long long hi, int kind) {
   pbs_mat* m = L.m;
@@ -546,7 +579,10 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     }
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
-    csr_pipe_kernel<Epi><<<grid, kPipeThreads, smem, L.s>>>(A, x, epi, W, bslots, cstages, chunk);
+    // programmatic dependent launch: overlaps this CTA's prologue and first
+    // matrix chunks with the previous kernel's drain
+    launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi>, grid, kPipeThreads, smem, A, x, epi, W, bslots, cstages, chunk);
+    if (L.err) return 0;
   } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>()) {
     StencilView S = m->sv;
     S.row_lo = lo;
@@ -560,8 +596,9 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     }
     const long long cap = (long long)L.ctx->sms * ctas;
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
-#define PBS_SPIPE(D, NP)                                                                                  \
-  stencil_pipe_kernel<Epi, D, NP><<<grid, kPipeThreads, smem, L.s>>>(S, x, epi, m->xwin, m->swin, bslots);
+#define PBS_SPIPE(D, NP)                                                                                   \
+  launch_pdl(L, kPdlStencilPipe, stencil_pipe_kernel<Epi, D, NP>, grid, kPipeThreads, smem, S, x, epi, m->xwin, \
+             m->swin, bslots);
     if (S.dim == 3 && S.npts == 7) PBS_SPIPE(3, 7)
     else if (S.dim == 3 && S.npts == 27) PBS_SPIPE(3, 27)
     else if (S.dim == 3) PBS_SPIPE(3, 0)
@@ -577,7 +614,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
 #define PBS_STENCIL(D, NP)                                                                 \
   {                                                                                        \
     grid = grid_for(L.ctx, (const void*)stencil_spmv_kernel<Epi, D, NP>, nblk);            \
-    stencil_spmv_kernel<Epi, D, NP><<<grid, kThreads, 0, L.s>>>(S, x, epi);               \
+    launch_pdl(L, kPdlStencilDirect, stencil_spmv_kernel<Epi, D, NP>, grid, kThreads, 0, S, x, epi); \
   }
     if (S.dim == 3 && S.npts == 7) PBS_STENCIL(3, 7)
     else if (S.dim == 3 && S.npts == 27) PBS_STENCIL(3, 27)
@@ -890,6 +927,17 @@ static void final_ss(Launcher& L, Workspace* ws, const Mode& md) {
 
 typedef void (*IterFn)(Launcher&, Workspace*, const Mode&);
 
+// steady iterations per graph (PBS_GRAPH_ITERS, default 4): inside one graph
+// K3 -> next K12 is a programmatic edge too, so the next iteration's matrix
+// stream starts while the check tail runs
+static int graph_iters() {
+  static int v = env_int("PBS_GRAPH_ITERS", 4, 1, 16);
+  return v;
+}
+static void iter_steady_batch(Launcher& L, Workspace* ws, const Mode& md) {
+  for (int k = 0; k < graph_iters(); ++k) iter_steady(L, ws, md);
+}
+
 static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const Mode& md,
                      cudaGraphExec_t* out, long long* nkernels) {
   Workspace* ws = m->ws;
@@ -1166,9 +1214,21 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
       std::this_thread::yield();
     }
     {
-      const bool replace = rr && (j % cfg->rr_epoch == 0) && 0 < j && j < cutoff;
+      auto is_replace = [&](long long i) { return rr && (i % cfg->rr_epoch == 0) && 0 < i && i < cutoff; };
+      const bool replace = is_replace(j);
       IterFn fn = !pipelined ? iter_ss : (replace ? iter_replace : iter_steady);
-      if (graphs) {
+      const int gu = graph_iters();
+      bool batch = graphs && pipelined && gu > 1 && j + gu <= cfg->max_iters;
+      for (long long i = j; batch && i < j + gu; ++i) batch = !is_replace(i);
+      if (batch) {
+        cudaGraphExec_t ge;
+        long long nk = 0;
+        int rc = get_graph(ctx, m, key_base + 8, iter_steady_batch, md, &ge, &nk);
+        if (rc) return rc;
+        CK(cudaGraphLaunch(ge, s));
+        launched_graph_kernels += nk;
+        j += gu - 1;
+      } else if (graphs) {
         long long key = key_base + (!pipelined ? 2 : (replace ? 1 : 0));
         cudaGraphExec_t ge;
         long long nk = 0;

@@ -47,6 +47,19 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch.  wait: block until the grids this one depends
+// on have completed and their writes are visible (a no-op for a kernel
+// launched without the programmatic attribute).  launch_dependents: this CTA
+// no longer holds back the dependent grid's launch.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// CTA-wide named barrier 2 (all threads of the pipelined engines)
+template <int kThreadsIn>
+__device__ __forceinline__ void cta_sync2() {
+  asm volatile("bar.sync 2, %0;" ::"n"(kThreadsIn) : "memory");
+}
+
 // named barrier over the consumer warps only (the producer warp never joins)
 template <int kThreadsIn>
 __device__ __forceinline__ void consumer_sync() {

@@ -400,17 +400,17 @@ struct ChunkLayout {
 };
 constexpr size_t kPipeBarrierBytes = 512;
 
+// Launched with programmatic dependent launch: the CTA comes up while the
+// previous kernel drains, the producer streams its first block's nonzeros
+// (the matrix does not depend on the previous kernel), and only then does
+// every thread wait for the previous grid (griddep_wait) and take the CTA's
+// one gate decision.  Consumers release the next kernel's launch once their
+// rows are written, before the dot reduction / check tail.
 template <class Epi>
 __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
                                                                    Epi epi, XWin W, int bslots, int cstages,
                                                                    int chunk) {
   __shared__ int go;
-  if (threadIdx.x == 0) {
-    go = epi.active();  // one gate decision per CTA
-    if (!go && blockIdx.x == 0) epi.on_skip();
-  }
-  __syncthreads();
-  if (!go) return;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* cfull = reinterpret_cast<uint64_t*>(smem);
   uint64_t* cempty = cfull + kMaxStages;
@@ -444,6 +444,17 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
     int cs = 0, bs = 0;
     uint32_t cph = 0, bph = 0;
     long long pf_base = 0, pf_end = 0;
+    bool gated = false;
+    int issued = 0;  // chunk stages filled before the gate
+    auto gate = [&]() -> bool {
+      gated = true;
+      griddep_wait();
+      cta_sync2<kPipeThreads>();  // thread 0 (a consumer) has taken the gate decision
+      if (go) return true;
+      for (int s2 = 0; s2 < issued; ++s2) mbar_wait(&cfull[s2], 0);  // let the early copies land
+      return false;
+    };
+    if (nblk <= blockIdx.x && !gate()) return;
     for (long long blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
       const int slot = (int)(q & 31);
       if (slot == 0) {  // prefetch bounds of blocks q .. q+31 of this CTA
@@ -464,6 +475,46 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       const long long nch = end > base ? (end - base + chunk - 1) / chunk : 1;
       const uint32_t brp = (uint32_t)(((nr + dr + 2) & ~1) * sizeof(long long));
       const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
+      // chunk stage c of this block: the block's nonzero range
+      auto issue_chunk = [&](long long c) {
+        mbar_wait(&cempty[cs], cph ^ 1);
+        unsigned char* st = chk0 + (size_t)cs * CL.bytes;
+        const long long c0 = base + c * chunk;
+        const long long c1 = min(end, c0 + chunk);
+        const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
+        // column stream: window-local u16 indices (8 per 16 bytes) or int32
+        const long long cal = A.wc ? 7 : 3;
+        const long long c0b = c0 & ~cal, c1b = (c1 + cal) & ~cal;
+        const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
+        const uint32_t bc = (uint32_t)((c1b - c0b) * (A.wc ? sizeof(unsigned short) : sizeof(int)));
+        if (lane == 0) {
+          ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
+          h->c0 = c0;
+          h->c1 = c1;
+          h->dv = (int)(c0 - c0a);
+          h->dci = (int)(c0 - c0b);
+          h->last = c == nch - 1;
+          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
+        }
+        __syncwarp();
+        if (lane == 0 && bv) bulk_g2s(st + CL.v, A.v + c0a, bv, &cfull[cs]);
+        if (lane == 1 && bc)
+          bulk_g2s(st + CL.ci, A.wc ? (const void*)(A.wc + c0b) : (const void*)(A.ci + c0b), bc, &cfull[cs]);
+        if (++cs == cstages) {
+          cs = 0;
+          cph ^= 1;
+        }
+      };
+      // first block: the matrix chunks that fit the free stages go before the
+      // gate (they do not depend on the previous kernel); the rest follow the
+      // block slot, as on every later block (consumers need the slot first)
+      long long cfirst = 0;
+      if (!gated) {
+        cfirst = nch < cstages ? nch : cstages;
+        for (long long c = 0; c < cfirst; ++c) issue_chunk(c);
+        issued = (int)cfirst;
+        if (!gate()) return;
+      }
       // x windows of this block (every lane computes them; lane 1+c copies window c)
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
@@ -520,41 +571,19 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         bs = 0;
         bph ^= 1;
       }
-      // chunk stages: the block's nonzero range
-      for (long long c = 0; c < nch; ++c) {
-        mbar_wait(&cempty[cs], cph ^ 1);
-        unsigned char* st = chk0 + (size_t)cs * CL.bytes;
-        const long long c0 = base + c * chunk;
-        const long long c1 = min(end, c0 + chunk);
-        const long long c0a = c0 & ~1LL, c1a = (c1 + 1) & ~1LL;
-        // column stream: window-local u16 indices (8 per 16 bytes) or int32
-        const long long cal = A.wc ? 7 : 3;
-        const long long c0b = c0 & ~cal, c1b = (c1 + cal) & ~cal;
-        const uint32_t bv = (uint32_t)((c1a - c0a) * sizeof(double));
-        const uint32_t bc = (uint32_t)((c1b - c0b) * (A.wc ? sizeof(unsigned short) : sizeof(int)));
-        if (lane == 0) {
-          ChunkHdr* h = reinterpret_cast<ChunkHdr*>(st);
-          h->c0 = c0;
-          h->c1 = c1;
-          h->dv = (int)(c0 - c0a);
-          h->dci = (int)(c0 - c0b);
-          h->last = c == nch - 1;
-          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
-        }
-        __syncwarp();
-        if (lane == 0 && bv) bulk_g2s(st + CL.v, A.v + c0a, bv, &cfull[cs]);
-        if (lane == 1 && bc)
-          bulk_g2s(st + CL.ci, A.wc ? (const void*)(A.wc + c0b) : (const void*)(A.ci + c0b), bc, &cfull[cs]);
-        if (++cs == cstages) {
-          cs = 0;
-          cph ^= 1;
-        }
-      }
+      for (long long c = cfirst; c < nch; ++c) issue_chunk(c);
     }
     return;
   }
 
   // ------------------------------------------------------------- consumers
+  griddep_wait();
+  if (threadIdx.x == 0) {
+    go = epi.active();  // one gate decision per CTA
+    if (!go && blockIdx.x == 0) epi.on_skip();
+  }
+  cta_sync2<kPipeThreads>();
+  if (!go) return;
   Epi e = epi;
   e.init();
   const int t = threadIdx.x;
@@ -642,6 +671,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       bph ^= 1;
     }
   }
+  griddep_launch();  // rows written: the next kernel may start its prologue
   e.template finish<kPipeRows, true>();
 }
 
@@ -662,6 +692,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
                                                                        const double* __restrict__ x, Epi epi,
                                                                        XWin W, StencilWin SW, int bslots) {
   __shared__ int go;
+  griddep_wait();  // PDL: everything here reads the previous kernel's output
   if (threadIdx.x == 0) {
     go = epi.active();
     if (!go && blockIdx.x == 0) epi.on_skip();
@@ -817,6 +848,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
       bph ^= 1;
     }
   }
+  griddep_launch();
   e.template finish<kPipeRows, true>();
 }
 
@@ -884,6 +916,7 @@ template <class Epi, int DIM, int NP>
 __global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel(const __grid_constant__ StencilView S,
                                                                 const double* __restrict__ x, Epi epi) {
   __shared__ int go;
+  griddep_wait();  // PDL: everything here reads the previous kernel's output
   if (threadIdx.x == 0) {
     go = epi.active();  // one gate decision per CTA
     if (!go && blockIdx.x == 0) epi.on_skip();
@@ -928,6 +961,7 @@ __global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel
     }
     e.row(i, acc, inr);
   }
+  griddep_launch();
   e.template finish<kThreads, false>();
 }
 
