@@ -402,6 +402,13 @@ static int pipe_chunk_cap() {
   static int v = env_int("PBS_PIPE_CHUNK", 2048, 256, kPipeChunkMax) & ~3;
   return v;
 }
+// band mode runs one CTA per SM (the circular x buffer takes 84+ KiB), where
+// larger chunks stream better (profiles/sweeps/r1_band.log: config 3, 2048 ->
+// 3072 nonzeros per chunk, 705 -> 667 us per iteration)
+static int band_chunk_cap() {
+  static int v = env_int("PBS_BAND_CHUNK", 3072, 256, kPipeChunkMax) & ~3;
+  return v;
+}
 static int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-row CSR engine
   static int v = -1;
   if (v < 0) {
@@ -434,7 +441,7 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   const BlockLayout BL(W.total, Epi::kInStaged);
   // one chunk per row block when the densest block fits the cap (stencils:
   // ~7 or ~27 nonzeros per row), else cap-sized chunks
-  int ch = pipe_chunk_cap();
+  int ch = W.band_s ? band_chunk_cap() : pipe_chunk_cap();
   if (blk_nnz_max > 0 && blk_nnz_max < ch) ch = (int)((blk_nnz_max + 3) & ~3LL);
   const ChunkLayout CL(ch, colb);
   int per_sm = 0, optin = 0;
@@ -446,7 +453,9 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
     // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
     size_t budget = (size_t)per_sm / c - 1024 - 2048;
     if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
-    budget -= kPipeBarrierBytes;
+    const size_t fixed = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double);
+    if (budget <= fixed) continue;
+    budget -= fixed;
     n = (int)(budget / (BL.bytes + CL.bytes));
     if (n > pipe_slots_cap()) n = pipe_slots_cap();
     if (n < 2) continue;
@@ -462,7 +471,7 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   *bslots = n;
   *cstages = n + xc;
   *chunk = ch;
-  *smem = kPipeBarrierBytes + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
+  *smem = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double) + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
   const void* k = (const void*)csr_pipe_kernel<Epi>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
@@ -1499,6 +1508,11 @@ __global__ void offset_bins_kernel(const long long* rp, const int* ci, long long
 __global__ void window_cols_kernel(const long long* rp, const int* ci, long long n_rows, long long n_cols, XWin W,
                                    unsigned short* wc, int* bad) {
   const long long stride = (long long)gridDim.x * blockDim.x;
+  if (W.band_s) {  // band mode: the column's slot in the circular buffer
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride)
+      for (long long k = rp[i]; k < rp[i + 1]; ++k) wc[k] = (unsigned short)(ci[k] % W.band_s);
+    return;
+  }
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n_rows; i += stride) {
     const long long r0 = i / kPipeRows * kPipeRows;
     const long long nr = min((long long)kPipeRows, n_rows - r0);
@@ -1541,7 +1555,7 @@ static int build_window_cols(pbs_ctx* ctx, pbs_mat* m) {
     pool_free(ctx, m->wc);
     m->wc = nullptr;
   }
-  if (!m->xwin.nwin || m->nnz == 0 || m->xwin.total > 65535) return PBS_OK;
+  if ((!m->xwin.nwin && !m->xwin.band_s) || m->nnz == 0 || m->xwin.total > 65535) return PBS_OK;
   cudaStream_t s = ctx->stream;
   int* bad = nullptr;
   CK(pool_alloc(ctx, &m->wc, sizeof(unsigned short) * (m->nnz + 16)));
@@ -1615,7 +1629,22 @@ static int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
     W.cap[c] = (int)cap;
     total += cap;
   }
-  if (total > kMaxWinElems || cl.empty()) return PBS_OK;  // too spread: gather mode
+  if (cl.empty()) return PBS_OK;
+  if (total > kMaxWinElems) {
+    // too spread for per-block windows: a band (one circular x buffer per
+    // CTA over a contiguous run of blocks) when the whole offset range is
+    // narrow enough, else gather x
+    const long long lo = cl.front().first, hi = cl.back().second;
+    // even size: the pieces stay 16-byte aligned in the circular buffer
+    const long long bs = (hi - lo + 2LL * kPipeRows + 8 + 255) / 256 * 256;
+    if (bs > kBandMaxElems || env_int("PBS_NO_BAND", 0, 0, 1)) return PBS_OK;
+    XWin B{};
+    B.band_s = (int)bs;
+    B.band_lo = (int)lo;
+    B.band_hi = (int)hi;
+    m->xwin = B;
+    return m->stencil ? PBS_OK : build_window_cols(ctx, m);
+  }
   W.nwin = (int)cl.size();
   W.total = (int)total;
   m->xwin = W;
@@ -1942,7 +1971,7 @@ PBS_EXPORT int pbs_spmv_dev(pbs_mat* m, const double* d_x, double* d_y, int64_t*
   e.st = ctx->tmp_state;
   e.tag = PBS_TAG_AX;
   const double* xin = d_x;
-  if (m->xwin.nwin) {
+  if (m->xwin.nwin || m->xwin.band_s) {
     // staged x windows are copied in 16-byte units and may read one element
     // past the end of x: stage a caller's x into a padded buffer
     double* xs = nullptr;

@@ -352,6 +352,7 @@ constexpr int kPipeThreads = kPipeRows + 32;  // + one producer warp
 constexpr int kMaxStages = 8;
 constexpr int kMaxWin = 4;            // x windows per row block
 constexpr int kMaxWinElems = 4096;    // staged x elements per row block (32 KiB)
+constexpr int kBandMaxElems = 16384;  // band mode's circular x buffer, at most (128 KiB)
 
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
 
@@ -364,6 +365,13 @@ struct XWin {
   int wmin[kMaxWin], wmax[kMaxWin];
   int cap[kMaxWin];  // staged elements reserved per cluster (even)
   int total;         // sum of cap
+  // band mode (nwin == 0, band_s > 0): every row's offsets lie in
+  // [band_lo, band_hi] but the span is too wide for per-block windows.  Each
+  // CTA then takes a contiguous run of row blocks and keeps x in a circular
+  // shared buffer of band_s doubles, x[g] at g % band_s, adding only each
+  // block's new columns.
+  int band_s;
+  int band_lo, band_hi;
 };
 
 struct BlockHdr {
@@ -418,7 +426,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   uint64_t* bempty = bfull + kMaxStages;
   const BlockLayout BL(W.total, Epi::kInStaged);
   const ChunkLayout CL(chunk, A.wc ? 2 : 4);
-  unsigned char* blk0 = smem + kPipeBarrierBytes;
+  double* xband = reinterpret_cast<double*>(smem + kPipeBarrierBytes);  // band mode only
+  unsigned char* blk0 = smem + kPipeBarrierBytes + (size_t)W.band_s * sizeof(double);
   unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -434,7 +443,17 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   }
   __syncthreads();
   const long long nrows = A.row_hi - A.row_lo;
-  const long long nblk = (nrows + kPipeRows - 1) / kPipeRows;
+  const long long nblk_all = (nrows + kPipeRows - 1) / kPipeRows;
+  // blocks of this CTA: strided (blockIdx.x, + gridDim.x, ...) or, in band
+  // mode, a contiguous run [first_blk, nblk)
+  const bool band = W.band_s > 0;
+  long long first_blk = blockIdx.x, nblk = nblk_all, bstep = gridDim.x;
+  if (band) {
+    const long long per = (nblk_all + gridDim.x - 1) / gridDim.x;
+    first_blk = (long long)blockIdx.x * per;
+    nblk = min(nblk_all, first_blk + per);
+    bstep = 1;
+  }
 
   if (warp == kConsumerWarps) {
     // ----------------------------------------------------------- producer
@@ -454,11 +473,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       for (int s2 = 0; s2 < issued; ++s2) mbar_wait(&cfull[s2], 0);  // let the early copies land
       return false;
     };
-    if (nblk <= blockIdx.x && !gate()) return;
-    for (long long blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
+    long long xhi = 0;  // band mode: x staged up to here (exclusive)
+    if (nblk <= first_blk && !gate()) return;
+    for (long long blk = first_blk, q = 0; blk < nblk; blk += bstep, ++q) {
       const int slot = (int)(q & 31);
       if (slot == 0) {  // prefetch bounds of blocks q .. q+31 of this CTA
-        const long long b2 = blk + (long long)lane * gridDim.x;
+        const long long b2 = blk + (long long)lane * bstep;
         if (b2 < nblk) {
           const long long rr0 = A.row_lo + b2 * kPipeRows;
           const long long rr1 = min(A.row_hi, rr0 + kPipeRows);
@@ -537,6 +557,30 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
           }
         }
       }
+      // band mode: the block's new columns [xhi, hi), as up to two pieces of
+      // the circular buffer (lanes 1 and 2 copy them)
+      long long bnd0 = 0, bnd1 = 0;
+      uint32_t bb0 = 0, bb1 = 0;
+      if (band) {
+        long long lo = r0 + W.band_lo, hi = r0 + nr - 1 + W.band_hi + 1;
+        if (lo < 0) lo = 0;
+        if (hi > A.n_cols) hi = A.n_cols;
+        lo &= ~1LL;
+        hi = (hi + 1) & ~1LL;
+        if (q == 0 || lo >= xhi) xhi = lo;  // first block of the run: fill from lo
+        if (hi > xhi) {
+          const long long room = W.band_s - xhi % W.band_s;
+          const long long n0 = min(hi - xhi, room);
+          bnd0 = xhi;
+          bb0 = (uint32_t)(n0 * sizeof(double));
+          if (hi - xhi > n0) {
+            bnd1 = xhi + n0;
+            bb1 = (uint32_t)((hi - xhi - n0) * sizeof(double));
+          }
+          total += bb0 + bb1;
+          xhi = hi;
+        }
+      }
       mbar_wait(&bempty[bs], bph ^ 1);
       unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
       if (lane == 0) {
@@ -554,6 +598,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       __syncwarp();
       if (lane == 0) {
         bulk_g2s(bst + BL.rp, A.rp + r0a, brp, &bfull[bs]);
+      } else if (band && lane <= 2) {
+        // the slot of block blk - bslots is free, so no block still being
+        // consumed needs the columns these pieces overwrite
+        // (band_s >= band span + 2 * 256 + 4, checked at upload)
+        if (lane == 1 && bb0) bulk_g2s(xband + bnd0 % W.band_s, x + bnd0, bb0, &bfull[bs]);
+        if (lane == 2 && bb1) bulk_g2s(xband + bnd1 % W.band_s, x + bnd1, bb1, &bfull[bs]);
       } else if (lane <= W.nwin) {
         // lane 1+c copies window c (static indexing keeps wlo/wbytes in registers)
         int soff = 0;
@@ -589,7 +639,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
   const int t = threadIdx.x;
   int cs = 0, bs = 0;
   uint32_t cph = 0, bph = 0;
-  for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  for (long long blk = first_blk; blk < nblk; blk += bstep) {
     mbar_wait(&bfull[bs], bph);
     const unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
     const BlockHdr* bhp = reinterpret_cast<const BlockHdr*>(bst);
@@ -605,8 +655,9 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
 #pragma unroll
       for (int k = Epi::kInStaged; k < Epi::kIn; ++k) inr[k] = __ldg(e.in[k] + r0 + t);
     }
-    // staged x windows, addressed by the window-local column stream
-    const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
+    // staged x windows (or the band buffer), addressed by the window-local
+    // column stream
+    const double* xw = band ? xband : reinterpret_cast<const double*>(bst + BL.xw);
     double acc = 0.0;
     for (long long c = 0;; ++c) {
       mbar_wait(&cfull[cs], cph);

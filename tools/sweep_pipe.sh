@@ -1,12 +1,9 @@
 # A/B sweep over env knobs (graph mode, device-time per iteration)
-run() { echo "$1 $2: $(env $1 timeout 300 python tools/prof_solve.py --iters 300 --graphs --repeat 3 $2 2>&1 | tail -1)"; }
-for rep in 1 2; do
-run "PBS_PDL=1" "--operator stencil"
-run "PBS_PDL=3" "--operator stencil"
-run "PBS_PDL=5" "--operator stencil"
-done
-run "PBS_PDL=1" "--config c4 --operator stencil --iters 30"
-run "PBS_PDL=3" "--config c4 --operator stencil --iters 30"
-run "PBS_PDL=1" "--config c1 --operator stencil --iters 300"
-run "PBS_PDL=3" "--config c1 --operator stencil --iters 300"
-run "PBS_PDL=7" "--config c1 --operator stencil --iters 300"
+run() { echo "$1 $2: $(env $1 timeout 100 python tools/prof_solve.py --iters 40 --graphs --repeat 2 $2 2>&1 | tail -1)"; }
+run "PBS_PIPE_SLOTS=3 PBS_PIPE_CHUNK=3072" "--config c3"
+run "PBS_PIPE_SLOTS=3 PBS_PIPE_CHUNK=1536" "--config c3"
+run "PBS_PIPE_SLOTS=4 PBS_PIPE_CHUNK=1536" "--config c3"
+run "PBS_PIPE_SLOTS=4 PBS_PIPE_CHUNK=1024" "--config c3"
+run "PBS_PIPE_SLOTS=2 PBS_PIPE_CHUNK=2048 PBS_PIPE_XCHUNK=2" "--config c3"
+run "PBS_PIPE_SLOTS=3 PBS_PIPE_CHUNK=1024 PBS_PIPE_XCHUNK=2" "--config c3"
+run "PBS_PIPE_SLOTS=2 PBS_PIPE_CHUNK=4096" "--config c3"
