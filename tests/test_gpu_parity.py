@@ -486,3 +486,81 @@ def test_config4_27point_iterations_track_oracle_scaled(pb):
     assert abs(o1.iterations - ref["iterations"]) <= max(2, 0.02 * ref["iterations"])
     sm.free()
     csr.free()
+
+
+# ------------------------------------------------------ staged-engine modes
+
+def _spmv_dev(dm, x):
+    import torch
+
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    assert dm.spmv_dev(xd.data_ptr(), yd.data_ptr()) == -1
+    torch.cuda.synchronize()
+    return yd.cpu().numpy()
+
+
+def _upload(rp, ci, v, **env):
+    from paper_2108_10591_b200.operators import DeviceMatrix
+
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(val) for k, val in env.items()})
+    try:  # the x-window / band decision is taken at upload
+        return DeviceMatrix.from_csr((rp, ci.astype(np.int32), v))
+    finally:
+        for k, val in old.items():
+            if val is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = val
+
+
+@pytest.mark.parametrize("n,lo,hi", [(200_003, -3000, 3000),   # symmetric band, ragged last block
+                                     (120_000, 0, 7000),       # upper band only
+                                     (90_001, -9000, 100),     # lower band, span near the 16k cap
+                                     (3000, -2500, 2500)])     # fewer blocks than CTAs
+def test_band_mode_spmv_bitwise(pb, n, lo, hi):
+    """Band mode (per-CTA circular x buffer) and gather mode give the
+    reference's row sums bitwise, for bands too wide for per-block windows."""
+    rng = np.random.default_rng(n)
+    rows, cols = [], []
+    for i in range(n):
+        a, b_ = max(0, i + lo), min(n - 1, i + hi)
+        k = rng.integers(3, 12)
+        c = np.unique(np.concatenate([[i], rng.integers(a, b_ + 1, k)]))
+        rows.append(np.full(c.size, i))
+        cols.append(c)
+    r = np.concatenate(rows)
+    c = np.concatenate(cols)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, r + 1, 1)
+    rp = np.cumsum(rp)
+    v = rng.uniform(-1, 1, c.size)
+    x = rng.standard_normal(n)
+    ref = orc.spmv(rp, c, v, x)
+    band = _upload(rp, c, v)
+    gather = _upload(rp, c, v, PBS_NO_BAND=1)
+    assert np.array_equal(_spmv_dev(band, x), ref)
+    assert np.array_equal(_spmv_dev(gather, x), ref)
+    band.free()
+    gather.free()
+
+
+def test_band_mode_plan_solve_bitwise_vs_oracle(pb):
+    """A whole solve through the band-mode engine in the reference's
+    PartitionPlan order: every rel and x bitwise equal to the oracle."""
+    from paper_2108_10591_b200 import problems
+
+    rp, ci, v, b = problems.random_banded_csr(150_000, seed=7, half_window=3000)
+    dm = _upload(rp, ci, v)
+    ref = orc.solve(rp, ci, v, b, tol=1e-10, max_iters=400, workers=8, threads=os.cpu_count() or 1)
+    out = pb.solve(dm, b, config=pb.SolverConfig(tol=1e-10, max_iters=400),
+                   engine=pb.DeviceEngine(reduce="plan", workers=8))
+    assert out.iterations == ref["iterations"]
+    assert np.array_equal([r.rel_res_recur for r in out.history], ref["rel"])
+    assert np.array_equal(out.x, ref["x"])
+    # the fast path: same operator, near-exact dots -> the oracle's near-exact run
+    ref2 = orc.solve(rp, ci, v, b, tol=1e-30, max_iters=10, workers=-1, threads=os.cpu_count() or 1)
+    fast = pb.solve(dm, b, config=pb.SolverConfig(tol=1e-30, max_iters=10))
+    np.testing.assert_allclose([r.rel_res_recur for r in fast.history], ref2["rel"], rtol=1e-12)
+    dm.free()
