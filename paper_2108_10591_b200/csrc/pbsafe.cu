@@ -803,8 +803,8 @@ static bool fuse_check() {
   return v;
 }
 
-static bool k12_dots() {
-  static int v = env_int("PBS_K12_DOTS", 1, 0, 1);
+static int k12_dots() {
+  static int v = env_int("PBS_K12_DOTS", 1, 0, 2);
   return v;
 }
 
@@ -856,7 +856,7 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
 // (Aw + l g s + the fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  if (!md.plan && !k3_dots_split() && k12_dots() && !L.m->stencil) {
+  if (!md.plan && !k3_dots_split() && k12_dots() && (!L.m->stencil || k12_dots() == 2)) {
     const int fuse = L.trace_cfg || !fuse_check() ? 0 : 1;
     const int np12 = spmv_launch(L, ws->X.v[VS], epi_k12d(ws, md), 0, ws->n, KK1);
     const int grid = spmv_launch(L, ws->X.v[VW], epi_k3s(ws, md, fuse, np12), 0, ws->n, KK3);
@@ -1736,8 +1736,17 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
   S.n = n;
   S.k = k;
   S.k2 = k * k;
+  S.dk = make_fastdiv(S.k);
+  S.dk2 = make_fastdiv(S.k2);
   S.dim = dim;
   S.npts = npts;
+  for (int a = 0; a < 3; ++a) S.nlo[a] = S.nhi[a] = 0xffffffffu;
+  for (int p = 0; p < npts; ++p)
+    for (int a = 0; a < dim; ++a) {
+      const int d = offsets[p * dim + a];
+      if (d == -1) S.nlo[3 - dim + a] &= ~(1u << p);
+      if (d == 1) S.nhi[3 - dim + a] &= ~(1u << p);
+    }
   long long nnz = 0;
   long long prev = -(1LL << 62);
   for (int p = 0; p < npts; ++p) {
@@ -1822,12 +1831,12 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
 __device__ __forceinline__ bool stencil_in(const StencilView& S, long long i, int p) {
   int c[3] = {0, 0, 0};
   if (S.dim == 3) {
-    const long long z = i / S.k2, rem = i - z * S.k2, yy = rem / S.k;
+    const long long z = S.dk2.div(i), rem = i - z * S.k2, yy = S.dk.div(rem);
     c[0] = (int)z;
     c[1] = (int)yy;
     c[2] = (int)(rem - yy * S.k);
   } else if (S.dim == 2) {
-    const long long yy = i / S.k;
+    const long long yy = S.dk.div(i);
     c[1] = (int)yy;
     c[2] = (int)(i - yy * S.k);
   } else {

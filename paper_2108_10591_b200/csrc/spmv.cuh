@@ -45,6 +45,9 @@ namespace pbs {
 #ifndef PBS_WCB_K3S
 #define PBS_WCB_K3S 4
 #endif
+#ifndef PBS_K12D_MINB
+#define PBS_K12D_MINB 1
+#endif
 
 struct CsrView {
   const long long* rp;
@@ -57,13 +60,56 @@ struct CsrView {
   const unsigned short* wc;
 };
 
+// Division of a row index i < 2^31 by an invariant d >= 1 with one 32x32->64
+// multiply and a shift: m = ceil(2^(31+l) / d), l = ceil(log2 d), s = 31 + l
+// gives floor(i * m / 2^s) == i / d for all i < 2^31 (Granlund-Montgomery);
+// m < 2^32.  The grid coordinates of every stencil row use it instead of a
+// 64-bit division.
+struct FastDiv {
+  unsigned long long m;
+  int s;
+  __host__ __device__ __forceinline__ long long div(long long i) const {
+    return (long long)(((unsigned long long)(unsigned)i * m) >> s);
+  }
+};
+
+__host__ inline FastDiv make_fastdiv(long long d) {
+  int l = 0;
+  while ((1LL << l) < d) ++l;
+  const unsigned __int128 two = (unsigned __int128)1 << (31 + l);
+  FastDiv f;
+  f.m = (unsigned long long)((two + (unsigned __int128)d - 1) / (unsigned __int128)d);
+  f.s = 31 + l;
+  return f;
+}
+
 struct StencilView {
   long long n, k, k2;
+  FastDiv dk, dk2;  // i / k, i / k^2
+  // boundary masks (offsets are in {-1, 0, 1} per axis): bit p of nlo[a] is
+  // clear when point p steps -1 along axis a, of nhi[a] when it steps +1; a
+  // row at coordinate 0 (k - 1) on axis a keeps only the points in nlo[a]
+  // (nhi[a]) — the Dirichlet elimination as two masks per axis instead of a
+  // bounds test per point and axis
+  unsigned nlo[3], nhi[3];
   int dim, npts;
   int off[kMaxStencil][3];      // (dz,)dy,dx per point, padded to 3 axes from the left
   long long foff[kMaxStencil];  // flattened offset
   double coef[kMaxStencil];
   long long row_lo, row_hi;
+  // neighbours of the row at grid coordinates c (padded to 3 axes) that lie
+  // in the grid, as a bit mask over the points
+  __device__ __forceinline__ unsigned valid_mask(const int (&c)[3], int dim) const {
+    const int km1 = (int)k - 1;
+    unsigned vm = 0xffffffffu;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (a < 3 - dim) continue;
+      if (c[a] == 0) vm &= nlo[a];
+      if (c[a] == km1) vm &= nhi[a];
+    }
+    return vm;
+  }
 };
 
 // ---------------------------------------------------------------- epilogues
@@ -191,7 +237,7 @@ struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-loca
   static constexpr int kIn = DOTS ? 12 : 11;
   static constexpr int kInStaged = 11;  // r0s (DOTS) is loaded by the consumer thread
   static constexpr int kWcBatch = DOTS ? PBS_WCB_K12D : 4;  // staged-window products in flight per row
-  static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
+  static constexpr int kMinBlocks = DOTS ? PBS_K12D_MINB : 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
   static constexpr int kGatherBatch = DOTS ? 4 : 8;  // x gathers in flight per row
   double* as;  // As is kept for K3
@@ -844,14 +890,14 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
       const long long i = r0 + t;
       int c[3] = {0, 0, 0};
       if (DIM == 3) {
-        const long long z = i / S.k2;
+        const long long z = S.dk2.div(i);
         const long long rem = i - z * S.k2;
-        const long long yy = rem / S.k;
+        const long long yy = S.dk.div(rem);
         c[0] = (int)z;
         c[1] = (int)yy;
         c[2] = (int)(rem - yy * S.k);
       } else if (DIM == 2) {
-        const long long yy = i / S.k;
+        const long long yy = S.dk.div(i);
         c[1] = (int)yy;
         c[2] = (int)(i - yy * S.k);
       } else {
@@ -868,18 +914,12 @@ __global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __g
           soff += cc < W.nwin ? W.cap[cc] : 0;
         }
       }
-      const int km1 = (int)S.k - 1;
+      const unsigned vm = S.valid_mask(c, DIM);
       double acc = 0.0;
 #pragma unroll
       for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
         if (NP == 0 && p >= npts) break;
-        bool ok = true;
-#pragma unroll
-        for (int a = 3 - DIM; a < 3; ++a) {
-          const int cc = c[a] + S.off[p][a];
-          ok = ok && cc >= 0 && cc <= km1;
-        }
-        if (ok) {
+        if ((vm >> p) & 1u) {
           const int col = (int)(i + S.foff[p]);
           acc = add(acc, mul(S.coef[p], xw[col - wsb[SW.pw[p]]]));
         }
@@ -980,14 +1020,14 @@ __global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel
   for (long long i = S.row_lo + (long long)blockIdx.x * kThreads + threadIdx.x; i < S.row_hi; i += stride) {
     int c[3] = {0, 0, 0};
     if (DIM == 3) {
-      const long long z = i / S.k2;
+      const long long z = S.dk2.div(i);
       const long long rem = i - z * S.k2;
-      const long long yy = rem / S.k;
+      const long long yy = S.dk.div(rem);
       c[0] = (int)z;
       c[1] = (int)yy;
       c[2] = (int)(rem - yy * S.k);
     } else if (DIM == 2) {
-      const long long yy = i / S.k;
+      const long long yy = S.dk.div(i);
       c[1] = (int)yy;
       c[2] = (int)(i - yy * S.k);
     } else {
@@ -996,19 +1036,13 @@ __global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel
     double inr[Epi::kIn > 0 ? Epi::kIn : 1];
 #pragma unroll
     for (int k = 0; k < Epi::kIn; ++k) inr[k] = epi.in[k][i];
-    const int km1 = (int)S.k - 1;
     const int npts = NP > 0 ? NP : S.npts;
+    const unsigned vm = S.valid_mask(c, DIM);
     double acc = 0.0;
 #pragma unroll
     for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
       if (NP == 0 && p >= npts) break;
-      bool ok = true;
-#pragma unroll
-      for (int a = 3 - DIM; a < 3; ++a) {
-        const int cc = c[a] + S.off[p][a];
-        ok = ok && cc >= 0 && cc <= km1;
-      }
-      if (ok) acc = add(acc, mul(S.coef[p], __ldg(x + i + S.foff[p])));
+      if ((vm >> p) & 1u) acc = add(acc, mul(S.coef[p], __ldg(x + i + S.foff[p])));
     }
     e.row(i, acc, inr);
   }
