@@ -21,7 +21,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 STATUS = {0: "converged", 1: "max_iters", 2: "breakdown", 3: "non_finite"}
-METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2}
+METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4}
 # coefficients.py:77, 80, 83, 102, 105
 BREAKDOWN_QUANTITIES = {
     1: "initial alpha denominator (r0*, s)",
@@ -29,9 +29,20 @@ BREAKDOWN_QUANTITIES = {
     3: "alpha denominator g + beta*h",
     4: "zeta denominator (s, s)",
     5: "zeta/eta denominator a*b - c^2",
+    # solvers.py:275, 283, 302, 303 (BiCGStab), 434 (GPBi-CG); coefficients.py:130, 134
+    6: "alpha denominator (r0*, Ap)",
+    7: "omega denominator (At, At)",
+    8: "beta denominator omega",
+    9: "beta denominator (r0*, r)",
+    10: "zeta denominator (At, At)",
+    11: "zeta/eta denominator e*a - d^2",
+    12: "beta denominator zeta",
 }
-SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay"}
+SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap"}
 TRACE_NAMES = ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l", "r0s")
+# trace_hook dicts of the product-type methods (solvers.py:315, 448)
+TRACE_NAMES_BY_METHOD = {"bicgstab": ("x", "r", "p", "t", "Ap", "At"),
+                         "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z")}
 
 
 class _Config(C.Structure):
@@ -80,6 +91,7 @@ def lib():
         L.or_plan_dot.restype = d
         L.or_alpha_beta_safe.argtypes = [d, d, d, d, d, d, C.c_int, p]
         L.or_zeta_eta_safe.argtypes = [d, d, d, d, d, C.c_int, p]
+        L.or_zeta_eta_gpbicg.argtypes = [d, d, d, d, d, C.c_int, p]
         L.or_solve.argtypes = [i64, p, p, p, p, p, C.POINTER(_Config), p, p, p, p, p,
                                C.POINTER(_Result), _TRACE_FN, p]
         L.or_solve.restype = C.c_int
@@ -169,7 +181,13 @@ def zeta_eta_safe(a, b, c, d, e, first):
     return q, float(out[0]), float(out[1])
 
 
-# -- solver (solvers.py:485-592, 595-779) ------------------------------------
+def zeta_eta_gpbicg(a, b, c, d, e, first):
+    out = np.zeros(2)
+    q = lib().or_zeta_eta_gpbicg(a, b, c, d, e, int(first), _ptr(out))
+    return q, float(out[0]), float(out[1])
+
+
+# -- solver (solvers.py:210-460, 485-592, 595-779) ------------------------------------
 
 def solve(row_ptr, col_idx, values, b, x0=None, method="pbicgsafe", tol=1e-8, max_iters=10_000,
           rr_epoch=100, rr_cutoff=None, workers=1, threads=0, trace=None):
@@ -177,7 +195,9 @@ def solve(row_ptr, col_idx, values, b, x0=None, method="pbicgsafe", tol=1e-8, ma
 
     ``trace(i, vecs: dict[name -> array copy], scalars: array)`` is called
     after every completed iteration like the reference's trace_hook
-    (solvers.py:725-732); scalars = alpha, beta, zeta, eta, f_prev, 9 dots.
+    (solvers.py:725-732); scalars = alpha, beta, zeta, eta, f_prev, 9 dots
+    (bicgstab / gpbicg: alpha, beta, omega|zeta, eta, f, rr).  The
+    coefficient record of bicgstab carries omega in the zeta column.
     """
     rp, ci, v, bb = _i64(row_ptr), _i64(col_idx), _f64(values), _f64(b)
     n = rp.shape[0] - 1
@@ -194,7 +214,7 @@ def solve(row_ptr, col_idx, values, b, x0=None, method="pbicgsafe", tol=1e-8, ma
     if trace is not None:
         def _cb(i, vecs, scalars, _user):
             d = {name: np.ctypeslib.as_array(vecs[k], shape=(n,)).copy()
-                 for k, name in enumerate(TRACE_NAMES)}
+                 for k, name in enumerate(TRACE_NAMES_BY_METHOD.get(method, TRACE_NAMES))}
             trace(int(i), d, np.ctypeslib.as_array(scalars, shape=(14,)).copy())
         cb = _TRACE_FN(_cb)
     else:

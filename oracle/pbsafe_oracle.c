@@ -17,7 +17,10 @@
  *     coefficients.py:35-106;
  *   - the solver loops _solve_pipelined (solvers.py:595-739, p-BiCGSafe and
  *     p-BiCGSafe-rr) and solve_ssbicgsafe2 (solvers.py:485-592), including
- *     the _Run bookkeeping (solvers.py:154-197) and the termination order.
+ *     the _Run bookkeeping (solvers.py:154-197) and the termination order;
+ *   - the product-type comparators solve_bicgstab (solvers.py:210-327) and
+ *     solve_gpbicg (solvers.py:330-460) with compute_zeta_eta_gpbicg
+ *     (coefficients.py:109-135).
  *
  * Threads: rows of SpMV / vector updates are split across OpenMP threads
  * (element-wise, so bitwise neutral); the dot batch runs one thread per plan
@@ -214,7 +217,15 @@ enum {
   Q_BETA = 2,          /* "beta denominator zeta_prev * f_prev" */
   Q_ALPHA = 3,         /* "alpha denominator g + beta*h" */
   Q_ZETA = 4,          /* "zeta denominator (s, s)" */
-  Q_ZETA_ETA = 5       /* "zeta/eta denominator a*b - c^2" */
+  Q_ZETA_ETA = 5,      /* "zeta/eta denominator a*b - c^2" */
+  /* the product-type comparators (solvers.py:270-309, 390-450; coefficients.py:130-135) */
+  Q_STAB_ALPHA = 6,    /* "alpha denominator (r0*, Ap)" */
+  Q_STAB_OMEGA = 7,    /* "omega denominator (At, At)" */
+  Q_STAB_BETA_OMEGA = 8, /* "beta denominator omega" */
+  Q_BETA_F = 9,        /* "beta denominator (r0*, r)" */
+  Q_GP_ZETA = 10,      /* "zeta denominator (At, At)" */
+  Q_GP_ZETA_ETA = 11,  /* "zeta/eta denominator e*a - d^2" */
+  Q_GP_BETA_ZETA = 12  /* "beta denominator zeta" */
 };
 
 /* coefficients.py:35-39 guard_denominator: returns nonzero on breakdown */
@@ -265,13 +276,39 @@ OR_API int or_zeta_eta_safe(double a, double b, double c, double d, double e, in
   return zeta_eta_safe(a, b, c, d, e, first, &out2[0], &out2[1]);
 }
 
+/* coefficients.py:109-135 compute_zeta_eta_gpbicg */
+static int zeta_eta_gpbicg(double a, double b, double c, double d, double e, int first,
+                           double* zeta, double* eta) {
+  if (first || (a == 0.0 && c == 0.0 && d == 0.0)) {
+    if (e == 0.0) {
+      *zeta = 0.0;
+      *eta = 0.0;
+      return Q_NONE;
+    }
+    if (guard(e, fabs(e))) return Q_GP_ZETA;
+    *zeta = b / e;
+    *eta = 0.0;
+    return Q_NONE;
+  }
+  double det = e * a - d * d;
+  if (guard(det, fabs(e * a) + d * d)) return Q_GP_ZETA_ETA;
+  *zeta = (a * b - c * d) / det;
+  *eta = (e * c - d * b) / det;
+  return Q_NONE;
+}
+
+OR_API int or_zeta_eta_gpbicg(double a, double b, double c, double d, double e, int first,
+                              double* out2) {
+  return zeta_eta_gpbicg(a, b, c, d, e, first, &out2[0], &out2[1]);
+}
+
 /* ------------------------------------------------------------------ solver */
 
 enum { ST_CONVERGED = 0, ST_MAX_ITERS = 1, ST_BREAKDOWN = 2, ST_NON_FINITE = 3 };
-enum { M_PBICGSAFE = 0, M_PBICGSAFE_RR = 1, M_SSBICGSAFE2 = 2 };
+enum { M_PBICGSAFE = 0, M_PBICGSAFE_RR = 1, M_SSBICGSAFE2 = 2, M_BICGSTAB = 3, M_GPBICG = 4 };
 
 /* SpMV tags for the NonFiniteVectorError message (reduction.py:330, 451) */
-enum { T_NONE = 0, T_AX = 1, T_AR = 2, T_AS = 3, T_AW = 4, T_AO = 5, T_AU = 6, T_AT = 7, T_AY = 8 };
+enum { T_NONE = 0, T_AX = 1, T_AR = 2, T_AS = 3, T_AW = 4, T_AO = 5, T_AU = 6, T_AT = 7, T_AY = 8, T_AP = 9 };
 
 typedef struct {
   double tol;
@@ -363,6 +400,154 @@ static void safe_batch(const or_plan* P, const double* s, const double* y, const
   plan_batch(P, 9, xs, ys, d9);
 }
 
+/* The two product-type comparators with their reduction phases:
+ *   BiCGStab  solvers.py:210-327 (2 phases: g after A p; b e c d after A t)
+ *   GPBi-CG   solvers.py:330-460 (3 phases: g; a b c d e after A t; f r)
+ * The coefficient record holds alpha beta zeta eta, with BiCGStab's omega
+ * in the zeta slot.  trace vecs: x r p t Ap At (BiCGStab) or
+ * x r p u t w y z (GPBi-CG); scalars alpha beta omega|zeta eta f rr. */
+static int solve_product(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                         const double* b, const double* x0, const or_config* cfg, double* x_out,
+                         double* hist_rel, uint8_t* hist_replaced, double* hist_coef,
+                         uint8_t* hist_has_coef, or_result* res, or_trace_fn trace, void* user) {
+  mat_t A = {n, rp, ci, v, res};
+  or_plan P;
+  int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;
+  P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(wk + 2));
+  P.workers = or_plan_balanced(n, wk, P.bounds);
+  P.compensated = cfg->workers < 0;
+  hist_t H = {hist_rel, hist_replaced, hist_coef, hist_has_coef, 0};
+  const int gp = cfg->method == M_GPBICG;
+  double* buf = (double*)calloc((size_t)12 * (size_t)(n > 0 ? n : 1), sizeof(double));
+  int idx = 0;
+  VEC(x); VEC(r); VEC(r0s); VEC(p); VEC(u); VEC(t); VEC(w); VEC(y); VEC(z);
+  VEC(ap); VEC(at); VEC(tmp);
+  if (x0) memcpy(x, x0, sizeof(double) * (size_t)n);
+  int rc = 0;
+  int64_t iterations = 0;
+  double r0_norm = 0.0;
+  /* r0 = b - A x0 ; r0s = r0 ; rr = (r, r) ; f = rr (solvers.py:238-248, 359-369) */
+  if (spmv_checked(&A, x, tmp, T_AX)) { rc = 1; goto done; }
+  or_lincomb2(n, r, 1.0, b, -1.0, tmp);
+  memcpy(r0s, r, sizeof(double) * (size_t)n);
+  double rr = plan_dot(&P, r, r);
+  double f = rr;
+  r0_norm = sqrt(rr);
+  double alpha = 0.0, beta = 0.0, omega = 0.0, zeta = 0.0, eta = 0.0;
+  for (int64_t i = 0; i < cfg->max_iters; ++i) {
+    double rel = rel_of(r0_norm, rr);
+    record(&H, i, rel, 0);
+    if (!isfinite(rel)) { res->status = ST_NON_FINITE; res->failure_iter = i; iterations = i; goto finish; }
+    if (rel <= cfg->tol) { res->status = ST_CONVERGED; iterations = i; goto finish; }
+    int q = Q_NONE;
+    if (gp)
+      or_add_scaled_diff(n, p, r, beta, p, u);               /* p = r + beta*(p - u) */
+    else
+      or_add_scaled_damped_diff(n, p, r, beta, p, omega, ap); /* p = r + beta*(p - omega*Ap) */
+    if (spmv_checked(&A, p, ap, T_AP)) { rc = 1; goto done; }
+    double gdot = plan_dot(&P, r0s, ap);
+    if (guard(gdot, fabs(gdot))) { q = Q_STAB_ALPHA; goto broke; }
+    alpha = f / gdot;
+    if (gp) {
+      or_lincomb4(n, y, 1.0, t, -1.0, r, -alpha, w, alpha, ap); /* y = t - r - alpha w + alpha Ap */
+      or_lincomb3(n, u, 1.0, t, -1.0, r, beta, u);              /* u = t - r + beta u (stash) */
+    }
+    or_lincomb2(n, t, 1.0, r, -alpha, ap);                      /* t = r - alpha*Ap */
+    if (spmv_checked(&A, t, at, T_AT)) { rc = 1; goto done; }
+    if (!gp) {
+      const double* xs[4] = {at, at, r0s, t};
+      const double* ys[4] = {t, at, at, t};
+      double d4[4]; /* b e c d */
+      plan_batch(&P, 4, xs, ys, d4);
+      if (d4[1] == 0.0 && d4[3] == 0.0) {
+        omega = 0.0;
+      } else {
+        if (guard(d4[1], fabs(d4[1]))) { q = Q_STAB_OMEGA; goto broke; }
+        omega = d4[0] / d4[1];
+      }
+      or_lincomb3(n, x, 1.0, x, alpha, p, omega, t); /* x = x + alpha*p + omega*t */
+      or_lincomb2(n, r, 1.0, t, -omega, at);         /* r = t - omega*At */
+      double f_next = (f - alpha * gdot) - omega * d4[2];
+      double v2 = d4[3] - 2.0 * omega * d4[0] + omega * omega * d4[1];
+      rr = (0.0 > v2) ? 0.0 : v2; /* Python max(v, 0.0) */
+      if (rr == 0.0) {
+        beta = 0.0;
+      } else {
+        if (guard(omega, fabs(omega))) { q = Q_STAB_BETA_OMEGA; goto broke; }
+        if (guard(f, fabs(f))) { q = Q_BETA_F; goto broke; }
+        beta = (alpha / omega) * (f_next / f);
+      }
+      f = f_next;
+      set_coef(&H, alpha, beta, omega, NAN);
+      if (!(isfinite(alpha) && isfinite(beta) && isfinite(omega))) {
+        res->status = ST_NON_FINITE; res->failure_iter = i; iterations = i; goto finish;
+      }
+      if (trace) {
+        double* vecs[6] = {x, r, p, t, ap, at};
+        double sc[14] = {alpha, beta, omega, 0.0, f, rr};
+        trace(i, vecs, sc, user);
+      }
+    } else {
+      const double* xs[5] = {y, at, y, at, at};
+      const double* ys[5] = {y, t, t, y, at};
+      double d5[5]; /* a b c d e */
+      plan_batch(&P, 5, xs, ys, d5);
+      q = zeta_eta_gpbicg(d5[0], d5[1], d5[2], d5[3], d5[4], i == 0, &zeta, &eta);
+      if (q) goto broke;
+      or_lincomb2(n, u, zeta, ap, eta, u);             /* u = zeta*Ap + eta*(stash) */
+      or_lincomb3(n, z, zeta, r, eta, z, -alpha, u);   /* z = zeta*r + eta*z - alpha*u */
+      or_lincomb3(n, x, 1.0, x, alpha, p, 1.0, z);     /* x = x + alpha*p + z */
+      or_lincomb3(n, r, 1.0, t, -eta, y, -zeta, at);   /* r = t - eta*y - zeta*At */
+      const double* xs3[2] = {r0s, r};
+      const double* ys3[2] = {r, r};
+      double d2[2]; /* f r */
+      plan_batch(&P, 2, xs3, ys3, d2);
+      rr = d2[1];
+      if (rr == 0.0) {
+        beta = 0.0;
+      } else {
+        if (guard(zeta, fabs(zeta))) { q = Q_GP_BETA_ZETA; goto broke; }
+        if (guard(f, fabs(f))) { q = Q_BETA_F; goto broke; }
+        beta = (alpha / zeta) * (d2[0] / f);
+      }
+      f = d2[0];
+      or_lincomb2(n, w, 1.0, at, beta, ap);            /* w = At + beta*Ap */
+      set_coef(&H, alpha, beta, zeta, eta);
+      if (!(isfinite(alpha) && isfinite(beta) && isfinite(zeta) && isfinite(eta))) {
+        res->status = ST_NON_FINITE; res->failure_iter = i; iterations = i; goto finish;
+      }
+      if (trace) {
+        double* vecs[8] = {x, r, p, u, t, w, y, z};
+        double sc[14] = {alpha, beta, zeta, eta, f, rr};
+        trace(i, vecs, sc, user);
+      }
+    }
+    iterations = i + 1;
+    continue;
+  broke:
+    res->status = ST_BREAKDOWN;
+    res->breakdown = q;
+    res->failure_iter = i;
+    iterations = i;
+    goto finish;
+  }
+  {
+    double rel = rel_of(r0_norm, rr); /* solvers.py:324-327, 457-460 */
+    record(&H, cfg->max_iters, rel, 0);
+    res->status = rel <= cfg->tol ? ST_CONVERGED : ST_MAX_ITERS;
+    iterations = cfg->max_iters;
+  }
+finish:
+  res->iterations = iterations;
+  res->r0_norm = r0_norm;
+  res->n_records = H.count;
+  memcpy(x_out, x, sizeof(double) * (size_t)n);
+done:
+  free(buf);
+  free(P.bounds);
+  return rc;
+}
+
 /* solvers.py:595-739 (_solve_pipelined) and solvers.py:485-592 (ssBiCGSafe2).
  * Returns 0, or 1 when a NonFiniteVectorError would have been raised. */
 OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
@@ -375,6 +560,9 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   memset(res, 0, sizeof(*res));
   res->failure_iter = -1;
   res->nonfinite_index = -1;
+  if (cfg->method == M_BICGSTAB || cfg->method == M_GPBICG)
+    return solve_product(n, rp, ci, v, b, x0, cfg, x_out, hist_rel, hist_replaced, hist_coef,
+                         hist_has_coef, res, trace, user);
   mat_t A = {n, rp, ci, v, res};
   or_plan P;
   int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;

@@ -41,6 +41,7 @@ from pipesafe import kernels as kn  # noqa: E402
 from pipesafe.coefficients import (  # noqa: E402
     BreakdownError,
     compute_alpha_beta_safe,
+    compute_zeta_eta_gpbicg,
     compute_zeta_eta_safe,
 )
 from pipesafe.linalg import NonFiniteVectorError, csr_from_coo, gen_poisson, spmv  # noqa: E402
@@ -140,7 +141,8 @@ def run_case(spec, trace=False):
     for j, rec in enumerate(hist):
         if rec.coefficients is not None:
             c = rec.coefficients
-            coef[j] = (c.alpha, c.beta, c.zeta, c.eta)
+            # BiCGStab's CoefficientSet carries omega, stored in the zeta column
+            coef[j] = (c.alpha, c.beta, c.omega if c.omega is not None else c.zeta, c.eta)
             has[j] = True
     payload = dict(
         csr_sha=np.array(csr_sha(A.row_ptr, A.col_idx, A.values)),
@@ -296,20 +298,64 @@ def coeffs_fixture():
                 ze_in=np.array(ze_in, dtype=np.float64), ze_out=np.array(ze_out))
 
 
+def coeffs_gpbicg_fixture():
+    """compute_zeta_eta_gpbicg (coefficients.py:109-135): the reference's own
+    hand values (test_coefficients.py:53-63, 135-138, 187-194) plus seeded
+    random normal-equation inputs."""
+    rng = np.random.default_rng(4243)
+    names = {"zeta denominator (At, At)": 10, "zeta/eta denominator e*a - d^2": 11}
+    special = [
+        (0.0, 3.0, 0.0, 0.0, 6.0, 1),
+        (1.0, 4.0, 1.0, 0.0, 2.0, 0),
+        (0.0, 3.0, 0.0, 0.0, 6.0, 0),
+        (0.0, 0.0, 0.0, 0.0, 0.0, 1),
+        (0.0, 1.0, 0.0, 0.0, 0.0, 0),
+        (0.0, 1.0, 0.0, 0.0, 1e-320, 1),
+        (1.0, 1.0, 1.0, 1.0, 1.0, 0),
+        (4.0, 1.0, 2.0, 2.0, 1.0, 0),
+        (np.nan, 1.0, 1.0, 1.0, 1.0, 0),
+    ]
+    rnd = []
+    for _ in range(500):
+        y, t, at = rng.standard_normal((3, 6))
+        rnd.append((y @ y, at @ t, y @ t, at @ y, at @ at, int(rng.random() < 0.1)))
+    gz_in, gz_out = [], []
+    for a, b, c, d, e, first in special + rnd:
+        try:
+            z, et = compute_zeta_eta_gpbicg(a, b, c, d, e, bool(first))
+            q = 0
+        except BreakdownError as ex:
+            z, et, q = np.nan, np.nan, names[ex.quantity]
+        gz_in.append((a, b, c, d, e, first))
+        gz_out.append((q, z, et))
+    return dict(gz_in=np.array(gz_in, dtype=np.float64), gz_out=np.array(gz_out))
+
+
 def main():
-    np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_fixture())
-    np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans_fixture())
-    np.savez_compressed(os.path.join(HERE, "coeffs.npz"), **coeffs_fixture())
+    # --only PREFIX regenerates just the solve/trace cases whose name starts with it
+    only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
+    if only is None or only == "gp_":
+        np.savez_compressed(os.path.join(HERE, "coeffs_gpbicg.npz"), **coeffs_gpbicg_fixture())
+    if only is None:
+        np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_fixture())
+        np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans_fixture())
+        np.savez_compressed(os.path.join(HERE, "coeffs.npz"), **coeffs_fixture())
     for name, spec in CASES.items():
+        if only is not None and not name.startswith(only):
+            continue
         payload = run_case(spec)
         if payload["n"] > 5000:
             del payload["b"]  # rebuilt from the generator + pinned by csr_sha
         np.savez_compressed(os.path.join(HERE, f"solve_{name}.npz"), **payload)
         print(name, str(payload["status"]), int(payload["iterations"]))
     for name, spec in TRACE_CASES.items():
+        if only is not None and not name.startswith(only):
+            continue
         payload = run_case(spec, trace=True)
         np.savez_compressed(os.path.join(HERE, f"trace_{name}.npz"), **payload)
         print("trace", name, str(payload["status"]), int(payload["iterations"]))
+    if only is not None:
+        return
     # non-finite matrix raises (test_solvers.py:226-230)
     A = csr_from_coo(2, 2, np.array([0, 1]), np.array([0, 1]), np.array([1.0, 1.0]))
     A.values[0] = np.nan

@@ -20,7 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="c2")
     ap.add_argument("--iters", type=int, default=40)
-    ap.add_argument("--operator", default="csr", choices=("csr", "stencil"))
+    ap.add_argument("--operator", default="csr", choices=("csr", "stencil", "devcsr"))
     ap.add_argument("--method", default="pbicgsafe")
     ap.add_argument("--graphs", action="store_true")
     ap.add_argument("--repeat", type=int, default=1)
@@ -43,6 +43,10 @@ def main():
         st = problems.config_stencil(args.config)
         rp, ci, v = problems.stencil_csr(st, col_dtype=np.int32)
         dm = DeviceMatrix.from_csr((rp, ci, v))
+    elif args.operator == "devcsr":  # CSR built on the device (config 4's 1.5e9 nonzeros)
+        sm = DeviceMatrix.from_stencil(problems.config_stencil(args.config))
+        dm = sm.to_csr()
+        sm.free()
     else:
         dm = DeviceMatrix.from_stencil(problems.config_stencil(args.config))
     n = dm.n_rows
