@@ -12,8 +12,10 @@
  * Reference interfaces each group replaces (paths under
  * /root/reference/pkg/src/pipesafe/):
  *   pbs_solve / pbs_solve_dev  — solve(), solve_pbicgsafe(),
- *                                solve_pbicgsafe_rr(), solve_ssbicgsafe2()
- *                                (solvers.py:791-803, 742-779, 485-592), with
+ *                                solve_pbicgsafe_rr(), solve_ssbicgsafe2(),
+ *                                solve_bicgstab(), solve_gpbicg()
+ *                                (solvers.py:791-803, 742-779, 485-592,
+ *                                210-327, 330-460), with
  *                                SolverConfig fields (solvers.py:51-78) in
  *                                pbs_config and SolveOutcome / IterationRecord
  *                                (solvers.py:81-114) in pbs_result + history
@@ -55,6 +57,8 @@ extern "C" {
 #define PBS_METHOD_PBICGSAFE 0
 #define PBS_METHOD_PBICGSAFE_RR 1
 #define PBS_METHOD_SSBICGSAFE2 2
+#define PBS_METHOD_BICGSTAB 3  /* two reduction phases (solvers.py:210-327) */
+#define PBS_METHOD_GPBICG 4    /* three reduction phases (solvers.py:330-460) */
 
 /* SolveStatus (solvers.py:44-48) */
 #define PBS_CONVERGED 0
@@ -69,6 +73,14 @@ extern "C" {
 #define PBS_BD_ALPHA 3         /* "alpha denominator g + beta*h" */
 #define PBS_BD_ZETA 4          /* "zeta denominator (s, s)" */
 #define PBS_BD_ZETA_ETA 5      /* "zeta/eta denominator a*b - c^2" */
+/* product-type comparators (solvers.py:275, 283, 302-303, 434; coefficients.py:130, 134) */
+#define PBS_BD_PROD_ALPHA 6    /* "alpha denominator (r0*, Ap)" */
+#define PBS_BD_STAB_OMEGA 7    /* "omega denominator (At, At)" */
+#define PBS_BD_STAB_BETA 8     /* "beta denominator omega" */
+#define PBS_BD_BETA_F 9        /* "beta denominator (r0*, r)" */
+#define PBS_BD_GP_ZETA 10      /* "zeta denominator (At, At)" */
+#define PBS_BD_GP_ZETA_ETA 11  /* "zeta/eta denominator e*a - d^2" */
+#define PBS_BD_GP_BETA 12      /* "beta denominator zeta" */
 
 /* SpMV tags of NonFiniteVectorError messages (reduction.py:330, 451) */
 #define PBS_TAG_AX 1
@@ -79,6 +91,7 @@ extern "C" {
 #define PBS_TAG_AU 6
 #define PBS_TAG_AT 7
 #define PBS_TAG_AY 8
+#define PBS_TAG_AP 9
 
 /* reduction orders for the per-iteration dot batch */
 #define PBS_REDUCE_TREE 0 /* fixed-shape block tree: deterministic, full speed */
@@ -94,7 +107,9 @@ typedef struct pbs_ctx pbs_ctx;
 typedef struct pbs_mat pbs_mat;
 
 /* trace_hook (solvers.py:725-732): called after each completed iteration with
- * 13 host arrays x r p u o t w y z s q g l (valid for the call only).
+ * host arrays (valid for the call only): 13 for the Safe methods,
+ * x r p u o t w y z s q g l; BiCGStab 6, x r p t Ap At (solvers.py:315);
+ * GPBi-CG 8, x r p u t w y z (solvers.py:448).
  * Tracing syncs the device every iteration; it is a parity/debug mode. */
 typedef void (*pbs_trace_fn)(int64_t iter, double* const* host_vecs, void* user);
 
@@ -135,6 +150,11 @@ typedef struct {
   int64_t nonfinite_index;  /* first non-finite row of that SpMV output */
   int64_t n_spmv;           /* SpMVs executed (reference counting) */
   int64_t n_replacements;   /* residual-replacement iterations executed */
+  int32_t stop_stage;       /* product-type methods: where the stopping
+                               iteration ended (0 loop-top check, 1 after the
+                               alpha step, 2 omega/zeta, 3 after the x/r
+                               update, 4 complete) */
+  int32_t pad2;
   double device_ms;         /* CUDA-event time from setup to the last check */
   int64_t kernel_launches;  /* kernels launched by this solve */
   double kernel_ms[PBS_NUM_KERNEL_KINDS];    /* timing mode: summed durations */

@@ -21,14 +21,14 @@ PBS_ERR_NOMEM = -4
 PBS_ERR_NCCL = -5
 PBS_ERR_UNSUPPORTED = -6
 
-METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2}
+METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4}
 REDUCE_TREE, REDUCE_PLAN = 0, 1
 HIST_REPLACED, HIST_HAS_COEF = 1, 2
 NUM_KERNEL_KINDS = 8
 KERNEL_KINDS = ("K1_As", "K2_update", "K3_Aw_epilogue", "F_finalize", "R_rr_update",
                 "RS_rr_spmv", "S_setup", "D_plan_dots")
 # reduction.py:330/451 tags of the NonFiniteVectorError message
-SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay"}
+SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap"}
 
 EXPORTS = (
     "pbs_init", "pbs_destroy", "pbs_last_error", "pbs_device_info", "pbs_set_stream",
@@ -67,7 +67,8 @@ class Result(C.Structure):
         ("status", C.c_int32), ("breakdown", C.c_int32), ("iterations", C.c_int64),
         ("failure_iter", C.c_int64), ("n_records", C.c_int64), ("r0_norm", C.c_double),
         ("nonfinite_tag", C.c_int32), ("pad", C.c_int32), ("nonfinite_index", C.c_int64),
-        ("n_spmv", C.c_int64), ("n_replacements", C.c_int64), ("device_ms", C.c_double),
+        ("n_spmv", C.c_int64), ("n_replacements", C.c_int64), ("stop_stage", C.c_int32),
+        ("pad2", C.c_int32), ("device_ms", C.c_double),
         ("kernel_launches", C.c_int64), ("kernel_ms", C.c_double * NUM_KERNEL_KINDS),
         ("kernel_count", C.c_int64 * NUM_KERNEL_KINDS),
     ]

@@ -22,6 +22,14 @@ BREAKDOWN_QUANTITIES = {
     3: "alpha denominator g + beta*h",
     4: "zeta denominator (s, s)",
     5: "zeta/eta denominator a*b - c^2",
+    # the product-type comparators (solvers.py:275, 283, 302, 303, 434; coefficients.py:130, 134)
+    6: "alpha denominator (r0*, Ap)",
+    7: "omega denominator (At, At)",
+    8: "beta denominator omega",
+    9: "beta denominator (r0*, r)",
+    10: "zeta denominator (At, At)",
+    11: "zeta/eta denominator e*a - d^2",
+    12: "beta denominator zeta",
 }
 
 

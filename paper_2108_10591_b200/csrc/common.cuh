@@ -34,6 +34,14 @@ enum Dot { DA = 0, DB, DC, DD, DE, DF, DG, DH, DR };
 constexpr unsigned kAllDots = (1u << kNumDots) - 1;
 constexpr unsigned kDotsK12 = (1u << DB) | (1u << DE) | (1u << DF) | (1u << DH) | (1u << DR);
 constexpr unsigned kDotsK3 = kAllDots & ~kDotsK12;
+// the product-type comparators' reduction phases (solvers.py:210-460), in the
+// same slots: g = (r0*, Ap); BiCGStab b=(At,t) e=(At,At) c=(r0*,At) d=(t,t);
+// GPBi-CG a=(y,y) b=(At,t) c=(y,t) d=(At,y) e=(At,At), then f=(r0*,r) r=(r,r)
+constexpr unsigned kDotsProdA = 1u << DG;
+constexpr unsigned kDotsStabB = (1u << DB) | (1u << DE) | (1u << DC) | (1u << DD);
+constexpr unsigned kDotsGpB = (1u << DA) | (1u << DB) | (1u << DC) | (1u << DD) | (1u << DE);
+constexpr unsigned kDotsGpC = (1u << DF) | (1u << DR);
+constexpr unsigned kDotsRR = 1u << DR;
 
 // Host-visible mirror, written by the finalize kernel through mapped pinned
 // memory so the host can stop launching without a device sync.
@@ -57,12 +65,18 @@ struct SolverState {
   double f_prev;
   double r0_norm;
   double dots[kNumDots];
+  double omega;  // BiCGStab's step (its coefficient record keeps it in the zeta slot)
+  double rr;     // product-type methods: the residual norm^2 of the next check
   // control
   long long iter;       // index of the next check the finalize kernel performs
   int run_all;          // 0 once a check stopped the solve
   int run_spine;        // the spine SpMV (As / Ar) still runs for the stop iteration
   int status;           // -1 running, else PBS_CONVERGED...
   int breakdown;
+  int upd;              // BiCGStab: this iteration's x/r update may run (omega passed)
+  int stop_stage;       // product-type methods: where the stopping iteration ended
+                        // (0 its loop-top check, 1 alpha, 2 omega/zeta, 3 after
+                        // the x/r update, 4 complete) -> the reference's tallies
   long long failure_iter;
   long long iterations;
   long long n_records;

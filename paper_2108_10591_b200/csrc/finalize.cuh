@@ -195,6 +195,206 @@ __device__ __forceinline__ void check_and_publish(SolverState* st, SolverState* 
   }
 }
 
+// ---- the product-type comparators: BiCGStab (solvers.py:210-327) and
+// GPBi-CG (solvers.py:330-460).  Their coefficient steps are split across
+// the iteration's reduction phases; each phase runs in the tail of the kernel
+// that produced its dots (or a 1-CTA finalize in plan order):
+//   setup      (r, r)                 -> r0_norm, f, check 0          (solvers.py:244-266)
+//   alpha      g = (r0*, Ap)          -> alpha                        (269-276, 385-392)
+//   stab omega b e c d after A t      -> omega, x/r go-ahead, f, rr,  (283-317)
+//                                        beta, record, check i+1
+//   gp zeta    a b c d e after A t    -> zeta, eta                    (401-413)
+//   gp beta    f, r after x/r update  -> beta, f, record, check i+1   (421-450)
+// ("no check" variants leave check i+1 to kPhProdCheck so a trace hook can
+// run between them, as in the reference.)
+enum Phase {
+  kPhSafe = 0,
+  kPhProdSetup,
+  kPhProdAlpha,
+  kPhStabOmega,
+  kPhStabOmegaNC,
+  kPhGpZeta,
+  kPhGpBeta,
+  kPhGpBetaNC,
+  kPhProdCheck,
+};
+
+__device__ __forceinline__ void prod_stop(SolverState* ss, int status, long long iters, long long fail, int stage) {
+  ss->status = status;
+  ss->iterations = iters;
+  if (fail >= 0) ss->failure_iter = fail;
+  ss->run_all = 0;
+  ss->run_spine = 0;
+  ss->stop_stage = stage;
+}
+
+__device__ __forceinline__ double prod_rel(const SolverState* ss, double rr) {  // _Run.rel_of
+  if (ss->r0_norm == 0.0) return 0.0;
+  return sqrt((0.0 > rr) ? 0.0 : rr) / ss->r0_norm;
+}
+
+// the loop-top record and tests of check j (solvers.py:258-263, 324-327)
+__device__ void prod_check(SolverState* ss, long long j) {
+  const double rel = prod_rel(ss, ss->rr);
+  if (ss->record_history) {
+    const long long slot = ss->n_records;
+    ss->hist_rel[slot] = rel;
+    ss->hist_flags[slot] = 0;
+    ss->n_records = slot + 1;
+  }
+  ss->iter = j + 1;
+  if (j == ss->max_iters) return prod_stop(ss, rel <= ss->tol ? PBS_CONVERGED : PBS_MAX_ITERS, j, -1, 0);
+  if (!isfinite(rel)) return prod_stop(ss, PBS_NON_FINITE, j, j, 0);
+  if (rel <= ss->tol) return prod_stop(ss, PBS_CONVERGED, j, -1, 0);
+}
+
+// rec.coefficients of iteration i, then the non-finite test (solvers.py:310-313, 443-446)
+__device__ bool prod_record_coef(SolverState* ss, long long i, double a, double b, double z, double e,
+                                 bool has_eta) {
+  if (ss->record_history) {
+    const long long slot = ss->n_records - 1;
+    ss->hist_coef[4 * slot + 0] = a;
+    ss->hist_coef[4 * slot + 1] = b;
+    ss->hist_coef[4 * slot + 2] = z;
+    ss->hist_coef[4 * slot + 3] = e;
+    ss->hist_flags[slot] |= PBS_HIST_HAS_COEF;
+  }
+  if (isfinite(a) && isfinite(b) && isfinite(z) && (!has_eta || isfinite(e))) return true;
+  prod_stop(ss, PBS_NON_FINITE, i, i, 4);
+  return false;
+}
+
+// compute_zeta_eta_gpbicg (coefficients.py:109-135); returns a PBS_BD_* or 0
+__device__ int zeta_eta_gpbicg(double a, double b, double c, double d, double e, bool first, double* zeta,
+                               double* eta) {
+  if (first || (a == 0.0 && c == 0.0 && d == 0.0)) {
+    if (e == 0.0) {
+      *zeta = 0.0;
+      *eta = 0.0;
+      return PBS_BD_NONE;
+    }
+    if (guard(e, fabs(e))) return PBS_BD_GP_ZETA;
+    *zeta = b / e;
+    *eta = 0.0;
+    return PBS_BD_NONE;
+  }
+  const double ea = mul(e, a), dd = mul(d, d);
+  const double det = sub(ea, dd);
+  if (guard(det, add(fabs(ea), dd))) return PBS_BD_GP_ZETA_ETA;
+  *zeta = sub(mul(a, b), mul(c, d)) / det;
+  *eta = sub(mul(e, c), mul(d, b)) / det;
+  return PBS_BD_NONE;
+}
+
+// One phase on the shared state copy (thread 0).  i = the iteration whose
+// body is running: its loop-top check was check i, so ss->iter == i + 1.
+__device__ void prod_phase(SolverState* ss, int phase, const double* d) {
+  const long long i = ss->iter - 1;
+  auto brk = [&](int q, int stage) {
+    ss->breakdown = q;
+    prod_stop(ss, PBS_BREAKDOWN, i, i, stage);
+  };
+  switch (phase) {
+    case kPhProdSetup: {  // rr = (r, r); f = rr; r0_norm = sqrt(rr)
+      const double rr = d[DR];
+      ss->r0_norm = sqrt(rr);
+      ss->f_prev = rr;
+      ss->rr = rr;
+      ss->upd = 0;
+      prod_check(ss, 0);
+      return;
+    }
+    case kPhProdAlpha: {  // guard (r0*, Ap); alpha = f / g
+      ss->upd = 0;
+      const double g = d[DG];
+      ss->dots[DG] = g;
+      if (guard(g, fabs(g))) return brk(PBS_BD_PROD_ALPHA, 1);
+      ss->alpha = ss->f_prev / g;
+      return;
+    }
+    case kPhStabOmega:
+    case kPhStabOmegaNC: {
+      const double b = d[DB], e = d[DE], c = d[DC], dd = d[DD];
+      double omega;
+      if (e == 0.0 && dd == 0.0) {
+        omega = 0.0;  // t = 0: the alpha half-step already landed
+      } else {
+        if (guard(e, fabs(e))) return brk(PBS_BD_STAB_OMEGA, 2);
+        omega = b / e;
+      }
+      ss->upd = 1;  // x = x + alpha p + omega t ; r = t - omega At run from here on
+      ss->omega = omega;
+      for (int k = 0; k < kNumDots; ++k)
+        if ((kDotsStabB >> k) & 1u) ss->dots[k] = d[k];
+      const double f = ss->f_prev, alpha = ss->alpha, g = ss->dots[DG];
+      const double f_next = sub(sub(f, mul(alpha, g)), mul(omega, c));
+      const double v = add(sub(dd, mul(mul(2.0, omega), b)), mul(mul(omega, omega), e));
+      const double rr = (0.0 > v) ? 0.0 : v;  // Python max(v, 0.0)
+      double beta;
+      if (rr == 0.0) {
+        beta = 0.0;
+      } else {
+        if (guard(omega, fabs(omega))) return brk(PBS_BD_STAB_BETA, 3);
+        if (guard(f, fabs(f))) return brk(PBS_BD_BETA_F, 3);
+        beta = mul(alpha / omega, f_next / f);
+      }
+      ss->f_prev = f_next;
+      ss->beta = beta;
+      ss->rr = rr;
+      if (!prod_record_coef(ss, i, alpha, beta, omega, __longlong_as_double(0x7ff8000000000000LL), false)) return;
+      if (phase == kPhStabOmega) prod_check(ss, i + 1);
+      return;
+    }
+    case kPhGpZeta: {
+      double zeta = 0.0, eta = 0.0;
+      const int q = zeta_eta_gpbicg(d[DA], d[DB], d[DC], d[DD], d[DE], i == 0, &zeta, &eta);
+      for (int k = 0; k < kNumDots; ++k)
+        if ((kDotsGpB >> k) & 1u) ss->dots[k] = d[k];
+      if (q) return brk(q, 2);
+      ss->zeta = zeta;
+      ss->eta = eta;
+      return;
+    }
+    case kPhGpBeta:
+    case kPhGpBetaNC: {
+      const double fn = d[DF], rr = d[DR], f = ss->f_prev, alpha = ss->alpha, zeta = ss->zeta;
+      ss->dots[DF] = fn;
+      ss->dots[DR] = rr;
+      ss->rr = rr;
+      double beta;
+      if (rr == 0.0) {
+        beta = 0.0;
+      } else {
+        if (guard(zeta, fabs(zeta))) return brk(PBS_BD_GP_BETA, 3);
+        if (guard(f, fabs(f))) return brk(PBS_BD_BETA_F, 3);
+        beta = mul(alpha / zeta, fn / f);
+      }
+      ss->f_prev = fn;
+      ss->beta = beta;
+      if (!prod_record_coef(ss, i, alpha, beta, zeta, ss->eta, true)) return;
+      if (phase == kPhGpBeta) prod_check(ss, i + 1);
+      return;
+    }
+    case kPhProdCheck:
+      prod_check(ss, i + 1);
+      return;
+  }
+}
+
+// state_store + host mirror (the tail of check_and_publish)
+template <int NT, bool NAMED>
+__device__ __forceinline__ void prod_and_publish(SolverState* st, SolverState* ss, const double* dots, int phase) {
+  block_bar<NT, NAMED>();
+  if (threadIdx.x != 0) return;
+  if (!dev_err(ss) && ss->run_all) prod_phase(ss, phase, dots);
+  state_store(st, ss);
+  if (ss->mirror) {
+    ss->mirror->iter = ss->iter;
+    ss->mirror->run_all = ss->run_all;
+    ss->mirror->err = dev_err(ss) ? 1 : 0;
+  }
+}
+
 // Reduce partial records (kPartStride doubles each: hi/lo per dot) -> dots[9]
 // with NT threads, fixed shape: one warp per dot, each lane summing a strided
 // subset of the records in double-double (pairwise, 16 records per pass),
@@ -293,7 +493,8 @@ __global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partial
 // the last CTA to arrive reduces all partials and performs the check.
 template <int NT, bool NAMED>
 __device__ void finalize_tail(SolverState* st, const double* partials, int nparts, int replaced,
-                              const double* partials2 = nullptr, int nparts2 = 0, unsigned mask2 = 0) {
+                              const double* partials2 = nullptr, int nparts2 = 0, unsigned mask2 = 0,
+                              int phase = kPhSafe) {
   __shared__ int last;
   __shared__ double dots[kNumDots];
   block_bar<NT, NAMED>();
@@ -309,7 +510,10 @@ __device__ void finalize_tail(SolverState* st, const double* partials, int npart
   state_load<NT>(st, &ss);
   reduce_parts<NT, NAMED>(partials, nparts, 0, dots, partials2, nparts2, mask2);  // ends with a barrier
   if (threadIdx.x == 0) st->done_ctas = 0;
-  check_and_publish<NT, NAMED>(st, &ss, dots, replaced);
+  if (phase == kPhSafe)
+    check_and_publish<NT, NAMED>(st, &ss, dots, replaced);
+  else
+    prod_and_publish<NT, NAMED>(st, &ss, dots, phase);
 }
 
 // Standalone finalize (1 CTA, 288 threads): reduce (tree or plan chain), then
@@ -317,7 +521,7 @@ __device__ void finalize_tail(SolverState* st, const double* partials, int npart
 __global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const double* partials, int nparts,
                                                        int chain, int replaced, const double* partials2 = nullptr,
                                                        int nparts2 = 0, unsigned mask2 = 0, int rs = 1,
-                                                       int fs = kMaxParts) {
+                                                       int fs = kMaxParts, int phase = kPhSafe) {
   __shared__ double dots[kNumDots];
   __shared__ SolverState ss;
 #ifdef PBS_TAIL_CLOCKS
@@ -328,7 +532,10 @@ __global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const do
 #ifdef PBS_TAIL_CLOCKS
   long long c1 = clock64();
 #endif
-  check_and_publish<288, false>(st, &ss, dots, replaced);
+  if (phase == kPhSafe)
+    check_and_publish<288, false>(st, &ss, dots, replaced);
+  else
+    prod_and_publish<288, false>(st, &ss, dots, phase);
 #ifdef PBS_TAIL_CLOCKS
   if (threadIdx.x == 0) {
     long long c2 = clock64();

@@ -333,6 +333,7 @@ struct Launcher {
   // calls trace_hook (after the updates, before the next check)
   const pbs_config* trace_cfg = nullptr;
   Workspace* trace_ws = nullptr;
+  int trace_method = 0;
   long long iter = 0;
   int trace_rc = 0;
   int err = 0;  // first launch-configuration failure (sticky)
@@ -376,9 +377,22 @@ void Launcher::trace_point() {
     trace_rc = set_err(ctx, PBS_ERR_NOMEM, "cannot allocate trace staging");
     return;
   }
-  const int order[13] = {VX, VR, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL};
+  // the reference's trace_hook dicts: Safe methods (solvers.py:725-732),
+  // BiCGStab (315), GPBi-CG (448)
+  static const int safe_order[13] = {VX, VR, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL};
+  static const int stab_order[6] = {VX, VR, VP, VT, VAP, VAT};
+  static const int gp_order[8] = {VX, VR, VP, VU, VT, VW, VY, VZ};
+  const int* order = safe_order;
+  int nv = 13;
+  if (trace_method == PBS_METHOD_BICGSTAB) {
+    order = stab_order;
+    nv = 6;
+  } else if (trace_method == PBS_METHOD_GPBICG) {
+    order = gp_order;
+    nv = 8;
+  }
   double* ptrs[13];
-  for (int k = 0; k < 13; ++k) {
+  for (int k = 0; k < nv; ++k) {
     ptrs[k] = ws->trace_host + k * n;
     cudaMemcpy(ptrs[k], ws->V.v[order[k]], sizeof(double) * n, cudaMemcpyDeviceToHost);
   }
@@ -435,10 +449,16 @@ static int pipe_extra_chunks() {  // chunk stages beyond the block slots
   return v;
 }
 
+// PBS_PIPE_STAGE_IN: 1 always stage the epilogue inputs, 0 never, 2 (default)
+// stage them unless that costs the second resident CTA per SM
+static int pipe_stage_in() {
+  static int v = env_int("PBS_PIPE_STAGE_IN", 2, 0, 2);
+  return v;
+}
+
 template <class Epi>
 static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_max, int* bslots, int* cstages,
-                       size_t* smem, int* ctas, int* chunk) {
-  const BlockLayout BL(W.total, Epi::kInStaged);
+                       size_t* smem, int* ctas, int* chunk, int* stage_in) {
   // one chunk per row block when the densest block fits the cap (stencils:
   // ~7 or ~27 nonzeros per row), else cap-sized chunks
   int ch = W.band_s ? band_chunk_cap() : pipe_chunk_cap();
@@ -447,7 +467,12 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  int n = 0, c = pipe_ctas_per_sm(), xc = 0;
+  int n = 0, c = pipe_ctas_per_sm(), xc = 0, si = 1;
+  // auto: windowed x only (config 4's 27-point rows: 15.3 -> 13.4 ms per
+  // iteration); band mode loses with unstaged inputs (config 3: 675 -> 818 us,
+  // profiles/sweeps/r1_stage_in.log)
+  int si_mode = Epi::kInStaged ? pipe_stage_in() : 1;
+  if (si_mode == 2 && !(W.nwin > 0 && W.band_s == 0)) si_mode = 1;
   for (; c >= 1; --c) {
     // per-CTA budget: the SM's shared memory split between the resident CTAs,
     // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
@@ -456,23 +481,30 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
     const size_t fixed = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double);
     if (budget <= fixed) continue;
     budget -= fixed;
-    n = (int)(budget / (BL.bytes + CL.bytes));
-    if (n > pipe_slots_cap()) n = pipe_slots_cap();
-    if (n < 2) continue;
-    // extra chunk stages so the next block's nonzeros stream while the
-    // current block's chunks are consumed
-    xc = (int)((budget - (size_t)n * (BL.bytes + CL.bytes)) / CL.bytes);
-    if (xc > pipe_extra_chunks()) xc = pipe_extra_chunks();
-    if (n + xc > kMaxStages) xc = kMaxStages - n;
-    break;
+    // staged inputs first; unstaged when only that keeps this many CTAs
+    for (si = si_mode == 0 ? 0 : 1; si >= (si_mode == 1 ? 1 : 0); --si) {
+      const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
+      n = (int)(budget / (BL.bytes + CL.bytes));
+      if (n > pipe_slots_cap()) n = pipe_slots_cap();
+      if (n < 2) continue;
+      // extra chunk stages so the next block's nonzeros stream while the
+      // current block's chunks are consumed
+      xc = (int)((budget - (size_t)n * (BL.bytes + CL.bytes)) / CL.bytes);
+      if (xc > pipe_extra_chunks()) xc = pipe_extra_chunks();
+      if (n + xc > kMaxStages) xc = kMaxStages - n;
+      break;
+    }
+    if (n >= 2) break;
   }
   if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
+  const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
   *ctas = c;
   *bslots = n;
   *cstages = n + xc;
   *chunk = ch;
+  *stage_in = si;
   *smem = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double) + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
-  const void* k = (const void*)csr_pipe_kernel<Epi>;
+  const void* k = si ? (const void*)csr_pipe_kernel<Epi, true> : (const void*)csr_pipe_kernel<Epi, false>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -579,9 +611,10 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, lo == 0 ? m->wc : nullptr};
     // staged x windows need the window-local columns; otherwise gather x
     const XWin W = A.wc ? m->xwin : XWin{};
-    int bslots, cstages, ctas, chunk;
+    int bslots, cstages, ctas, chunk, stage_in;
     size_t smem;
-    int rc = pipe_config<Epi>(L.ctx, W, A.wc ? 2 : 4, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk);
+    int rc = pipe_config<Epi>(L.ctx, W, A.wc ? 2 : 4, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk,
+                              &stage_in);
     if (rc) {
       L.err = rc;
       return 0;
@@ -590,7 +623,12 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     // programmatic dependent launch: overlaps this CTA's prologue and first
     // matrix chunks with the previous kernel's drain
-    launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi>, grid, kPipeThreads, smem, A, x, epi, W, bslots, cstages, chunk);
+    if (stage_in)
+      launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, true>, grid, kPipeThreads, smem, A, x, epi, W, bslots, cstages,
+                 chunk);
+    else
+      launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, false>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
+                 cstages, chunk);
     if (L.err) return 0;
   } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>()) {
     StencilView S = m->sv;
@@ -649,6 +687,7 @@ static void vec_launch(Launcher& L, K kernel, long long n, int kind, Args... arg
 struct Mode {
   int plan = 0;  // PBS_REDUCE_PLAN
   int store_temps = 0;
+  int method = PBS_METHOD_PBICGSAFE;
 };
 
 // ---- epilogue constructors (pointers into the workspace)
@@ -833,9 +872,10 @@ static int plan_dots(Launcher& L, Workspace* ws, int kind) {
   return ws->plan_w_actual;
 }
 
-static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int replaced, int np12 = 0) {
+static void finalize(Launcher& L, Workspace* ws, int nparts, int chain, int replaced, int np12 = 0,
+                     int phase = kPhSafe) {
   finalize_kernel<<<1, 288, 0, L.s>>>(ws->st, ws->partials, nparts, chain, replaced, ws->partials12, np12,
-                                      np12 ? kDotsK12 : 0u);
+                                      np12 ? kDotsK12 : 0u, 1, kMaxParts, phase);
   L.done(KF);
 }
 
@@ -934,6 +974,146 @@ static void final_ss(Launcher& L, Workspace* ws, const Mode& md) {
   finalize(L, ws, np, md.plan, 0);
 }
 
+// ---- product-type comparators: BiCGStab (solvers.py:210-327) and GPBi-CG
+// (solvers.py:330-460).  Per iteration (p materialised by the previous one):
+//   BiCGStab: Ap = A p + g [alpha] -> t -> At = A t + b e c d [omega, beta,
+//             check i+1] -> x, r and the next p
+//   GPBi-CG:  Ap = A p + g [alpha] -> y u t -> At = A t + a..e [zeta, eta]
+//             -> u z x r + f rr [beta, check i+1] -> w and the next p
+// Tree mode runs each phase in the tail of the kernel that produced its
+// dots; plan mode computes the reference's PartitionPlan chains and runs a
+// 1-CTA finalize.  With a trace hook the next p waits until after the hook.
+
+static int plan_pairs(Launcher& L, Workspace* ws, const DotPairs& P) {
+  dots_pairs_plan_kernel<<<ws->plan_w_actual, 32, 0, L.s>>>(ws->plan_bounds, P, ws->partials, ws->st);
+  L.done(KD);
+  return ws->plan_w_actual;
+}
+
+static DotPairs pairs_of(unsigned mask, const double* const* x, const double* const* y) {
+  DotPairs P{};
+  P.mask = mask;
+  for (int k = 0; k < kNumDots; ++k) {
+    P.x[k] = x[k];
+    P.y[k] = y[k];
+  }
+  return P;
+}
+
+static void setup_prod(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, ws->n, KS);  // r0 = b - A x0 ; r0s = r0
+  const int gp = md.method == PBS_METHOD_GPBICG;
+  long long nblk = (ws->n + kThreads - 1) / kThreads;
+  int np = grid_for(L.ctx, (const void*)prod_setup_kernel, nblk);
+  prod_setup_kernel<<<np, kThreads, 0, L.s>>>(ws->V, ws->n, ws->st, gp, md.plan ? nullptr : ws->partials, 1);
+  L.done(KS);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DR] = V[VR];
+    y[DR] = V[VR];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsRR, x, y)), 1, 0, 0, kPhProdSetup);
+  }
+}
+
+static EpiPA epi_pa(Workspace* ws, const Mode& md) {
+  EpiPA e{};
+  e.ap = ws->V.v[VAP];
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, 1, 0);
+  e.sink.phase = kPhProdAlpha;
+  e.in[0] = ws->V.v[VR0S];
+  return e;
+}
+
+template <class E>
+static E epi_prod_b(Workspace* ws, const Mode& md, int second, int phase) {
+  E e{};
+  e.at = ws->V.v[VAT];
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, 1, 0);
+  e.sink.phase = phase;
+  e.in[0] = ws->V.v[VT];
+  e.in[1] = ws->V.v[second];
+  return e;
+}
+
+// Ap = A p + g, then alpha
+static void prod_alpha(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  spmv_launch(L, ws->X.v[VP], epi_pa(ws, md), 0, ws->n, KK1);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DG] = V[VR0S];
+    y[DG] = V[VAP];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsProdA, x, y)), 1, 0, 0, kPhProdAlpha);
+  }
+}
+
+static void iter_stab(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  const bool tracing = L.trace_cfg != nullptr;
+  prod_alpha(L, ws, md);
+  vec_launch(L, stab_t_kernel, ws->n, KK2, ws->V, ws->n, ws->st);
+  const int ph = tracing ? kPhStabOmegaNC : kPhStabOmega;
+  spmv_launch(L, ws->X.v[VT], epi_prod_b<EpiStabB>(ws, md, VR0S, ph), 0, ws->n, KK3);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DB] = V[VAT], y[DB] = V[VT];
+    x[DE] = V[VAT], y[DE] = V[VAT];
+    x[DC] = V[VR0S], y[DC] = V[VAT];
+    x[DD] = V[VT], y[DD] = V[VT];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsStabB, x, y)), 1, 0, 0, ph);
+  }
+  vec_launch(L, stab_xrp_kernel, ws->n, KK2, ws->V, ws->n, ws->st, tracing ? 0 : 1);
+  if (tracing) {
+    L.trace_point();
+    finalize(L, ws, 0, 1, 0, 0, kPhProdCheck);
+    vec_launch(L, prod_p_kernel, ws->n, KK2, ws->V, ws->n, ws->st, 0);
+  }
+}
+
+static void iter_gp(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  const bool tracing = L.trace_cfg != nullptr;
+  prod_alpha(L, ws, md);
+  vec_launch(L, gp_yut_kernel, ws->n, KK2, ws->V, ws->n, ws->st);
+  spmv_launch(L, ws->X.v[VT], epi_prod_b<EpiGpB>(ws, md, VY, kPhGpZeta), 0, ws->n, KK3);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DA] = V[VY], y[DA] = V[VY];
+    x[DB] = V[VAT], y[DB] = V[VT];
+    x[DC] = V[VY], y[DC] = V[VT];
+    x[DD] = V[VAT], y[DD] = V[VY];
+    x[DE] = V[VAT], y[DE] = V[VAT];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsGpB, x, y)), 1, 0, 0, kPhGpZeta);
+  }
+  const int ph = tracing ? kPhGpBetaNC : kPhGpBeta;
+  {
+    long long nblk = (ws->n + kThreads - 1) / kThreads;
+    int np = grid_for(L.ctx, (const void*)gp_uzxr_kernel, nblk);
+    gp_uzxr_kernel<<<np, kThreads, 0, L.s>>>(ws->V, ws->n, ws->st, md.plan ? nullptr : ws->partials, 1, ph);
+    L.done(KK2);
+  }
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DF] = V[VR0S], y[DF] = V[VR];
+    x[DR] = V[VR], y[DR] = V[VR];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsGpC, x, y)), 1, 0, 0, ph);
+  }
+  vec_launch(L, gp_wp_kernel, ws->n, KK2, ws->V, ws->n, ws->st, tracing ? 0 : 1);
+  if (tracing) {
+    L.trace_point();
+    finalize(L, ws, 0, 1, 0, 0, kPhProdCheck);
+    vec_launch(L, prod_p_kernel, ws->n, KK2, ws->V, ws->n, ws->st, 1);
+  }
+}
+
 typedef void (*IterFn)(Launcher&, Workspace*, const Mode&);
 
 // steady iterations per graph (PBS_GRAPH_ITERS, default 4): inside one graph
@@ -945,6 +1125,12 @@ static int graph_iters() {
 }
 static void iter_steady_batch(Launcher& L, Workspace* ws, const Mode& md) {
   for (int k = 0; k < graph_iters(); ++k) iter_steady(L, ws, md);
+}
+static void iter_stab_batch(Launcher& L, Workspace* ws, const Mode& md) {
+  for (int k = 0; k < graph_iters(); ++k) iter_stab(L, ws, md);
+}
+static void iter_gp_batch(Launcher& L, Workspace* ws, const Mode& md) {
+  for (int k = 0; k < graph_iters(); ++k) iter_gp(L, ws, md);
 }
 
 static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const Mode& md,
@@ -1084,7 +1270,7 @@ static int collect_result(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
                           std::vector<std::pair<int, cudaEvent_t>>& marks, long long launched_graph_kernels) {
   pbs_ctx* ctx = m->ctx;
   Workspace* ws = m->ws;
-  const bool pipelined = method != PBS_METHOD_SSBICGSAFE2;
+  const bool pipelined = method == PBS_METHOD_PBICGSAFE || method == PBS_METHOD_PBICGSAFE_RR;
   const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
   const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
   SolverState out;
@@ -1128,7 +1314,12 @@ static int collect_result(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
     for (long long i = 1; i < completed && i < cutoff; ++i)
       if (i % cfg->rr_epoch == 0) ++nrep;
   res->n_replacements = nrep;
-  if (pipelined)
+  res->stop_stage = out.stop_stage;
+  if (method == PBS_METHOD_BICGSTAB || method == PBS_METHOD_GPBICG)
+    // r0 = b - A x0, then Ap and At per completed iteration; a stopping
+    // iteration that got past its loop-top check ran Ap (alpha stage) or both
+    res->n_spmv = 1 + 2 * completed + (out.stop_stage == 0 ? 0 : (out.stop_stage == 1 ? 1 : 2));
+  else if (pipelined)
     res->n_spmv = 2 + reached + completed + 5 * nrep;
   else
     res->n_spmv = 1 + reached + completed;
@@ -1147,6 +1338,8 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   md.plan = cfg->reduce_mode == PBS_REDUCE_PLAN;
   const bool tracing = cfg->trace_fn != nullptr;
   md.store_temps = tracing ? 1 : 0;
+  md.method = method;
+  const bool product = method == PBS_METHOD_BICGSTAB || method == PBS_METHOD_GPBICG;
   if (md.plan) {
     int rc = ensure_plan(m, cfg->plan_workers);
     if (rc) return rc;
@@ -1158,6 +1351,8 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   h.max_iters = cfg->max_iters;
   h.record_history = cfg->record_history ? 1 : 0;
   h.spine_done = method == PBS_METHOD_SSBICGSAFE2 ? 1 : 0;
+  h.upd = 0;
+  h.stop_stage = 0;
   h.iter = 0;
   h.run_all = 1;
   h.run_spine = 1;
@@ -1172,8 +1367,8 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   ws->mirror_h->run_all = 1;
   ws->mirror_h->err = 0;
   CK(cudaMemcpyAsync(ws->st, &h, sizeof(h), cudaMemcpyHostToDevice, s));
-  // zero-initialised workspace (solvers.py:621-628)
-  const int zero_slots[] = {VP, VU, VT, VY, VZ, VG, VL, VW};
+  // zero-initialised workspace (solvers.py:621-628; 251-253, 371-376)
+  const int zero_slots[] = {VP, VU, VT, VY, VZ, VG, VL, VW, VAP, VAT};
   for (int k : zero_slots) CK(cudaMemsetAsync(ws->V.v[k], 0, sizeof(double) * n, s));
 
   std::vector<std::pair<int, cudaEvent_t>> marks;
@@ -1184,9 +1379,10 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   if (tracing) {
     L.trace_cfg = cfg;
     L.trace_ws = ws;
+    L.trace_method = method;
   }
   const bool graphs = cfg->use_graphs && !L.timing && !tracing;
-  const bool pipelined = method != PBS_METHOD_SSBICGSAFE2;
+  const bool pipelined = method == PBS_METHOD_PBICGSAFE || method == PBS_METHOD_PBICGSAFE_RR;
   const bool rr = method == PBS_METHOD_PBICGSAFE_RR;
   const long long cutoff = cfg->rr_cutoff >= 0 ? cfg->rr_cutoff : cfg->max_iters;
   const long long key_base = (long long)md.plan * 4;
@@ -1195,6 +1391,9 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   if (L.timing) marks.push_back({-1, ws->ev0});
   if (pipelined) {
     setup_pipelined(L, ws, md);
+    if (L.err) return L.err;
+  } else if (product) {
+    setup_prod(L, ws, md);
     if (L.err) return L.err;
   } else {
     spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, n, KS);
@@ -1225,20 +1424,26 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
     {
       auto is_replace = [&](long long i) { return rr && (i % cfg->rr_epoch == 0) && 0 < i && i < cutoff; };
       const bool replace = is_replace(j);
-      IterFn fn = !pipelined ? iter_ss : (replace ? iter_replace : iter_steady);
+      IterFn fn = method == PBS_METHOD_BICGSTAB ? iter_stab
+                  : method == PBS_METHOD_GPBICG ? iter_gp
+                  : !pipelined ? iter_ss
+                  : (replace ? iter_replace : iter_steady);
+      IterFn bfn = method == PBS_METHOD_BICGSTAB ? iter_stab_batch
+                   : method == PBS_METHOD_GPBICG ? iter_gp_batch
+                   : iter_steady_batch;
       const int gu = graph_iters();
-      bool batch = graphs && pipelined && gu > 1 && j + gu <= cfg->max_iters;
+      bool batch = graphs && (pipelined || product) && gu > 1 && j + gu <= cfg->max_iters;
       for (long long i = j; batch && i < j + gu; ++i) batch = !is_replace(i);
       if (batch) {
         cudaGraphExec_t ge;
         long long nk = 0;
-        int rc = get_graph(ctx, m, key_base + 8, iter_steady_batch, md, &ge, &nk);
+        int rc = get_graph(ctx, m, key_base + 8 + 16 * method, bfn, md, &ge, &nk);
         if (rc) return rc;
         CK(cudaGraphLaunch(ge, s));
         launched_graph_kernels += nk;
         j += gu - 1;
       } else if (graphs) {
-        long long key = key_base + (!pipelined ? 2 : (replace ? 1 : 0));
+        long long key = key_base + (product ? 16 * method : (!pipelined ? 2 : (replace ? 1 : 0)));
         cudaGraphExec_t ge;
         long long nk = 0;
         int rc = get_graph(ctx, m, key, fn, md, &ge, &nk);
@@ -1253,7 +1458,7 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
       }
     }
   }
-  if (!pipelined) final_ss(L, ws, md);
+  if (method == PBS_METHOD_SSBICGSAFE2) final_ss(L, ws, md);
 loop_end:
   CK(cudaEventRecord(ws->ev1, s));
   CK(cudaStreamSynchronize(s));
@@ -1270,8 +1475,8 @@ static int run_solve_dist(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
   pbs_ctx* ctx = m->ctx;
   Workspace* ws = m->ws;
   pbs_dist* D = m->part.dist;
-  if (method == PBS_METHOD_SSBICGSAFE2)
-    return set_err(ctx, PBS_ERR_UNSUPPORTED, "ssBiCGSafe2 has no multi-GPU schedule yet");
+  if (method != PBS_METHOD_PBICGSAFE && method != PBS_METHOD_PBICGSAFE_RR)
+    return set_err(ctx, PBS_ERR_UNSUPPORTED, "only p-BiCGSafe(-rr) has a multi-GPU schedule");
   if (cfg->reduce_mode != PBS_REDUCE_TREE)
     return set_err(ctx, PBS_ERR_UNSUPPORTED, "multi-GPU solves use the compensated tree reduction");
   if (cfg->trace_fn) return set_err(ctx, PBS_ERR_UNSUPPORTED, "trace_hook is single-GPU only");
@@ -2002,7 +2207,7 @@ static int solve_common(pbs_mat* m, int32_t method, const pbs_config* cfg) {
   pbs_ctx* ctx = m ? m->ctx : nullptr;
   if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
   if (!m->part.dist && m->n_rows != m->n_cols) return set_err(ctx, PBS_ERR_INVALID, "solver needs a square operator");
-  if (method < 0 || method > 2) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
+  if (method < 0 || method > PBS_METHOD_GPBICG) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
   int rc = validate_cfg(ctx, cfg);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));

@@ -145,6 +145,7 @@ struct DotSink {
   double* partials;  // nullptr: no partials (PBS_REDUCE_PLAN computes them separately)
   int fuse;          // last CTA runs finalize_tail (check + coefficients)
   int replaced;      // the record this check writes follows a replacement
+  int phase;         // finalize phase (kPhSafe: the Safe methods' check)
   // the dots this kernel does not carry: K12's records (mask2 = kDotsK12)
   const double* partials2;
   int nparts2;
@@ -153,7 +154,7 @@ struct DotSink {
   __device__ void finish(DotsT<M>& d, SolverState* st) {
     if (!partials) return;
     block_reduce9<NT, NAMED, M>(d.acc, partials + blockIdx.x);
-    if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced, partials2, nparts2, mask2);
+    if (fuse) finalize_tail<NT, NAMED>(st, partials, gridDim.x, replaced, partials2, nparts2, mask2, phase);
   }
 };
 
@@ -389,6 +390,79 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
   __device__ void finish() {}
 };
 
+// ---- product-type comparators (BiCGStab solvers.py:210-327, GPBi-CG 330-460)
+
+// Ap = A p (check_finite tag "Ap"), then the partials of g = (r0*, Ap)
+struct EpiPA {
+  static constexpr int kIn = 1;
+  static constexpr int kInStaged = kIn;
+  static constexpr int kWcBatch = 4;
+  static constexpr int kMinBlocks = 1;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 8;
+  double* ap;
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // r0s
+  DotsT<kDotsProdA> d;
+  __device__ bool active() const { return gate_all(st); }
+  // a stopped solve: the stopping iteration's x/r update has run, so close
+  // its gate for iterations the host launched ahead
+  __device__ void on_skip() const {
+    if (!dev_err(st) && !st->run_all) st->upd = 0;
+  }
+  __device__ void init() { d.zero(); }
+  __device__ void row(long long i, double v, const double* in1) {
+    ap[i] = v;
+    if (!isfinite(v)) report_nonfinite(st, PBS_TAG_AP, i);
+    if (sink.partials) d.step(DG, in1[0], v);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+
+// At = A t (tag "At"), then BiCGStab's b=(At,t) e=(At,At) c=(r0*,At) d=(t,t)
+// or GPBi-CG's a=(y,y) b=(At,t) c=(y,t) d=(At,y) e=(At,At)
+template <bool GP>
+struct EpiProdBT {
+  static constexpr int kIn = 2;
+  static constexpr int kInStaged = kIn;
+  static constexpr int kWcBatch = 4;
+  static constexpr int kMinBlocks = 1;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 8;
+  double* at;
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // t, then r0s (BiCGStab) or y (GPBi-CG)
+  DotsT<GP ? kDotsGpB : kDotsStabB> d;
+  __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() { d.zero(); }
+  __device__ void row(long long i, double v, const double* in2) {
+    at[i] = v;
+    if (!isfinite(v)) report_nonfinite(st, PBS_TAG_AT, i);
+    if (!sink.partials) return;
+    const double t = in2[0], q = in2[1];
+    if constexpr (GP) {
+      d.step(DA, q, q);
+      d.step(DB, v, t);
+      d.step(DC, q, t);
+      d.step(DD, v, q);
+      d.step(DE, v, v);
+    } else {
+      d.step(DB, v, t);
+      d.step(DE, v, v);
+      d.step(DC, q, v);
+      d.step(DD, t, t);
+    }
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+using EpiStabB = EpiProdBT<false>;
+using EpiGpB = EpiProdBT<true>;
+
 // --------------------------------------------------- CSR pipelined engine
 
 constexpr int kPipeRows = 256;        // rows per block = consumer threads
@@ -460,17 +534,21 @@ constexpr size_t kPipeBarrierBytes = 512;
 // every thread wait for the previous grid (griddep_wait) and take the CTA's
 // one gate decision.  Consumers release the next kernel's launch once their
 // rows are written, before the dot reduction / check tail.
-template <class Epi>
+template <class Epi, bool SI = true>
 __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
                                                                    Epi epi, XWin W, int bslots, int cstages,
                                                                    int chunk) {
+  constexpr bool stage_in = SI;
   __shared__ int go;
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* cfull = reinterpret_cast<uint64_t*>(smem);
   uint64_t* cempty = cfull + kMaxStages;
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
-  const BlockLayout BL(W.total, Epi::kInStaged);
+  // stage_in = 0: the epilogue inputs are not staged (their slot space goes
+  // to a second resident CTA when x windows are wide, e.g. 27-point rows);
+  // consumers load them from global memory while the row's products run
+  const BlockLayout BL(W.total, stage_in ? Epi::kInStaged : 0);
   const ChunkLayout CL(chunk, A.wc ? 2 : 4);
   double* xband = reinterpret_cast<double*>(smem + kPipeBarrierBytes);  // band mode only
   unsigned char* blk0 = smem + kPipeBarrierBytes + (size_t)W.band_s * sizeof(double);
@@ -584,7 +662,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       // x windows of this block (every lane computes them; lane 1+c copies window c)
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = brp + Epi::kInStaged * bin;
+      uint32_t total = brp + (stage_in ? Epi::kInStaged * bin : 0u);
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0x7fffffff;
@@ -659,7 +737,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
             bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
           soff += cc < W.nwin ? W.cap[cc] : 0;
         }
-      } else if (lane >= 8 && lane < 8 + Epi::kInStaged) {
+      } else if (stage_in && lane >= 8 && lane < 8 + Epi::kInStaged) {
         const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
       }
@@ -699,7 +777,8 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
       my_e = rps[t + dr + 1];
       // inputs the producer does not stage: in flight during the row's products
 #pragma unroll
-      for (int k = Epi::kInStaged; k < Epi::kIn; ++k) inr[k] = __ldg(e.in[k] + r0 + t);
+      for (int k = 0; k < Epi::kIn; ++k)
+        if (k >= Epi::kInStaged || !stage_in) inr[k] = __ldg(e.in[k] + r0 + t);
     }
     // staged x windows (or the band buffer), addressed by the window-local
     // column stream
@@ -757,8 +836,10 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
     }
     if (t < nr) {
       const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
+      if (stage_in) {
 #pragma unroll
-      for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+        for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
+      }
       e.row(r0 + t, acc, inr);
     }
     __syncwarp();

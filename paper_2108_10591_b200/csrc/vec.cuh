@@ -10,6 +10,8 @@ namespace pbs {
 enum Vec {
   VX = 0, VR, VR0S, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL, VAS, VAW, VTMP, VB, kNumVecs
 };
+// the product-type comparators keep A p and A t in the As / Aw slots
+constexpr int VAP = VAS, VAT = VAW;
 
 struct VecPtrs {
   double* v[kNumVecs];
@@ -99,6 +101,165 @@ __global__ void __launch_bounds__(kThreads) tzyx_kernel(VecPtrs V, long long n, 
     y[i] = lc3(zeta, s[i], eta, y[i], -alpha, wv);
     x[i] = lc3(1.0, x[i], alpha, p[i], 1.0, zn);
   }
+}
+
+// ---------------------------------------------------------------------------
+// product-type comparators (BiCGStab solvers.py:210-327, GPBi-CG 330-460).
+// Grid-stride loops; kernels that carry a reduction phase accumulate its
+// compensated dots and the last CTA runs that phase (finalize_tail).
+
+// after r0 = b - A x0: p0 = r + 0*(p - ...) on the zeroed workspace (the
+// first iteration's p update, solvers.py:265 / 381) and the partials of
+// (r, r) (solvers.py:244 / 365) -> r0_norm, f, check 0
+__global__ void __launch_bounds__(kThreads) prod_setup_kernel(VecPtrs V, long long n, SolverState* st, int gp,
+                                                              double* partials, int fuse) {
+  __shared__ int go;
+  if (threadIdx.x == 0) go = gate_all(st);
+  __syncthreads();
+  if (!go) return;
+  Ddbl acc[kNumDots];
+#pragma unroll
+  for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
+  double *__restrict__ p = V.v[VP];
+  const double *__restrict__ r = V.v[VR], *__restrict__ u = V.v[VU], *__restrict__ ap = V.v[VAP];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double rv = r[i];
+    p[i] = gp ? asd(rv, 0.0, p[i], u[i]) : asdd(rv, 0.0, p[i], 0.0, ap[i]);
+    acc[DR] = dot2_step(acc[DR], rv, rv);
+  }
+  if (!partials) return;
+  block_reduce9<kThreads, false, kDotsRR>(acc, partials + blockIdx.x);
+  if (fuse) finalize_tail<kThreads, false>(st, partials, gridDim.x, 0, nullptr, 0, 0u, kPhProdSetup);
+}
+
+// BiCGStab t = r - alpha*Ap (solvers.py:279)
+__global__ void __launch_bounds__(kThreads) stab_t_kernel(VecPtrs V, long long n, SolverState* st) {
+  if (!gate_all(st)) return;
+  const double alpha = st->alpha;
+  double *__restrict__ t = V.v[VT];
+  const double *__restrict__ r = V.v[VR], *__restrict__ ap = V.v[VAP];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    t[i] = lc2(1.0, r[i], -alpha, ap[i]);
+}
+
+// BiCGStab x = x + alpha*p + omega*t; r = t - omega*At (solvers.py:295-298),
+// then (with_p) the next iteration's p = r + beta*(p - omega*Ap)
+// (solvers.py:265).  Gated on the omega phase's go-ahead: the update runs
+// even when the beta guard or check i+1 stops the solve.
+__global__ void __launch_bounds__(kThreads) stab_xrp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
+  if (dev_err(st) || !st->upd) return;
+  const double alpha = st->alpha, omega = st->omega, beta = st->beta;
+  double *__restrict__ x = V.v[VX], *__restrict__ r = V.v[VR], *__restrict__ p = V.v[VP];
+  const double *__restrict__ t = V.v[VT], *__restrict__ at = V.v[VAT], *__restrict__ ap = V.v[VAP];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double tv = t[i], pv = p[i];
+    x[i] = lc3(1.0, x[i], alpha, pv, omega, tv);
+    const double rn = lc2(1.0, tv, -omega, at[i]);
+    r[i] = rn;
+    if (with_p) p[i] = asdd(rn, beta, pv, omega, ap[i]);
+  }
+}
+
+// the p update at the top of the next iteration, when a trace hook had to
+// see the old p: BiCGStab p = r + beta*(p - omega*Ap), GPBi-CG
+// p = r + beta*(p - u) (solvers.py:265, 381)
+__global__ void __launch_bounds__(kThreads) prod_p_kernel(VecPtrs V, long long n, SolverState* st, int gp) {
+  if (!gate_all(st)) return;
+  const double beta = st->beta, omega = st->omega;
+  double *__restrict__ p = V.v[VP];
+  const double *__restrict__ r = V.v[VR], *__restrict__ u = V.v[VU], *__restrict__ ap = V.v[VAP];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride)
+    p[i] = gp ? asd(r[i], beta, p[i], u[i]) : asdd(r[i], beta, p[i], omega, ap[i]);
+}
+
+// GPBi-CG y = t - r - alpha*w + alpha*Ap; u = t - r + beta*u (stash);
+// t = r - alpha*Ap (solvers.py:394-399) in one pass
+__global__ void __launch_bounds__(kThreads) gp_yut_kernel(VecPtrs V, long long n, SolverState* st) {
+  if (!gate_all(st)) return;
+  const double alpha = st->alpha, beta = st->beta;
+  double *__restrict__ y = V.v[VY], *__restrict__ u = V.v[VU], *__restrict__ t = V.v[VT];
+  const double *__restrict__ r = V.v[VR], *__restrict__ w = V.v[VW], *__restrict__ ap = V.v[VAP];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double tv = t[i], rv = r[i], apv = ap[i];
+    y[i] = lc4(1.0, tv, -1.0, rv, -alpha, w[i], alpha, apv);
+    u[i] = lc3(1.0, tv, -1.0, rv, beta, u[i]);
+    t[i] = lc2(1.0, rv, -alpha, apv);
+  }
+}
+
+// GPBi-CG u = zeta*Ap + eta*u; z = zeta*r + eta*z - alpha*u; x = x + alpha*p
+// + z; r = t - eta*y - zeta*At (solvers.py:416-419), with the partials of
+// the third phase f = (r0*, r), rr = (r, r) (solvers.py:421-423)
+__global__ void __launch_bounds__(kThreads) gp_uzxr_kernel(VecPtrs V, long long n, SolverState* st,
+                                                           double* partials, int fuse, int phase) {
+  __shared__ int go;
+  if (threadIdx.x == 0) go = gate_all(st);
+  __syncthreads();
+  if (!go) return;
+  const double alpha = st->alpha, zeta = st->zeta, eta = st->eta;
+  double *__restrict__ u = V.v[VU], *__restrict__ z = V.v[VZ], *__restrict__ x = V.v[VX], *__restrict__ r = V.v[VR];
+  const double *__restrict__ ap = V.v[VAP], *__restrict__ p = V.v[VP], *__restrict__ t = V.v[VT],
+               *__restrict__ y = V.v[VY], *__restrict__ at = V.v[VAT], *__restrict__ r0s = V.v[VR0S];
+  Ddbl acc[kNumDots];
+#pragma unroll
+  for (int j = 0; j < kNumDots; ++j) acc[j] = Ddbl{0.0, 0.0};
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    const double rv = r[i];
+    const double un = lc2(zeta, ap[i], eta, u[i]);
+    const double zn = lc3(zeta, rv, eta, z[i], -alpha, un);
+    u[i] = un;
+    z[i] = zn;
+    x[i] = lc3(1.0, x[i], alpha, p[i], 1.0, zn);
+    const double rn = lc3(1.0, t[i], -eta, y[i], -zeta, at[i]);
+    r[i] = rn;
+    acc[DF] = dot2_step(acc[DF], r0s[i], rn);
+    acc[DR] = dot2_step(acc[DR], rn, rn);
+  }
+  if (!partials) return;
+  block_reduce9<kThreads, false, kDotsGpC>(acc, partials + blockIdx.x);
+  if (fuse) finalize_tail<kThreads, false>(st, partials, gridDim.x, 0, nullptr, 0, 0u, phase);
+}
+
+// GPBi-CG w = At + beta*Ap (solvers.py:440), then (with_p) the next
+// iteration's p = r + beta*(p - u) (solvers.py:381)
+__global__ void __launch_bounds__(kThreads) gp_wp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
+  if (!gate_all(st)) return;
+  const double beta = st->beta;
+  double *__restrict__ w = V.v[VW], *__restrict__ p = V.v[VP];
+  const double *__restrict__ at = V.v[VAT], *__restrict__ ap = V.v[VAP], *__restrict__ r = V.v[VR],
+               *__restrict__ u = V.v[VU];
+  const long long stride = (long long)gridDim.x * kThreads;
+  for (long long i = (long long)blockIdx.x * kThreads + threadIdx.x; i < n; i += stride) {
+    w[i] = lc2(1.0, at[i], beta, ap[i]);
+    if (with_p) p[i] = asd(r[i], beta, p[i], u[i]);
+  }
+}
+
+// PartitionPlan chains over up to 9 arbitrary pairs (reduction.py:282-283):
+// block w sums range w of pair j (mask bit j) sequentially into field 2j
+struct DotPairs {
+  const double* x[kNumDots];
+  const double* y[kNumDots];
+  unsigned mask;
+};
+__global__ void dots_pairs_plan_kernel(const long long* bounds, DotPairs P, double* partials,
+                                       const SolverState* st) {
+  if (st && !gate_all(st)) return;
+  const int j = threadIdx.x;
+  if (j >= kNumDots || !((P.mask >> j) & 1u)) return;
+  const double* xa = P.x[j];
+  const double* ya = P.y[j];
+  const long long lo = bounds[blockIdx.x], hi = bounds[blockIdx.x + 1];
+  double acc = 0.0;
+  for (long long k = lo; k < hi; ++k) acc = add(acc, mul(xa[k], ya[k]));
+  partials[(size_t)(2 * j) * kMaxParts + blockIdx.x] = acc;
+  partials[(size_t)(2 * j + 1) * kMaxParts + blockIdx.x] = 0.0;
 }
 
 // ---------------------------------------------------------------------------

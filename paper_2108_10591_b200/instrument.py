@@ -14,10 +14,11 @@ from dataclasses import dataclass, field
 
 # (#Ax, #dots, #reductions) a steady-state iteration must cost (instrument.py:28-32)
 EXPECTED_PER_ITERATION = {
+    "bicgstab": (2, 5, 2),
     "ssbicgsafe2": (2, 9, 1),
     "pbicgsafe": (2, 9, 1),
 }
-EXPECTED_WORKSPACE = {"ssbicgsafe2": 10, "pbicgsafe": 15, "pbicgsafe-rr": 15}
+EXPECTED_WORKSPACE = {"bicgstab": 7, "ssbicgsafe2": 10, "pbicgsafe": 15, "pbicgsafe-rr": 15}
 
 # per-update (scalar mults, vector adds) exactly as the reference tallies them
 _PIPE_STEADY = (21, 22)   # solvers.py:679-724
@@ -64,7 +65,39 @@ class OpCounters:
         }
 
 
-def synthesize(method: str, iterations: int, stopped_in_loop: bool, replaced_at) -> OpCounters:
+# The product-type comparators tick in stages (solvers.py:239-317, 360-450);
+# each stage is (spmv, dots-in-batch or 0, (mults, adds) updates...).  A
+# stopping iteration runs the stages up to its stop stage (the device reports
+# it: 1 alpha, 2 omega/zeta, 3 after the x/r update, 4 complete).
+_PROD_STAGES = {
+    "bicgstab": [
+        [(0, 0, (2, 2)), (1, 1, None)],                      # p, Ap, (r0*, Ap)
+        [(0, 0, (1, 1)), (1, 4, None)],                      # t, At, b e c d
+        [(0, 0, (2, 2)), (0, 0, (1, 1))],                    # x, r
+        [],                                                  # beta, record
+    ],
+    "gpbicg": [
+        [(0, 0, (1, 2)), (1, 1, None)],                      # p, Ap, (r0*, Ap)
+        [(0, 0, (2, 3)), (0, 0, (1, 2)), (0, 0, (1, 1)), (1, 5, None)],  # y u t, At, a..e
+        [(0, 0, (2, 1)), (0, 0, (3, 2)), (0, 0, (1, 2)), (0, 0, (2, 2)), (0, 2, None)],  # u z x r, f rr
+        [(0, 0, (1, 1))],                                    # w
+    ],
+}
+
+
+def _prod_tick(c: OpCounters, method: str, stages: int) -> None:
+    for stage in _PROD_STAGES[method][:stages]:
+        for spmv_n, dots, upd in stage:
+            if spmv_n:
+                c.spmv(spmv_n)
+            if dots:
+                c.batch(dots)
+            if upd:
+                c.updates(*upd)
+
+
+def synthesize(method: str, iterations: int, stopped_in_loop: bool, replaced_at,
+               stop_stage: int = 0) -> OpCounters:
     """Counters the reference loop would have ticked for this outcome.
 
     ``iterations`` completed iterations; ``stopped_in_loop`` when a loop check
@@ -72,6 +105,18 @@ def synthesize(method: str, iterations: int, stopped_in_loop: bool, replaced_at)
     iteration's batch and spine SpMV were still counted; ``replaced_at`` the
     set of completed iterations that ran residual replacement.
     """
+    if method in _PROD_STAGES:
+        c = OpCounters(n_workspace_vectors=7 if method == "bicgstab" else 11)
+        c.spmv()
+        c.updates(0, 1)
+        c.batch(1)
+        c.snapshot()
+        for _ in range(iterations):
+            _prod_tick(c, method, 4)
+            c.snapshot()
+        if stopped_in_loop and stop_stage:
+            _prod_tick(c, method, stop_stage)
+        return c
     pipelined = method != "ssbicgsafe2"
     c = OpCounters(n_workspace_vectors=16 if pipelined else 11)
     c.spmv(2 if pipelined else 1)

@@ -167,6 +167,9 @@ def _prepare(A, b, x0):
 
 
 _TRACE_NAMES = ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l")
+# the reference's trace_hook dicts of the product-type methods (solvers.py:315, 448)
+_TRACE_NAMES_BY_METHOD = {"bicgstab": ("x", "r", "p", "t", "Ap", "At"),
+                          "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z")}
 
 
 def _ptr(a):
@@ -203,9 +206,11 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
             cfg.events_count = C.pointer(ev_cnt)
         cb_keep = None
         if trace_hook is not None:
+            names = _TRACE_NAMES_BY_METHOD.get(method, _TRACE_NAMES)
+
             def _cb(i, vecs, _user):
                 ws = {name: np.ctypeslib.as_array(vecs[k], shape=(n,))
-                      for k, name in enumerate(_TRACE_NAMES)}
+                      for k, name in enumerate(names)}
                 trace_hook(int(i), ws)
             cb_keep = _lib.TRACE_FN(_cb)
             cfg.trace_fn = cb_keep
@@ -233,8 +238,12 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
     for i in range(k):
         rec = IterationRecord(i, float(rel[i]), replaced=bool(flags[i] & _lib.HIST_REPLACED))
         if flags[i] & _lib.HIST_HAS_COEF:
-            rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
-                                              zeta=float(coef[i, 2]), eta=float(coef[i, 3]))
+            if method == "bicgstab":  # CoefficientSet(alpha, beta, omega) (solvers.py:309)
+                rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
+                                                  omega=float(coef[i, 2]))
+            else:
+                rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
+                                                  zeta=float(coef[i, 2]), eta=float(coef[i, 3]))
         history.append(rec)
     status = _STATUS[res.status]
     iterations = int(res.iterations)
@@ -243,7 +252,7 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
     if method == "pbicgsafe-rr":
         cutoff = config.rr_cutoff if config.rr_cutoff is not None else config.max_iters
         replaced_at = {i for i in range(1, iterations) if i % config.rr_epoch == 0 and i < cutoff}
-    counters = synthesize(method, iterations, stopped_in_loop, replaced_at)
+    counters = synthesize(method, iterations, stopped_in_loop, replaced_at, stop_stage=int(res.stop_stage))
     best = min((r.rel_res_recur for r in history), default=math.inf)
     final = history[-1].rel_res_recur if history else math.inf
     device = {
@@ -286,7 +295,21 @@ def solve_ssbicgsafe2(A, b, x0=None, config=None, engine=None, trace_hook=None) 
     return _solve_device(A, b, "ssbicgsafe2", x0, config, engine, trace_hook)
 
 
+def solve_bicgstab(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Stabilized bi-conjugate gradients, two reduction phases per iteration
+    (solvers.py:210-327) on the device: BASELINE config 2's BiCGStab comparator."""
+    return _solve_device(A, b, "bicgstab", x0, config, engine, trace_hook)
+
+
+def solve_gpbicg(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Generalized product-type solver, three reduction phases per iteration
+    (solvers.py:330-460) on the device."""
+    return _solve_device(A, b, "gpbicg", x0, config, engine, trace_hook)
+
+
 METHODS = {
+    "bicgstab": solve_bicgstab,
+    "gpbicg": solve_gpbicg,
     "ssbicgsafe2": solve_ssbicgsafe2,
     "pbicgsafe": solve_pbicgsafe,
     "pbicgsafe-rr": solve_pbicgsafe_rr,

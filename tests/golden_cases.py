@@ -97,3 +97,8 @@ def load_case(name: str, spmv, trace: bool = False):
 def case_names(trace: bool = False):
     mod = _spec_module()
     return list((mod.TRACE_CASES if trace else mod.CASES).keys())
+
+
+def case_spec(name: str, trace: bool = False) -> dict:
+    mod = _spec_module()
+    return (mod.TRACE_CASES if trace else mod.CASES)[name]

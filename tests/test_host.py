@@ -106,7 +106,13 @@ def test_counter_synthesis_matches_reference(name):
         cutoff = spec.get("rr_cutoff") or spec["max_iters"]
         m = spec.get("rr_epoch", 100)
         replaced = {i for i in range(1, iters) if i % m == 0 and i < cutoff}
-    c = synthesize(method, iters, iters < spec["max_iters"], replaced)
+    # product-type methods: where a breakdown stopped the iteration (the
+    # device reports it as stop_stage)
+    stage = {"alpha denominator (r0*, Ap)": 1, "omega denominator (At, At)": 2,
+             "zeta denominator (At, At)": 2, "zeta/eta denominator e*a - d^2": 2,
+             "beta denominator omega": 3, "beta denominator zeta": 3,
+             "beta denominator (r0*, r)": 3}.get(str(g["breakdown"]), 0)
+    c = synthesize(method, iters, iters < spec["max_iters"], replaced, stop_stage=stage)
     assert c.n_spmv == int(g["n_spmv"])
     assert c.n_dots == int(g["n_dots"])
     assert c.n_reductions == int(g["n_reductions"])
@@ -120,6 +126,15 @@ def test_synthesized_costs_match_cost_model():
     c = synthesize("ssbicgsafe2", 30, True, set())
     row = per_iteration_costs(c, "ssbicgsafe2")
     assert (row.scalar_mults_per_iter, row.vec_adds_per_iter) == (13, 14)
+    # test_instrument.py:32-39, 62-66
+    c = synthesize("bicgstab", 30, True, set())
+    row = per_iteration_costs(c, "bicgstab")
+    assert (row.ax_per_iter, row.dots_per_iter, row.reductions_per_iter) == (2, 5, 2)
+    assert (row.scalar_mults_per_iter, row.vec_adds_per_iter, row.workspace_vectors) == (6, 6, 7)
+    assert row.tabulated_workspace_vectors == 7
+    c = synthesize("gpbicg", 30, True, set())
+    row = per_iteration_costs(c, "gpbicg")
+    assert (row.ax_per_iter, row.dots_per_iter, row.reductions_per_iter) == (2, 8, 3)
 
 
 def test_generators_and_config_sizes():
