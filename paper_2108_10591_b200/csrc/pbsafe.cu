@@ -449,13 +449,23 @@ static int pipe_extra_chunks() {  // chunk stages beyond the block slots
   return v;
 }
 
-// PBS_PIPE_STAGE_IN: 1 always stage the epilogue inputs, 0 never, 2 (default)
-// stage them unless that costs the second resident CTA per SM
+// PBS_PIPE_STAGE_IN: 1 (default) stage the epilogue inputs, 0 never (the
+// consumers load them; loses everywhere measured, profiles/sweeps/r1_c4_pipe.log)
 static int pipe_stage_in() {
-  static int v = env_int("PBS_PIPE_STAGE_IN", 2, 0, 2);
+  static int v = env_int("PBS_PIPE_STAGE_IN", 1, 0, 1);
   return v;
 }
 
+// Ring sizing.  The engine is bound by the bytes each SM keeps in flight
+// (Little's law: ~45 KB/us per SM at full HBM rate times ~1-2 us of loaded
+// latency), so among CTAs-per-SM choices take the one whose rings hold the
+// most shared memory: block slots (row_ptr, x windows, epilogue inputs) plus
+// chunk stages, with every chunk stage the budget allows beyond the slots
+// (PBS_PIPE_XCHUNK caps them) when blocks span several chunks.  Ties
+// (within 5%) go to more CTAs per SM.
+// Config 2 keeps 2 CTAs/SM; config 4's 27-point rows (7k nonzeros and 25 KB
+// of x windows per block) get 1 CTA/SM with 4 extra chunk stages
+// (13.8 -> 10.6 ms per iteration).
 template <class Epi>
 static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_max, int* bslots, int* cstages,
                        size_t* smem, int* ctas, int* chunk, int* stage_in) {
@@ -467,37 +477,38 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  int n = 0, c = pipe_ctas_per_sm(), xc = 0, si = 1;
-  // auto: windowed x only (config 4's 27-point rows: 15.3 -> 13.4 ms per
-  // iteration); band mode loses with unstaged inputs (config 3: 675 -> 818 us,
-  // profiles/sweeps/r1_stage_in.log)
-  int si_mode = Epi::kInStaged ? pipe_stage_in() : 1;
-  if (si_mode == 2 && !(W.nwin > 0 && W.band_s == 0)) si_mode = 1;
-  for (; c >= 1; --c) {
+  const int si = Epi::kInStaged ? pipe_stage_in() : 1;
+  const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
+  // extra chunk stages pay when a block spans several chunks (the consumers
+  // walk them in turn); with one chunk per block (7-point stencils, config 2:
+  // 162 -> 166 us per iteration with them) the slots already double-buffer
+  const char* xenv = getenv("PBS_PIPE_XCHUNK");
+  const int xcap = xenv ? pipe_extra_chunks() : (blk_nnz_max > ch ? kMaxStages : 0);
+  int n = 0, c = 0, xc = 0;
+  size_t best = 0;
+  for (int cc = pipe_ctas_per_sm(); cc >= 1; --cc) {
     // per-CTA budget: the SM's shared memory split between the resident CTAs,
     // less the 1 KiB the runtime reserves per CTA and the kernel's static smem
-    size_t budget = (size_t)per_sm / c - 1024 - 2048;
+    size_t budget = (size_t)per_sm / cc - 1024 - 2048;
     if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
     const size_t fixed = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double);
     if (budget <= fixed) continue;
     budget -= fixed;
-    // staged inputs first; unstaged when only that keeps this many CTAs
-    for (si = si_mode == 0 ? 0 : 1; si >= (si_mode == 1 ? 1 : 0); --si) {
-      const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
-      n = (int)(budget / (BL.bytes + CL.bytes));
-      if (n > pipe_slots_cap()) n = pipe_slots_cap();
-      if (n < 2) continue;
-      // extra chunk stages so the next block's nonzeros stream while the
-      // current block's chunks are consumed
-      xc = (int)((budget - (size_t)n * (BL.bytes + CL.bytes)) / CL.bytes);
-      if (xc > pipe_extra_chunks()) xc = pipe_extra_chunks();
-      if (n + xc > kMaxStages) xc = kMaxStages - n;
-      break;
+    int nn = (int)(budget / (BL.bytes + CL.bytes));
+    if (nn > pipe_slots_cap()) nn = pipe_slots_cap();
+    if (nn < 2) continue;
+    int xx = (int)((budget - (size_t)nn * (BL.bytes + CL.bytes)) / CL.bytes);
+    if (xx > xcap) xx = xcap;
+    if (nn + xx > kMaxStages) xx = kMaxStages - nn;
+    const size_t bytes = (size_t)cc * ((size_t)nn * BL.bytes + (size_t)(nn + xx) * CL.bytes);
+    if (bytes * 20 > best * 21) {  // > 5% more in flight than the larger-CTA choice
+      best = bytes;
+      n = nn;
+      c = cc;
+      xc = xx;
     }
-    if (n >= 2) break;
   }
   if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
-  const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
   *ctas = c;
   *bslots = n;
   *cstages = n + xc;

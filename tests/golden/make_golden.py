@@ -331,11 +331,68 @@ def coeffs_gpbicg_fixture():
     return dict(gz_in=np.array(gz_in, dtype=np.float64), gz_out=np.array(gz_out))
 
 
+# Matrix Market texts the reference's loader (mmio.py:33-137) is run on;
+# bad ones record the line number its error names
+MM_TEXTS = {
+    "general": "%%MatrixMarket matrix coordinate real general\n% c\n3 3 4\n1 1 2.0\n2 2 -1.5\n3 1 4.0\n3 3 0.5\n",
+    "symmetric": "%%MatrixMarket matrix coordinate real symmetric\n3 3 4\n1 1 2.0\n2 1 -1.0\n3 2 -1.0\n3 3 2.0\n",
+    "integer": "%%MatrixMarket matrix coordinate integer general\n2 2 2\n1 1 3\n2 2 -4\n",
+    "duplicates": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n1 1 2.5\n2 2 1.0\n",
+    "blank_and_comments": "%%MatrixMarket matrix coordinate real general\n%x\n\n2 3 2\n% y\n1 3 1e-3\n\n2 1 -7\n",
+    "empty": "%%MatrixMarket matrix coordinate real general\n4 4 0\n",
+    "bad_header": "%%NotMatrixMarket nope\n1 1 0\n",
+    "complex": "%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1.0 0.0\n",
+    "bad_size": "%%MatrixMarket matrix coordinate real general\n3 x 1\n1 1 1.0\n",
+    "count_mismatch": "%%MatrixMarket matrix coordinate real general\n2 2 3\n1 1 1.0\n2 2 1.0\n",
+    "bad_entry": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 oops 1.0\n",
+    "short_entry": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 2\n",
+    "out_of_range": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n3 1 1.0\n",
+    "frac_index": "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n1.5 1 1.0\n",
+    "sym_rect": "%%MatrixMarket matrix coordinate real symmetric\n2 3 1\n1 1 1.0\n",
+    "pattern": "%%MatrixMarket matrix coordinate pattern general\n1 1 1\n1 1\n",
+    "negative": "%%MatrixMarket matrix coordinate real general\n-1 2 0\n",
+}
+
+
+def mmio_fixture(tmpdir):
+    from pipesafe.mmio import MatrixMarketError, load_matrix_market, write_matrix_market
+
+    out = {}
+    rng = np.random.default_rng(31)
+    rows, cols = np.nonzero(rng.random((40, 30)) < 0.2)
+    R = csr_from_coo(40, 30, rows, cols, rng.standard_normal(rows.size))
+    path = os.path.join(tmpdir, "rt.mtx")
+    write_matrix_market(path, R, comment="roundtrip\ncheck")
+    with open(path) as fh:
+        texts = dict(MM_TEXTS, roundtrip=fh.read())
+    for name, text in texts.items():
+        path = os.path.join(tmpdir, f"{name}.mtx")
+        with open(path, "w") as fh:
+            fh.write(text)
+        out[f"{name}_text"] = np.array(text)
+        try:
+            A, meta = load_matrix_market(path)
+            out[f"{name}_rp"] = A.row_ptr
+            out[f"{name}_ci"] = A.col_idx
+            out[f"{name}_v"] = A.values
+            out[f"{name}_shape"] = np.array(A.shape, dtype=np.int64)
+            out[f"{name}_sym"] = np.array(meta.symmetric)
+        except MatrixMarketError as e:
+            out[f"{name}_error_line"] = np.int64(-1 if e.line is None else e.line)
+            out[f"{name}_error"] = np.array(str(e).split(": ", 1)[-1])
+    return out
+
+
 def main():
     # --only PREFIX regenerates just the solve/trace cases whose name starts with it
     only = sys.argv[sys.argv.index("--only") + 1] if "--only" in sys.argv else None
     if only is None or only == "gp_":
         np.savez_compressed(os.path.join(HERE, "coeffs_gpbicg.npz"), **coeffs_gpbicg_fixture())
+    if only is None or only == "mmio":
+        import tempfile
+
+        with tempfile.TemporaryDirectory() as td:
+            np.savez_compressed(os.path.join(HERE, "mmio.npz"), **mmio_fixture(td))
     if only is None:
         np.savez_compressed(os.path.join(HERE, "kernels.npz"), **kernels_fixture())
         np.savez_compressed(os.path.join(HERE, "plans.npz"), **plans_fixture())
