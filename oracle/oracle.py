@@ -21,7 +21,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "liboracle.so")
 
 STATUS = {0: "converged", 1: "max_iters", 2: "breakdown", 3: "non_finite"}
-METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4}
+METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4,
+              "pbicgstab": 5}
 # coefficients.py:77, 80, 83, 102, 105
 BREAKDOWN_QUANTITIES = {
     1: "initial alpha denominator (r0*, s)",
@@ -37,12 +38,16 @@ BREAKDOWN_QUANTITIES = {
     10: "zeta denominator (At, At)",
     11: "zeta/eta denominator e*a - d^2",
     12: "beta denominator zeta",
+    # p-BiCGStab (pbsafe_oracle.c solve_pstab; not in the reference)
+    13: "alpha denominator (r0*, w) + beta*((r0*, s) - omega*(r0*, z))",
+    14: "omega denominator (y, y)",
 }
-SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap"}
+SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap", 10: "Az"}
 TRACE_NAMES = ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l", "r0s")
 # trace_hook dicts of the product-type methods (solvers.py:315, 448)
 TRACE_NAMES_BY_METHOD = {"bicgstab": ("x", "r", "p", "t", "Ap", "At"),
-                         "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z")}
+                         "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z"),
+                         "pbicgstab": ("x", "r", "p", "s", "z", "q", "y", "w", "t", "v")}
 
 
 class _Config(C.Structure):

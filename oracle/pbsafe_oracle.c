@@ -20,7 +20,12 @@
  *     the _Run bookkeeping (solvers.py:154-197) and the termination order;
  *   - the product-type comparators solve_bicgstab (solvers.py:210-327) and
  *     solve_gpbicg (solvers.py:330-460) with compute_zeta_eta_gpbicg
- *     (coefficients.py:109-135).
+ *     (coefficients.py:109-135);
+ *   - p-BiCGStab (Cools & Vanroose), which the reference does NOT ship: its
+ *     restatement here (solve_pstab) follows the published algorithm with the
+ *     reference BiCGStab's conventions and is pinned only through BiCGStab
+ *     equivalence in exact arithmetic (tests/test_oracle.py) — parity for it
+ *     is unpinned against reference outputs.
  *
  * Threads: rows of SpMV / vector updates are split across OpenMP threads
  * (element-wise, so bitwise neutral); the dot batch runs one thread per plan
@@ -225,7 +230,10 @@ enum {
   Q_BETA_F = 9,        /* "beta denominator (r0*, r)" */
   Q_GP_ZETA = 10,      /* "zeta denominator (At, At)" */
   Q_GP_ZETA_ETA = 11,  /* "zeta/eta denominator e*a - d^2" */
-  Q_GP_BETA_ZETA = 12  /* "beta denominator zeta" */
+  Q_GP_BETA_ZETA = 12, /* "beta denominator zeta" */
+  /* p-BiCGStab (not in the reference; see solve_pstab) */
+  Q_PSTAB_ALPHA = 13,  /* "alpha denominator (r0*, w) + beta*((r0*, s) - omega*(r0*, z))" */
+  Q_PSTAB_OMEGA = 14   /* "omega denominator (y, y)" */
 };
 
 /* coefficients.py:35-39 guard_denominator: returns nonzero on breakdown */
@@ -305,10 +313,10 @@ OR_API int or_zeta_eta_gpbicg(double a, double b, double c, double d, double e, 
 /* ------------------------------------------------------------------ solver */
 
 enum { ST_CONVERGED = 0, ST_MAX_ITERS = 1, ST_BREAKDOWN = 2, ST_NON_FINITE = 3 };
-enum { M_PBICGSAFE = 0, M_PBICGSAFE_RR = 1, M_SSBICGSAFE2 = 2, M_BICGSTAB = 3, M_GPBICG = 4 };
+enum { M_PBICGSAFE = 0, M_PBICGSAFE_RR = 1, M_SSBICGSAFE2 = 2, M_BICGSTAB = 3, M_GPBICG = 4, M_PBICGSTAB = 5 };
 
 /* SpMV tags for the NonFiniteVectorError message (reduction.py:330, 451) */
-enum { T_NONE = 0, T_AX = 1, T_AR = 2, T_AS = 3, T_AW = 4, T_AO = 5, T_AU = 6, T_AT = 7, T_AY = 8, T_AP = 9 };
+enum { T_NONE = 0, T_AX = 1, T_AR = 2, T_AS = 3, T_AW = 4, T_AO = 5, T_AU = 6, T_AT = 7, T_AY = 8, T_AP = 9, T_AZ = 10 };
 
 typedef struct {
   double tol;
@@ -548,6 +556,153 @@ done:
   return rc;
 }
 
+/* p-BiCGStab: the pipelined BiCGStab of Cools & Vanroose (2017), the
+ * comparator the paper cites for Table 3 (its algorithm
+ * is NOT in the reference).  It maintains w = A r, s = A p,
+ * z = A s, t = A w, v = A z, q = r - alpha s, y = w - alpha z (= A q) by
+ * recurrences, so each of its two reduction phases is followed by an
+ * independent product it can overlap: (q,y) (y,y) with v = A z, and the
+ * five dots of the next alpha / beta / convergence check with t = A w.
+ * Conventions follow the reference's solve_bicgstab (solvers.py:210-327):
+ * shadow residual r0* = r0, f = (r0*, r), check order (record, non-finite,
+ * converged, then guards), the t = 0 omega rule, the rr == 0 beta rule, the
+ * BiCGStab breakdown guards (coefficients.py:35-39) and the coefficient
+ * record (alpha, beta, omega).  The alpha denominator is (r0*, A p) by its
+ * recurrence: (r0*, w) + beta*((r0*, s) - omega*(r0*, z)).
+ *
+ *   setup   r = b - A x0; r0* = r; w = A r; rr = (r, r), gw = (r0*, w)
+ *   loop i  check i; alpha = f / (gw + beta*(sd - omega*zd)); t = A w
+ *           p = r + beta*(p - omega s); s = w + beta*(s - omega z)
+ *           z = t + beta*(z - omega v); q = r - alpha s; y = w - alpha z
+ *           [b = (q, y), e = (y, y), d = (q, q)]  v = A z
+ *           omega = b / e (0 when e = d = 0)
+ *           x = x + alpha p + omega q; r = q - omega y; w = y - omega (t - alpha v)
+ *           [f' = (r0*, r), rr = (r, r), gw = (r0*, w), sd = (r0*, s), zd = (r0*, z)]
+ *           beta = (alpha / omega) (f' / f) (0 when rr = 0); record (alpha, beta, omega)
+ *
+ * trace vecs: x r p s z q y w t v; scalars alpha beta omega 0 f rr. */
+static int solve_pstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                       const double* b, const double* x0, const or_config* cfg, double* x_out,
+                       double* hist_rel, uint8_t* hist_replaced, double* hist_coef,
+                       uint8_t* hist_has_coef, or_result* res, or_trace_fn trace, void* user) {
+  mat_t A = {n, rp, ci, v, res};
+  or_plan P;
+  int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;
+  P.bounds = (int64_t*)malloc(sizeof(int64_t) * (size_t)(wk + 2));
+  P.workers = or_plan_balanced(n, wk, P.bounds);
+  P.compensated = cfg->workers < 0;
+  hist_t H = {hist_rel, hist_replaced, hist_coef, hist_has_coef, 0};
+  double* buf = (double*)calloc((size_t)12 * (size_t)(n > 0 ? n : 1), sizeof(double));
+  int idx = 0;
+  VEC(x); VEC(r); VEC(r0s); VEC(p); VEC(s); VEC(z); VEC(q); VEC(y); VEC(w); VEC(t); VEC(av);
+  VEC(tmp);
+  if (x0) memcpy(x, x0, sizeof(double) * (size_t)n);
+  int rc = 0;
+  int64_t iterations = 0;
+  double r0_norm = 0.0;
+  if (spmv_checked(&A, x, tmp, T_AX)) { rc = 1; goto done; }
+  or_lincomb2(n, r, 1.0, b, -1.0, tmp); /* r0 = b - A x0 */
+  memcpy(r0s, r, sizeof(double) * (size_t)n);
+  if (spmv_checked(&A, r, w, T_AR)) { rc = 1; goto done; } /* w0 = A r0 */
+  double rr, gw;
+  {
+    const double* xs[2] = {r, r0s};
+    const double* ys[2] = {r, w};
+    double d2[2];
+    plan_batch(&P, 2, xs, ys, d2);
+    rr = d2[0];
+    gw = d2[1];
+  }
+  double f = rr; /* (r0*, r0) = ||r0||^2 */
+  r0_norm = sqrt(rr);
+  double alpha = 0.0, beta = 0.0, omega = 0.0, sd = 0.0, zd = 0.0;
+  for (int64_t i = 0; i < cfg->max_iters; ++i) {
+    double rel = rel_of(r0_norm, rr);
+    record(&H, i, rel, 0);
+    if (!isfinite(rel)) { res->status = ST_NON_FINITE; res->failure_iter = i; iterations = i; goto finish; }
+    if (rel <= cfg->tol) { res->status = ST_CONVERGED; iterations = i; goto finish; }
+    int q_bd = Q_NONE;
+    {
+      const double bt = beta * (sd - omega * zd);
+      const double den = gw + bt;
+      if (guard(den, fabs(gw) + fabs(bt))) { q_bd = Q_PSTAB_ALPHA; goto broke; }
+      alpha = f / den;
+    }
+    if (spmv_checked(&A, w, t, T_AW)) { rc = 1; goto done; } /* t = A w */
+    or_add_scaled_damped_diff(n, p, r, beta, p, omega, s);   /* p = r + beta*(p - omega*s) */
+    or_add_scaled_damped_diff(n, s, w, beta, s, omega, z);   /* s = w + beta*(s - omega*z) */
+    or_add_scaled_damped_diff(n, z, t, beta, z, omega, av);  /* z = t + beta*(z - omega*v) */
+    or_lincomb2(n, q, 1.0, r, -alpha, s);                    /* q = r - alpha*s */
+    or_lincomb2(n, y, 1.0, w, -alpha, z);                    /* y = w - alpha*z */
+    double d3[3]; /* b e d */
+    {
+      const double* xs[3] = {q, y, q};
+      const double* ys[3] = {y, y, q};
+      plan_batch(&P, 3, xs, ys, d3);
+    }
+    if (spmv_checked(&A, z, av, T_AZ)) { rc = 1; goto done; } /* v = A z */
+    if (d3[1] == 0.0 && d3[2] == 0.0) {
+      omega = 0.0; /* q = 0: the alpha half-step already landed */
+    } else {
+      if (guard(d3[1], fabs(d3[1]))) { q_bd = Q_PSTAB_OMEGA; goto broke; }
+      omega = d3[0] / d3[1];
+    }
+    or_lincomb3(n, x, 1.0, x, alpha, p, omega, q);           /* x = x + alpha*p + omega*q */
+    or_lincomb2(n, r, 1.0, q, -omega, y);                    /* r = q - omega*y */
+    or_add_scaled_damped_diff(n, w, y, -omega, t, alpha, av); /* w = y - omega*(t - alpha*v) */
+    double d5[5]; /* f' rr gw sd zd */
+    {
+      const double* xs[5] = {r0s, r, r0s, r0s, r0s};
+      const double* ys[5] = {r, r, w, s, z};
+      plan_batch(&P, 5, xs, ys, d5);
+    }
+    rr = d5[1];
+    if (rr == 0.0) {
+      beta = 0.0;
+    } else {
+      if (guard(omega, fabs(omega))) { q_bd = Q_STAB_BETA_OMEGA; goto broke; }
+      if (guard(f, fabs(f))) { q_bd = Q_BETA_F; goto broke; }
+      beta = (alpha / omega) * (d5[0] / f);
+    }
+    f = d5[0];
+    gw = d5[2];
+    sd = d5[3];
+    zd = d5[4];
+    set_coef(&H, alpha, beta, omega, NAN);
+    if (!(isfinite(alpha) && isfinite(beta) && isfinite(omega))) {
+      res->status = ST_NON_FINITE; res->failure_iter = i; iterations = i; goto finish;
+    }
+    if (trace) {
+      double* vecs[10] = {x, r, p, s, z, q, y, w, t, av};
+      double sc[14] = {alpha, beta, omega, 0.0, f, rr};
+      trace(i, vecs, sc, user);
+    }
+    iterations = i + 1;
+    continue;
+  broke:
+    res->status = ST_BREAKDOWN;
+    res->breakdown = q_bd;
+    res->failure_iter = i;
+    iterations = i;
+    goto finish;
+  }
+  {
+    double rel = rel_of(r0_norm, rr);
+    record(&H, cfg->max_iters, rel, 0);
+    res->status = rel <= cfg->tol ? ST_CONVERGED : ST_MAX_ITERS;
+    iterations = cfg->max_iters;
+  }
+finish:
+  res->iterations = iterations;
+  res->r0_norm = r0_norm;
+  res->n_records = H.count;
+  memcpy(x_out, x, sizeof(double) * (size_t)n);
+done:
+  free(buf);
+  free(P.bounds);
+  return rc;
+}
+
 /* solvers.py:595-739 (_solve_pipelined) and solvers.py:485-592 (ssBiCGSafe2).
  * Returns 0, or 1 when a NonFiniteVectorError would have been raised. */
 OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
@@ -563,6 +718,9 @@ OR_API int or_solve(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   if (cfg->method == M_BICGSTAB || cfg->method == M_GPBICG)
     return solve_product(n, rp, ci, v, b, x0, cfg, x_out, hist_rel, hist_replaced, hist_coef,
                          hist_has_coef, res, trace, user);
+  if (cfg->method == M_PBICGSTAB)
+    return solve_pstab(n, rp, ci, v, b, x0, cfg, x_out, hist_rel, hist_replaced, hist_coef,
+                       hist_has_coef, res, trace, user);
   mat_t A = {n, rp, ci, v, res};
   or_plan P;
   int32_t wk = cfg->workers < 0 ? 1 : cfg->workers;

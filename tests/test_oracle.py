@@ -131,3 +131,69 @@ def test_threads_do_not_change_bits():
             for t in (1, 3, 8)]
     for o in outs:
         assert np.array_equal(o["rel"], g["rel"]) and np.array_equal(o["x"], g["x"])
+
+
+# -- p-BiCGStab (pbsafe_oracle.c solve_pstab) -----------------------------------
+# The reference does not ship p-BiCGStab, so its restatement
+# cannot be pinned bitwise.  It is pinned instead by what the algorithm
+# guarantees: in exact arithmetic p-BiCGStab produces BiCGStab's iterates
+# (Cools & Vanroose), so against the reference's own BiCGStab fixtures the
+# early history must agree to rounding, the iteration count closely, and the
+# auxiliary vectors must satisfy their defining products.
+
+_BS_CASES = [n for n in gc.case_names() if n.startswith("bs_")]
+
+
+@pytest.mark.parametrize("name", _BS_CASES)
+def test_pbicgstab_tracks_reference_bicgstab(name):
+    spec, A, b, x0, g = gc.load_case(name, orc.spmv)
+    out = orc.solve(A.row_ptr, A.col_idx, A.values, b, x0=x0, method="pbicgstab", tol=spec["tol"],
+                    max_iters=spec["max_iters"], workers=spec["workers"])
+    assert out["status"] == str(g["status"])
+    it_ref = int(g["iterations"])
+    # the reference's own BiCGStab count moves by 4% with the reduction order
+    # alone (bs_c1: 166 at W = 1, 173 at W = 3), so allow twice that
+    assert abs(out["iterations"] - it_ref) <= max(3, 0.08 * it_ref), (out["iterations"], it_ref)
+    assert out["r0_norm"] == float(g["r0_norm"])
+    k = min(10, len(out["rel"]), len(g["rel"]))
+    ref = g["rel"][:k]
+    assert np.all(np.abs(out["rel"][:k] - ref) <= 1e-6 * np.maximum(np.abs(ref), 1e-300) + 1e-300), name
+    # coefficients (alpha, beta, omega) of the first iterations
+    kc = min(5, int(out["has_coef"].sum()), int(g["has_coef"].sum()))
+    if kc:
+        np.testing.assert_allclose(out["coef"][:kc, :3], g["coef"][:kc, :3], rtol=1e-6)
+    if out["status"] == "converged" and np.linalg.norm(g["x"]) > 0:
+        assert np.linalg.norm(out["x"] - g["x"]) <= 1e-6 * np.linalg.norm(g["x"])
+    if out["status"] == "breakdown":
+        assert out["failure_iter"] == int(g["failure_iter"])
+        assert out["breakdown"] == "alpha denominator (r0*, w) + beta*((r0*, s) - omega*(r0*, z))"
+
+
+def test_pbicgstab_auxiliary_identities():
+    """w = A r, s = A p, z = A s, y = A q, v = A z, t = A w_prev hold along
+    the recurrences (cf. the reference's p-BiCGSafe identity test,
+    test_solvers.py:142-158)."""
+    spec, A, b, x0, g = gc.load_case("bs_c1", orc.spmv)
+    rp, ci, v = A.row_ptr, A.col_idx, A.values
+    seen = {}
+    orc.solve(rp, ci, v, b, method="pbicgstab", tol=1e-10, max_iters=25,
+              trace=lambda i, d, s: seen.__setitem__(i, d))
+    assert sorted(seen) == list(range(25))
+    Ax = lambda a: orc.spmv(rp, ci, v, a)
+    anorm = np.abs(v).sum() / A.n_rows * 10
+    for i, d in seen.items():
+        for lhs, rhs in (("w", "r"), ("s", "p"), ("z", "s"), ("y", "q"), ("v", "z")):
+            ref = Ax(d[rhs])
+            err = np.linalg.norm(d[lhs] - ref) / max(np.linalg.norm(ref), anorm * np.linalg.norm(d[rhs]), 1e-300)
+            assert err < 1e-8, (i, lhs, rhs, err)
+        if i > 0:
+            ref = Ax(seen[i - 1]["w"])
+            assert np.linalg.norm(d["t"] - ref) <= 1e-8 * max(np.linalg.norm(ref), 1e-300), i
+
+
+def test_pbicgstab_counts_two_products_per_iteration():
+    spec, A, b, x0, g = gc.load_case("bs_maxiters5", orc.spmv)
+    out = orc.solve(A.row_ptr, A.col_idx, A.values, b, method="pbicgstab", tol=spec["tol"],
+                    max_iters=spec["max_iters"])
+    assert out["status"] == "max_iters" and out["iterations"] == 5
+    assert len(out["rel"]) == 6 and out["n_spmv"] == 2 + 2 * 5
