@@ -297,16 +297,17 @@ def run_ours(args):
     comparators = None
     if dsys is None:
         comparators = {}
-        for mname in ("pbicgsafe", "ssbicgsafe2", "bicgstab", "gpbicg"):
+        for mname in ("pbicgsafe", "ssbicgsafe2", "pbicgstab", "bicgstab", "gpbicg"):
             solve_dev(method=mname, max_iters=4000)  # warm (graph capture)
             rr_ = solve_dev(method=mname, max_iters=4000)
             comparators[mname] = {"status": {0: "converged", 1: "max_iters", 2: "breakdown",
                                              3: "non_finite"}[rr_.status],
                                   "iterations": int(rr_.iterations), "time_to_tol_ms": rr_.device_ms,
                                   "it_per_s": rr_.iterations / (rr_.device_ms * 1e-3)}
-        comparators["note"] = ("one device solve each to 1e-10, CSR resident; bicgstab is the reference's "
-                               "two-reduction BiCGStab (solvers.py:210-327), the BiCGStab comparator the "
-                               "reference ships (a pipelined p-BiCGStab is not in it)")
+        comparators["note"] = ("one device solve each to 1e-10, CSR resident; pbicgstab is the pipelined "
+                               "BiCGStab of Cools & Vanroose BASELINE names (not in the reference; restated in "
+                               "oracle/pbsafe_oracle.c solve_pstab, parity unpinned against reference outputs); "
+                               "bicgstab is the reference's two-reduction BiCGStab (solvers.py:210-327)")
 
     # e2e through the public API, pinned host buffers, upload + solve + readback per step
     e2e = None

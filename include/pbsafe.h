@@ -59,6 +59,8 @@ extern "C" {
 #define PBS_METHOD_SSBICGSAFE2 2
 #define PBS_METHOD_BICGSTAB 3  /* two reduction phases (solvers.py:210-327) */
 #define PBS_METHOD_GPBICG 4    /* three reduction phases (solvers.py:330-460) */
+#define PBS_METHOD_PBICGSTAB 5 /* pipelined BiCGStab (Cools & Vanroose; not in the reference,
+                                  restated in oracle/pbsafe_oracle.c solve_pstab) */
 
 /* SolveStatus (solvers.py:44-48) */
 #define PBS_CONVERGED 0
@@ -81,6 +83,8 @@ extern "C" {
 #define PBS_BD_GP_ZETA 10      /* "zeta denominator (At, At)" */
 #define PBS_BD_GP_ZETA_ETA 11  /* "zeta/eta denominator e*a - d^2" */
 #define PBS_BD_GP_BETA 12      /* "beta denominator zeta" */
+#define PBS_BD_PSTAB_ALPHA 13  /* "alpha denominator (r0*, w) + beta*((r0*, s) - omega*(r0*, z))" */
+#define PBS_BD_PSTAB_OMEGA 14  /* "omega denominator (y, y)" */
 
 /* SpMV tags of NonFiniteVectorError messages (reduction.py:330, 451) */
 #define PBS_TAG_AX 1
@@ -92,6 +96,7 @@ extern "C" {
 #define PBS_TAG_AT 7
 #define PBS_TAG_AY 8
 #define PBS_TAG_AP 9
+#define PBS_TAG_AZ 10 /* p-BiCGStab v = A z */
 
 /* reduction orders for the per-iteration dot batch */
 #define PBS_REDUCE_TREE 0 /* fixed-shape block tree: deterministic, full speed */

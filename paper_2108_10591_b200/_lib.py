@@ -21,14 +21,15 @@ PBS_ERR_NOMEM = -4
 PBS_ERR_NCCL = -5
 PBS_ERR_UNSUPPORTED = -6
 
-METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4}
+METHOD_IDS = {"pbicgsafe": 0, "pbicgsafe-rr": 1, "ssbicgsafe2": 2, "bicgstab": 3, "gpbicg": 4,
+              "pbicgstab": 5}
 REDUCE_TREE, REDUCE_PLAN = 0, 1
 HIST_REPLACED, HIST_HAS_COEF = 1, 2
 NUM_KERNEL_KINDS = 8
 KERNEL_KINDS = ("K1_As", "K2_update", "K3_Aw_epilogue", "F_finalize", "R_rr_update",
                 "RS_rr_spmv", "S_setup", "D_plan_dots")
 # reduction.py:330/451 tags of the NonFiniteVectorError message
-SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap"}
+SPMV_TAGS = {1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay", 9: "Ap", 10: "Az"}
 
 EXPORTS = (
     "pbs_init", "pbs_destroy", "pbs_last_error", "pbs_device_info", "pbs_set_stream",

@@ -30,6 +30,9 @@ BREAKDOWN_QUANTITIES = {
     10: "zeta denominator (At, At)",
     11: "zeta/eta denominator e*a - d^2",
     12: "beta denominator zeta",
+    # p-BiCGStab (not in the reference; oracle/pbsafe_oracle.c solve_pstab)
+    13: "alpha denominator (r0*, w) + beta*((r0*, s) - omega*(r0*, z))",
+    14: "omega denominator (y, y)",
 }
 
 

@@ -42,6 +42,11 @@ constexpr unsigned kDotsStabB = (1u << DB) | (1u << DE) | (1u << DC) | (1u << DD
 constexpr unsigned kDotsGpB = (1u << DA) | (1u << DB) | (1u << DC) | (1u << DD) | (1u << DE);
 constexpr unsigned kDotsGpC = (1u << DF) | (1u << DR);
 constexpr unsigned kDotsRR = 1u << DR;
+// p-BiCGStab (oracle solve_pstab): setup rr=(r,r) g=(r0*,w); omega phase
+// b=(q,y) e=(y,y) d=(q,q); beta phase f=(r0*,r) r=(r,r) g=(r0*,w) a=(r0*,s) h=(r0*,z)
+constexpr unsigned kDotsPsW = (1u << DR) | (1u << DG);
+constexpr unsigned kDotsPsA = (1u << DB) | (1u << DE) | (1u << DD);
+constexpr unsigned kDotsPsB = (1u << DF) | (1u << DR) | (1u << DG) | (1u << DA) | (1u << DH);
 
 // Host-visible mirror, written by the finalize kernel through mapped pinned
 // memory so the host can stop launching without a device sync.

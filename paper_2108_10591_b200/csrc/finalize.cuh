@@ -217,6 +217,12 @@ enum Phase {
   kPhGpBeta,
   kPhGpBetaNC,
   kPhProdCheck,
+  // p-BiCGStab (oracle solve_pstab)
+  kPhPsSetup,   // rr, g -> r0_norm, f, check 0, alpha 0
+  kPhPsOmega,   // b e d after t = A w and the p s z q y update -> omega
+  kPhPsBeta,    // f r g a h after v = A z and the x r w update -> beta, record,
+  kPhPsBetaNC,  //   check i+1, alpha i+1 ("NC": leave the check to kPhPsCheck)
+  kPhPsCheck,
 };
 
 __device__ __forceinline__ void prod_stop(SolverState* ss, int status, long long iters, long long fail, int stage) {
@@ -284,6 +290,23 @@ __device__ int zeta_eta_gpbicg(double a, double b, double c, double d, double e,
   *zeta = sub(mul(a, b), mul(c, d)) / det;
   *eta = sub(mul(e, c), mul(d, b)) / det;
   return PBS_BD_NONE;
+}
+
+// p-BiCGStab's alpha for the iteration whose loop-top check just passed
+// (ss->iter == i + 1): f / ((r0*, w) + beta*((r0*, s) - omega*(r0*, z))),
+// the recurrence for (r0*, A p), with beta and omega of iteration i - 1
+__device__ void ps_alpha(SolverState* ss) {
+  if (!ss->run_all) return;
+  const long long i = ss->iter - 1;
+  const double gw = ss->dots[DG], sd = ss->dots[DA], zd = ss->dots[DH];
+  const double bt = mul(ss->beta, sub(sd, mul(ss->omega, zd)));
+  const double den = add(gw, bt);
+  if (guard(den, add(fabs(gw), fabs(bt)))) {
+    ss->breakdown = PBS_BD_PSTAB_ALPHA;
+    prod_stop(ss, PBS_BREAKDOWN, i, i, 1);
+    return;
+  }
+  ss->alpha = ss->f_prev / den;
 }
 
 // One phase on the shared state copy (thread 0).  i = the iteration whose
@@ -377,6 +400,62 @@ __device__ void prod_phase(SolverState* ss, int phase, const double* d) {
     }
     case kPhProdCheck:
       prod_check(ss, i + 1);
+      return;
+    case kPhPsSetup: {
+      const double rr = d[DR];
+      ss->r0_norm = sqrt(rr);
+      ss->f_prev = rr;
+      ss->rr = rr;
+      ss->dots[DG] = d[DG];
+      ss->dots[DA] = 0.0;
+      ss->dots[DH] = 0.0;
+      ss->alpha = ss->beta = ss->omega = 0.0;
+      prod_check(ss, 0);
+      ps_alpha(ss);
+      return;
+    }
+    case kPhPsOmega: {
+      const double b = d[DB], e = d[DE], dd = d[DD];
+      ss->dots[DB] = b;
+      ss->dots[DE] = e;
+      ss->dots[DD] = dd;
+      if (e == 0.0 && dd == 0.0) {
+        ss->omega = 0.0;  // q = 0: the alpha half-step already landed
+      } else {
+        if (guard(e, fabs(e))) return brk(PBS_BD_PSTAB_OMEGA, 2);
+        ss->omega = b / e;
+      }
+      return;
+    }
+    case kPhPsBeta:
+    case kPhPsBetaNC: {
+      const double fn = d[DF], rr = d[DR], f = ss->f_prev, alpha = ss->alpha, omega = ss->omega;
+      ss->rr = rr;
+      double beta;
+      if (rr == 0.0) {
+        beta = 0.0;
+      } else {
+        if (guard(omega, fabs(omega))) return brk(PBS_BD_STAB_BETA, 3);
+        if (guard(f, fabs(f))) return brk(PBS_BD_BETA_F, 3);
+        beta = mul(alpha / omega, fn / f);
+      }
+      ss->f_prev = fn;
+      ss->beta = beta;
+      ss->dots[DF] = fn;
+      ss->dots[DR] = rr;
+      ss->dots[DG] = d[DG];
+      ss->dots[DA] = d[DA];
+      ss->dots[DH] = d[DH];
+      if (!prod_record_coef(ss, i, alpha, beta, omega, __longlong_as_double(0x7ff8000000000000LL), false)) return;
+      if (phase == kPhPsBeta) {
+        prod_check(ss, i + 1);
+        ps_alpha(ss);
+      }
+      return;
+    }
+    case kPhPsCheck:
+      prod_check(ss, i + 1);
+      ps_alpha(ss);
       return;
   }
 }

@@ -382,6 +382,7 @@ void Launcher::trace_point() {
   static const int safe_order[13] = {VX, VR, VP, VU, VO, VT, VW, VY, VZ, VS, VQ, VG, VL};
   static const int stab_order[6] = {VX, VR, VP, VT, VAP, VAT};
   static const int gp_order[8] = {VX, VR, VP, VU, VT, VW, VY, VZ};
+  static const int ps_order[10] = {VX, VR, VP, VS, VZ, VQ, VY, VW, VT, VO};
   const int* order = safe_order;
   int nv = 13;
   if (trace_method == PBS_METHOD_BICGSTAB) {
@@ -390,6 +391,9 @@ void Launcher::trace_point() {
   } else if (trace_method == PBS_METHOD_GPBICG) {
     order = gp_order;
     nv = 8;
+  } else if (trace_method == PBS_METHOD_PBICGSTAB) {
+    order = ps_order;
+    nv = 10;
   }
   double* ptrs[13];
   for (int k = 0; k < nv; ++k) {
@@ -1125,6 +1129,101 @@ static void iter_gp(Launcher& L, Workspace* ws, const Mode& md) {
   }
 }
 
+// ---- p-BiCGStab (oracle solve_pstab).  Two SpMV kernels per iteration,
+// each carrying one reduction phase in its tail:
+//   t = A w  + p s z q y + b e d   [omega]
+//   v = A z  + x r w + f r g a h   [beta, record, check i+1, alpha i+1]
+// v (A z) lives in the o slot.  On several GPUs each phase's reduction would
+// overlap the next SpMV, which is the method's point; on one GPU the two
+// kernels simply stream.
+
+static EpiPsW epi_ps_w(Workspace* ws, const Mode& md) {
+  EpiPsW e{};
+  auto& V = ws->V.v;
+  e.w = V[VW];
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, 1, 0);
+  e.sink.phase = kPhPsSetup;
+  e.in[0] = V[VR];
+  e.in[1] = V[VR0S];
+  return e;
+}
+
+static EpiPsA epi_ps_a(Workspace* ws, const Mode& md) {
+  EpiPsA e{};
+  auto& V = ws->V.v;
+  e.t = V[VT];
+  e.p = V[VP];
+  e.s = V[VS];
+  e.z = V[VZ];
+  e.q = V[VQ];
+  e.y = V[VY];
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, 1, 0);
+  e.sink.phase = kPhPsOmega;
+  const int in[6] = {VR, VP, VS, VW, VZ, VO};
+  for (int k = 0; k < 6; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+static EpiPsB epi_ps_b(Workspace* ws, const Mode& md, int phase) {
+  EpiPsB e{};
+  auto& V = ws->V.v;
+  e.v = V[VO];
+  e.x = V[VX];
+  e.r = V[VR];
+  e.w = V[VW];
+  e.st = ws->st;
+  e.sink = sink_for(ws, md, 1, 0);
+  e.sink.phase = phase;
+  const int in[8] = {VX, VP, VQ, VY, VT, VR0S, VS, VZ};
+  for (int k = 0; k < 8; ++k) e.in[k] = V[in[k]];
+  return e;
+}
+
+static void setup_pstab(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  spmv_launch(L, ws->X.v[VX], epi_resid(ws, true), 0, ws->n, KS);  // r0 = b - A x0 ; r0* = r0
+  spmv_launch(L, ws->X.v[VR], epi_ps_w(ws, md), 0, ws->n, KS);      // w0 = A r0 + rr, g
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DR] = V[VR], y[DR] = V[VR];
+    x[DG] = V[VR0S], y[DG] = V[VW];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsPsW, x, y)), 1, 0, 0, kPhPsSetup);
+  }
+}
+
+static void iter_pstab(Launcher& L, Workspace* ws, const Mode& md) {
+  auto& V = ws->V.v;
+  const bool tracing = L.trace_cfg != nullptr;
+  spmv_launch(L, ws->X.v[VW], epi_ps_a(ws, md), 0, ws->n, KK1);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DB] = V[VQ], y[DB] = V[VY];
+    x[DE] = V[VY], y[DE] = V[VY];
+    x[DD] = V[VQ], y[DD] = V[VQ];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsPsA, x, y)), 1, 0, 0, kPhPsOmega);
+  }
+  const int ph = tracing ? kPhPsBetaNC : kPhPsBeta;
+  spmv_launch(L, ws->X.v[VZ], epi_ps_b(ws, md, ph), 0, ws->n, KK3);
+  if (md.plan) {
+    const double* x[kNumDots] = {};
+    const double* y[kNumDots] = {};
+    x[DF] = V[VR0S], y[DF] = V[VR];
+    x[DR] = V[VR], y[DR] = V[VR];
+    x[DG] = V[VR0S], y[DG] = V[VW];
+    x[DA] = V[VR0S], y[DA] = V[VS];
+    x[DH] = V[VR0S], y[DH] = V[VZ];
+    finalize(L, ws, plan_pairs(L, ws, pairs_of(kDotsPsB, x, y)), 1, 0, 0, ph);
+  }
+  if (tracing) {
+    L.trace_point();
+    finalize(L, ws, 0, 1, 0, 0, kPhPsCheck);
+  }
+}
+
 typedef void (*IterFn)(Launcher&, Workspace*, const Mode&);
 
 // steady iterations per graph (PBS_GRAPH_ITERS, default 4): inside one graph
@@ -1142,6 +1241,9 @@ static void iter_stab_batch(Launcher& L, Workspace* ws, const Mode& md) {
 }
 static void iter_gp_batch(Launcher& L, Workspace* ws, const Mode& md) {
   for (int k = 0; k < graph_iters(); ++k) iter_gp(L, ws, md);
+}
+static void iter_pstab_batch(Launcher& L, Workspace* ws, const Mode& md) {
+  for (int k = 0; k < graph_iters(); ++k) iter_pstab(L, ws, md);
 }
 
 static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const Mode& md,
@@ -1330,6 +1432,10 @@ static int collect_result(pbs_mat* m, int method, const pbs_config* cfg, pbs_res
     // r0 = b - A x0, then Ap and At per completed iteration; a stopping
     // iteration that got past its loop-top check ran Ap (alpha stage) or both
     res->n_spmv = 1 + 2 * completed + (out.stop_stage == 0 ? 0 : (out.stop_stage == 1 ? 1 : 2));
+  else if (method == PBS_METHOD_PBICGSTAB)
+    // r0 = b - A x0 and w0 = A r0, then t = A w and v = A z per completed
+    // iteration; a stopping iteration past its alpha ran both
+    res->n_spmv = 2 + 2 * completed + (out.stop_stage >= 2 ? 2 : 0);
   else if (pipelined)
     res->n_spmv = 2 + reached + completed + 5 * nrep;
   else
@@ -1350,7 +1456,8 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   const bool tracing = cfg->trace_fn != nullptr;
   md.store_temps = tracing ? 1 : 0;
   md.method = method;
-  const bool product = method == PBS_METHOD_BICGSTAB || method == PBS_METHOD_GPBICG;
+  const bool product = method == PBS_METHOD_BICGSTAB || method == PBS_METHOD_GPBICG ||
+                       method == PBS_METHOD_PBICGSTAB;
   if (md.plan) {
     int rc = ensure_plan(m, cfg->plan_workers);
     if (rc) return rc;
@@ -1381,6 +1488,10 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   // zero-initialised workspace (solvers.py:621-628; 251-253, 371-376)
   const int zero_slots[] = {VP, VU, VT, VY, VZ, VG, VL, VW, VAP, VAT};
   for (int k : zero_slots) CK(cudaMemsetAsync(ws->V.v[k], 0, sizeof(double) * n, s));
+  if (method == PBS_METHOD_PBICGSTAB) {  // s and v (o slot) start at zero too
+    CK(cudaMemsetAsync(ws->V.v[VS], 0, sizeof(double) * n, s));
+    CK(cudaMemsetAsync(ws->V.v[VO], 0, sizeof(double) * n, s));
+  }
 
   std::vector<std::pair<int, cudaEvent_t>> marks;
   ctx->events.reset();
@@ -1402,6 +1513,9 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
   if (L.timing) marks.push_back({-1, ws->ev0});
   if (pipelined) {
     setup_pipelined(L, ws, md);
+    if (L.err) return L.err;
+  } else if (method == PBS_METHOD_PBICGSTAB) {
+    setup_pstab(L, ws, md);
     if (L.err) return L.err;
   } else if (product) {
     setup_prod(L, ws, md);
@@ -1437,10 +1551,12 @@ static int run_solve(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* 
       const bool replace = is_replace(j);
       IterFn fn = method == PBS_METHOD_BICGSTAB ? iter_stab
                   : method == PBS_METHOD_GPBICG ? iter_gp
+                  : method == PBS_METHOD_PBICGSTAB ? iter_pstab
                   : !pipelined ? iter_ss
                   : (replace ? iter_replace : iter_steady);
       IterFn bfn = method == PBS_METHOD_BICGSTAB ? iter_stab_batch
                    : method == PBS_METHOD_GPBICG ? iter_gp_batch
+                   : method == PBS_METHOD_PBICGSTAB ? iter_pstab_batch
                    : iter_steady_batch;
       const int gu = graph_iters();
       bool batch = graphs && (pipelined || product) && gu > 1 && j + gu <= cfg->max_iters;
@@ -2218,7 +2334,7 @@ static int solve_common(pbs_mat* m, int32_t method, const pbs_config* cfg) {
   pbs_ctx* ctx = m ? m->ctx : nullptr;
   if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
   if (!m->part.dist && m->n_rows != m->n_cols) return set_err(ctx, PBS_ERR_INVALID, "solver needs a square operator");
-  if (method < 0 || method > PBS_METHOD_GPBICG) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
+  if (method < 0 || method > PBS_METHOD_PBICGSTAB) return set_err(ctx, PBS_ERR_INVALID, "unknown method");
   int rc = validate_cfg(ctx, cfg);
   if (rc) return rc;
   CK(cudaSetDevice(ctx->device));

@@ -463,6 +463,124 @@ struct EpiProdBT {
 using EpiStabB = EpiProdBT<false>;
 using EpiGpB = EpiProdBT<true>;
 
+// ---- p-BiCGStab (oracle solve_pstab; Cools & Vanroose's pipelined BiCGStab)
+
+// setup: w = A r (tag "Ar"), then the partials of rr = (r, r), g = (r0*, w)
+struct EpiPsW {
+  static constexpr int kIn = 2;
+  static constexpr int kInStaged = kIn;
+  static constexpr int kWcBatch = 4;
+  static constexpr int kMinBlocks = 1;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 8;
+  double* w;
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // r r0s
+  DotsT<kDotsPsW> d;
+  __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() { d.zero(); }
+  __device__ void row(long long i, double wv, const double* v) {
+    w[i] = wv;
+    if (!isfinite(wv)) report_nonfinite(st, PBS_TAG_AR, i);
+    if (!sink.partials) return;
+    d.step(DR, v[0], v[0]);
+    d.step(DG, v[1], wv);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+
+// t = A w (tag "Aw") fused with the row-local p s z q y update and the omega
+// phase's partials b = (q, y), e = (y, y), d = (q, q)
+struct EpiPsA {
+  static constexpr int kIn = 6;
+  static constexpr int kInStaged = kIn;
+  static constexpr int kWcBatch = 2;  // dot-carrying: register-bound
+  static constexpr int kMinBlocks = 1;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 8;
+  double *t, *p, *s, *z, *q, *y;
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // r p s w z v
+  double alpha, beta, omega;
+  DotsT<kDotsPsA> d;
+  __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() {
+    d.zero();
+    alpha = st->alpha;
+    beta = st->beta;
+    omega = st->omega;
+  }
+  __device__ void row(long long i, double tv, const double* v) {
+    t[i] = tv;
+    if (!isfinite(tv)) report_nonfinite(st, PBS_TAG_AW, i);
+    const double rv = v[0], wv = v[3];
+    const double pn = asdd(rv, beta, v[1], omega, v[2]);  // p = r + beta*(p - omega*s)
+    const double sn = asdd(wv, beta, v[2], omega, v[4]);  // s = w + beta*(s - omega*z)
+    const double zn = asdd(tv, beta, v[4], omega, v[5]);  // z = t + beta*(z - omega*v)
+    const double qn = lc2(1.0, rv, -alpha, sn);           // q = r - alpha*s
+    const double yn = lc2(1.0, wv, -alpha, zn);           // y = w - alpha*z
+    p[i] = pn;
+    s[i] = sn;
+    z[i] = zn;
+    q[i] = qn;
+    y[i] = yn;
+    if (!sink.partials) return;
+    d.step(DB, qn, yn);
+    d.step(DE, yn, yn);
+    d.step(DD, qn, qn);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+
+// v = A z (tag "Az") fused with x, r, w and the beta phase's partials
+// f = (r0*, r), r = (r, r), g = (r0*, w), a = (r0*, s), h = (r0*, z)
+struct EpiPsB {
+  static constexpr int kIn = 8;
+  static constexpr int kInStaged = kIn;
+  static constexpr int kWcBatch = 2;  // dot-carrying: register-bound
+  static constexpr int kMinBlocks = 1;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 8;
+  double *v, *x, *r, *w;
+  SolverState* st;
+  DotSink sink;
+  const double* in[kIn];  // x p q y t r0s s z
+  double alpha, omega;
+  DotsT<kDotsPsB> d;
+  __device__ bool active() const { return gate_all(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() {
+    d.zero();
+    alpha = st->alpha;
+    omega = st->omega;
+  }
+  __device__ void row(long long i, double vv, const double* in8) {
+    v[i] = vv;
+    if (!isfinite(vv)) report_nonfinite(st, PBS_TAG_AZ, i);
+    const double qv = in8[2], yv = in8[3];
+    x[i] = lc3(1.0, in8[0], alpha, in8[1], omega, qv);   // x = x + alpha*p + omega*q
+    const double rn = lc2(1.0, qv, -omega, yv);           // r = q - omega*y
+    const double wn = asdd(yv, -omega, in8[4], alpha, vv);  // w = y - omega*(t - alpha*v)
+    r[i] = rn;
+    w[i] = wn;
+    if (!sink.partials) return;
+    const double r0 = in8[5];
+    d.step(DF, r0, rn);
+    d.step(DR, rn, rn);
+    d.step(DG, r0, wn);
+    d.step(DA, r0, in8[6]);
+    d.step(DH, r0, in8[7]);
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+};
+
 // --------------------------------------------------- CSR pipelined engine
 
 constexpr int kPipeRows = 256;        // rows per block = consumer threads

@@ -82,7 +82,17 @@ _PROD_STAGES = {
         [(0, 0, (2, 1)), (0, 0, (3, 2)), (0, 0, (1, 2)), (0, 0, (2, 2)), (0, 2, None)],  # u z x r, f rr
         [(0, 0, (1, 1))],                                    # w
     ],
+    # p-BiCGStab (oracle solve_pstab; not in the reference): stage 1 alpha
+    # (scalar), 2 omega, 3 after the x/r/w update, 4 complete
+    "pbicgstab": [
+        [],                                                  # alpha
+        [(1, 0, None), (0, 0, (2, 2)), (0, 0, (2, 2)), (0, 0, (2, 2)), (0, 0, (1, 1)),
+         (0, 0, (1, 1)), (0, 3, None), (1, 0, None)],        # t, p s z q y, b e d, v
+        [(0, 0, (2, 2)), (0, 0, (1, 1)), (0, 0, (2, 2)), (0, 5, None)],  # x r w, f rr g sd zd
+        [],                                                  # beta, record
+    ],
 }
+_PROD_WORKSPACE = {"bicgstab": 7, "gpbicg": 11, "pbicgstab": 11}
 
 
 def _prod_tick(c: OpCounters, method: str, stages: int) -> None:
@@ -106,10 +116,14 @@ def synthesize(method: str, iterations: int, stopped_in_loop: bool, replaced_at,
     set of completed iterations that ran residual replacement.
     """
     if method in _PROD_STAGES:
-        c = OpCounters(n_workspace_vectors=7 if method == "bicgstab" else 11)
+        c = OpCounters(n_workspace_vectors=_PROD_WORKSPACE[method])
         c.spmv()
         c.updates(0, 1)
-        c.batch(1)
+        if method == "pbicgstab":  # w0 = A r0, then rr and (r0*, w0)
+            c.spmv()
+            c.batch(2)
+        else:
+            c.batch(1)
         c.snapshot()
         for _ in range(iterations):
             _prod_tick(c, method, 4)

@@ -169,7 +169,8 @@ def _prepare(A, b, x0):
 _TRACE_NAMES = ("x", "r", "p", "u", "o", "t", "w", "y", "z", "s", "q", "g", "l")
 # the reference's trace_hook dicts of the product-type methods (solvers.py:315, 448)
 _TRACE_NAMES_BY_METHOD = {"bicgstab": ("x", "r", "p", "t", "Ap", "At"),
-                          "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z")}
+                          "gpbicg": ("x", "r", "p", "u", "t", "w", "y", "z"),
+                          "pbicgstab": ("x", "r", "p", "s", "z", "q", "y", "w", "t", "v")}
 
 
 def _ptr(a):
@@ -238,7 +239,7 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
     for i in range(k):
         rec = IterationRecord(i, float(rel[i]), replaced=bool(flags[i] & _lib.HIST_REPLACED))
         if flags[i] & _lib.HIST_HAS_COEF:
-            if method == "bicgstab":  # CoefficientSet(alpha, beta, omega) (solvers.py:309)
+            if method in ("bicgstab", "pbicgstab"):  # CoefficientSet(alpha, beta, omega) (solvers.py:309)
                 rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
                                                   omega=float(coef[i, 2]))
             else:
@@ -307,8 +308,20 @@ def solve_gpbicg(A, b, x0=None, config=None, engine=None, trace_hook=None) -> So
     return _solve_device(A, b, "gpbicg", x0, config, engine, trace_hook)
 
 
+def solve_pbicgstab(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:
+    """Pipelined BiCGStab (Cools & Vanroose), the paper's p-BiCGStab comparator
+     on the device.  The reference does not ship it
+    (SPEC.md:13); this follows the restatement in oracle/pbsafe_oracle.c
+    (solve_pstab) with the reference BiCGStab's conventions
+    (solvers.py:210-327): same shadow residual, check order, guards and
+    (alpha, beta, omega) records.  Two reduction phases per iteration, each
+    overlappable with an independent SpMV (t = A w, v = A z)."""
+    return _solve_device(A, b, "pbicgstab", x0, config, engine, trace_hook)
+
+
 METHODS = {
     "bicgstab": solve_bicgstab,
+    "pbicgstab": solve_pbicgstab,
     "gpbicg": solve_gpbicg,
     "ssbicgsafe2": solve_ssbicgsafe2,
     "pbicgsafe": solve_pbicgsafe,
