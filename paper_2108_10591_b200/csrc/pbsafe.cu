@@ -118,6 +118,21 @@ struct Partition {
 
 struct Workspace;
 
+// What a captured solver graph bakes in about its operator: pointers and the
+// staged-engine metadata.  A workspace (with its graphs) freed together with
+// an operator is kept by the context and adopted by the next operator whose
+// signature is identical — the stream-ordered pool hands an upload of the
+// same shape the same addresses, so a solve(CsrMatrix) per step re-uses the
+// graphs instead of capturing and instantiating them again.
+struct MatSig {
+  long long n_rows, n_cols, nnz, blk_nnz_max;
+  long long stencil;
+  const void *rp, *ci, *v, *wc;
+  XWin xwin;
+  StencilView sv;
+  StencilWin swin;
+};
+
 struct pbs_ctx {
   int device = 0;
   int sms = 148;
@@ -132,6 +147,8 @@ struct pbs_ctx {
   SolverState* tmp_state = nullptr;
   std::map<const void*, int> occ;  // kernel -> resident CTAs per SM
   EventPool events;
+  Workspace* ws_cache = nullptr;  // workspace of the last freed single-GPU operator
+  MatSig ws_sig{};
 };
 
 struct pbs_mat {
@@ -246,9 +263,42 @@ static void free_ws(Workspace* ws) {
   delete ws;
 }
 
+static MatSig mat_sig(const pbs_mat* m) {
+  MatSig g;
+  memset(&g, 0, sizeof(g));  // padding too: signatures compare with memcmp
+  g.n_rows = m->n_rows;
+  g.n_cols = m->n_cols;
+  g.nnz = m->nnz;
+  g.blk_nnz_max = m->blk_nnz_max;
+  g.stencil = m->stencil;
+  g.rp = m->rp;
+  g.ci = m->ci;
+  g.v = m->v;
+  g.wc = m->wc;
+  memcpy(&g.xwin, &m->xwin, sizeof(XWin));
+  memcpy(&g.sv, &m->sv, sizeof(StencilView));
+  memcpy(&g.swin, &m->swin, sizeof(StencilWin));
+  return g;
+}
+
+static void drop_ws_cache(pbs_ctx* ctx) {
+  if (!ctx || !ctx->ws_cache) return;
+  free_ws(ctx->ws_cache);
+  ctx->ws_cache = nullptr;
+}
+
 static int ensure_ws(pbs_mat* m, long long hist_slots) {
   pbs_ctx* ctx = m->ctx;
   Workspace* ws = m->ws;
+  if (!ws && ctx->ws_cache && !m->part.dist) {
+    const MatSig g = mat_sig(m);
+    if (memcmp(&g, &ctx->ws_sig, sizeof(MatSig)) == 0) {
+      ws = m->ws = ctx->ws_cache;  // same operator layout: its graphs stay valid
+      ctx->ws_cache = nullptr;
+    } else {
+      drop_ws_cache(ctx);
+    }
+  }
   if (!ws) {
     ws = new Workspace();
     ws->ctx = ctx;
@@ -1762,6 +1812,7 @@ PBS_EXPORT int pbs_destroy(pbs_ctx* ctx) {
   if (!ctx) return PBS_OK;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  drop_ws_cache(ctx);
   cudaFree(ctx->scratch);
   cudaFree(ctx->partials);
   cudaFree(ctx->tmp_state);
@@ -1993,6 +2044,7 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
   if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
     return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with nnz arrays");
   CK(cudaSetDevice(ctx->device));
+  if (ctx->ws_cache && ctx->ws_cache->n != n_rows) drop_ws_cache(ctx);  // cannot match: release it now
   pbs_mat* m = new pbs_mat();
   m->ctx = ctx;
   m->n_rows = n_rows;
@@ -2273,7 +2325,13 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   if (!m) return PBS_OK;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
-  free_ws(m->ws);
+  if (m->ws && !m->part.dist) {
+    drop_ws_cache(m->ctx);
+    m->ctx->ws_cache = m->ws;
+    m->ctx->ws_sig = mat_sig(m);
+  } else {
+    free_ws(m->ws);
+  }
   pool_free(m->ctx, m->rp);
   pool_free(m->ctx, m->ci);
   pool_free(m->ctx, m->v);

@@ -586,3 +586,23 @@ def test_band_mode_plan_solve_bitwise_vs_oracle(pb):
     fast = pb.solve(dm, b, config=pb.SolverConfig(tol=1e-30, max_iters=10))
     np.testing.assert_allclose([r.rel_res_recur for r in fast.history], ref2["rel"], rtol=1e-12)
     dm.free()
+
+
+def test_workspace_reuse_across_uploads(pb):
+    """solve(CsrMatrix) uploads and frees its operator every call; the context
+    keeps the freed operator's workspace and graphs for the next operator with
+    the same device layout.  A re-used graph must compute the new operator's
+    solve: values changed in place of the same pattern give the same result
+    as an eager (graph-free) solve of that operator."""
+    spec, A, b, x0, g = gc.load_case("cd3d16_pbicgsafe", orc.spmv)
+    cfg = _cfg(pb, spec)
+    first = pb.solve(A, b, config=cfg)
+    again = pb.solve(A, b, config=cfg)
+    assert np.array_equal(first.x, again.x)
+    assert np.array_equal([r.rel_res_recur for r in first.history], [r.rel_res_recur for r in again.history])
+    A2 = pb.CsrMatrix(A.n_rows, A.n_cols, A.row_ptr, A.col_idx, A.values * 1.5 + 0.01 * (A.row_ptr[1:] - A.row_ptr[:-1]).repeat(A.row_ptr[1:] - A.row_ptr[:-1]))
+    graphed = pb.solve(A2, b, config=cfg)
+    eager = pb.solve(A2, b, config=cfg, engine=pb.DeviceEngine(use_graphs=False))
+    assert np.array_equal(graphed.x, eager.x)
+    assert graphed.iterations == eager.iterations
+    assert not np.array_equal(graphed.x, first.x)

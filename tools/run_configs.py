@@ -55,7 +55,7 @@ def main():
             ms = out.device["device_ms"]
             its = max(out.iterations, 1)
             # vector passes of each method's device schedule
-            passes = {"ssbicgsafe2": 26, "bicgstab": 17, "gpbicg": 35}.get(method, 32)
+            passes = {"ssbicgsafe2": 26, "bicgstab": 17, "gpbicg": 35, "pbicgstab": 24}.get(method, 32)
             it_bytes = 2 * m_a + passes * 8 * n
             row = {
                 "config": cfg_name, "operator": op_name, "method": method, "n": n, "nnz": dm.nnz,
@@ -79,7 +79,7 @@ def main():
             dm = DeviceMatrix.from_csr((rp, ci.astype(np.int32), v))
             b_t = torch.from_numpy(b).cuda()
             gen_s = time.time() - t0
-            run(name, "csr", dm, b_t, ["pbicgsafe", "pbicgsafe-rr", "ssbicgsafe2", "bicgstab", "gpbicg"], c["tol"],
+            run(name, "csr", dm, b_t, ["pbicgsafe", "pbicgsafe-rr", "ssbicgsafe2", "pbicgstab", "bicgstab", "gpbicg"], c["tol"],
                 extra={"gen_s": gen_s})
             dm.free()
             continue
@@ -89,7 +89,7 @@ def main():
         ones = torch.ones(sm.n_rows, dtype=torch.float64, device="cuda")
         b_t = torch.empty_like(ones)
         csr.spmv_dev(ones.data_ptr(), b_t.data_ptr())
-        methods = ["pbicgsafe", "pbicgsafe-rr", "ssbicgsafe2", "bicgstab", "gpbicg"]
+        methods = ["pbicgsafe", "pbicgsafe-rr", "ssbicgsafe2", "pbicgstab", "bicgstab", "gpbicg"]
         run(name, "csr", csr, b_t, methods, c["tol"])
         run(name, "stencil", sm, b_t, methods, c["tol"])
         csr.free()
