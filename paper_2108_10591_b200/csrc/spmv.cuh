@@ -983,8 +983,13 @@ struct StencilWin {
   int pw[kMaxStencil];  // window of each stencil point
 };
 
+// resident CTAs per SM the staged stencil engine is compiled for (register cap)
+#ifndef PBS_SPIPE_MINB
+#define PBS_SPIPE_MINB 2
+#endif
+
 template <class Epi, int DIM, int NP>
-__global__ void __launch_bounds__(kPipeThreads, 2) stencil_pipe_kernel(const __grid_constant__ StencilView S,
+__global__ void __launch_bounds__(kPipeThreads, PBS_SPIPE_MINB) stencil_pipe_kernel(const __grid_constant__ StencilView S,
                                                                        const double* __restrict__ x, Epi epi,
                                                                        XWin W, StencilWin SW, int bslots) {
   __shared__ int go;
