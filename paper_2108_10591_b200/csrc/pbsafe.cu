@@ -569,7 +569,8 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   *chunk = ch;
   *stage_in = si;
   *smem = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double) + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
-  const void* k = si ? (const void*)csr_pipe_kernel<Epi, true> : (const void*)csr_pipe_kernel<Epi, false>;
+  const void* k = si ? (c == 1 ? (const void*)csr_pipe_kernel<Epi, true, 1> : (const void*)csr_pipe_kernel<Epi, true>)
+                     : (const void*)csr_pipe_kernel<Epi, false>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -688,7 +689,10 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
     // programmatic dependent launch: overlaps this CTA's prologue and first
     // matrix chunks with the previous kernel's drain
-    if (stage_in)
+    if (stage_in && ctas == 1)  // 1-CTA layout: the instantiation with more products in flight
+      launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, true, 1>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
+                 cstages, chunk);
+    else if (stage_in)
       launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, true>, grid, kPipeThreads, smem, A, x, epi, W, bslots, cstages,
                  chunk);
     else

@@ -45,6 +45,9 @@ namespace pbs {
 #ifndef PBS_WCB_K3S
 #define PBS_WCB_K3S 4
 #endif
+#ifndef PBS_WCB_ONE  // the 1-CTA-per-SM instantiation (band mode, long rows)
+#define PBS_WCB_ONE 8
+#endif
 #ifndef PBS_K12D_MINB
 #define PBS_K12D_MINB 1
 #endif
@@ -652,8 +655,13 @@ constexpr size_t kPipeBarrierBytes = 512;
 // every thread wait for the previous grid (griddep_wait) and take the CTA's
 // one gate decision.  Consumers release the next kernel's launch once their
 // rows are written, before the dot reduction / check tail.
-template <class Epi, bool SI = true>
-__global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
+// MINB: resident CTAs per SM the instantiation is compiled for.  2 (96
+// registers) is the window-mode default; the 1-CTA layouts (band mode,
+// config 4's long rows with extra chunk stages) get their own instantiation
+// with the register room for 8 staged products in flight per row
+// (profiles/sweeps/r1_band_ilp.log: config 3, 692 -> 615 us per iteration).
+template <class Epi, bool SI = true, int MINB = 2>
+__global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A, const double* __restrict__ x,
                                                                    Epi epi, XWin W, int bslots, int cstages,
                                                                    int chunk) {
   constexpr bool stage_in = SI;
@@ -913,7 +921,7 @@ __global__ void __launch_bounds__(kPipeThreads, 2) csr_pipe_kernel(CsrView A, co
         if (A.wc) {
           // staged window index per nonzero: no window search, half the bytes
           const unsigned short* wcs = reinterpret_cast<const unsigned short*>(st + CL.ci) + h.dci;
-          constexpr int U = Epi::kWcBatch;
+          constexpr int U = MINB == 1 ? PBS_WCB_ONE : Epi::kWcBatch;
           for (int k = lo; k < hi; k += U) {
             double vv[U], xv[U];
 #pragma unroll
