@@ -582,15 +582,18 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
 
 // PBS_STENCIL_ENGINE=direct|pipe forces one stencil engine; default: per
 // epilogue (Epi::kStencilPipe — the staged engine for the dot-carrying K3,
-// the L1-cached direct engine for the streaming K12)
+// the L1-cached direct engine for the streaming K12), except that stencils
+// wider than 7 points stage everything: 27 L1 neighbour loads per row cost
+// the direct engine more than the staging (config 4 K12: 1883 -> 1758 us,
+// profiles/sweeps/r1_stencil_engines.log)
 template <class Epi>
-static bool stencil_engine_pipe() {
+static bool stencil_engine_pipe(int npts) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PBS_STENCIL_ENGINE");
     v = (e && std::string(e) == "direct") ? 0 : ((e && std::string(e) == "pipe") ? 1 : 2);
   }
-  return v == 2 ? Epi::kStencilPipe : v == 1;
+  return v == 2 ? (Epi::kStencilPipe || npts > 7) : v == 1;
 }
 
 template <class Epi, int DIM, int NP>
@@ -699,7 +702,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, false>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
                  cstages, chunk);
     if (L.err) return 0;
-  } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>()) {
+  } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>(m->sv.npts)) {
     StencilView S = m->sv;
     S.row_lo = lo;
     S.row_hi = hi;
@@ -2207,6 +2210,17 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
         W.total = (int)total;
         m->xwin = W;
         for (int q = 0; q < npts; ++q) m->swin.pw[q] = owner[q];
+        // constant staged offsets of interior blocks (see StencilWin)
+        long long soff[kMaxWin] = {0, 0, 0, 0}, clamp = 0;
+        for (int c = 1; c < W.nwin; ++c) soff[c] = soff[c - 1] + W.cap[c - 1];
+        for (int c = 0; c < W.nwin; ++c)
+          if (-(long long)W.wmin[c] > clamp) clamp = -(long long)W.wmin[c];
+        for (int q = 0; q < npts; ++q) {
+          const int c = owner[q];
+          const long long wmin_even = (long long)W.wmin[c] & ~1LL;  // (r0 + wmin) & ~1 == r0 + (wmin & ~1), r0 even
+          m->swin.kfix[q] = (int)(S.foff[q] - wmin_even + soff[c]);
+        }
+        m->swin.clamp_r0 = clamp;
       }
     }
   }

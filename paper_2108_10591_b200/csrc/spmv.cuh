@@ -989,6 +989,12 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
 // column order), so the result is bitwise the CSR engine's.
 struct StencilWin {
   int pw[kMaxStencil];  // window of each stencil point
+  // Blocks whose windows all start in the grid (r0 >= clamp_r0) stage window
+  // c from r0 + (wmin[c] & ~1), so row t's neighbour p sits at the staged
+  // index t + kfix[p], a constant; only the first blocks (windows clamped at
+  // row 0) look the window start up per block.
+  int kfix[kMaxStencil];
+  long long clamp_r0;
 };
 
 // resident CTAs per SM the staged stencil engine is compiled for (register cap)
@@ -1115,25 +1121,35 @@ __global__ void __launch_bounds__(kPipeThreads, PBS_SPIPE_MINB) stencil_pipe_ker
       } else {
         c[2] = (int)i;
       }
-      // window base per cluster: x[col] = xw[col - wsb[w]]
       const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
-      int wsb[kMaxWin];
-      {
-        int soff = 0;
-#pragma unroll
-        for (int cc = 0; cc < kMaxWin; ++cc) {
-          wsb[cc] = cc < W.nwin ? (int)bhp->ws[cc] - soff : 0;
-          soff += cc < W.nwin ? W.cap[cc] : 0;
-        }
-      }
       const unsigned vm = S.valid_mask(c, DIM);
       double acc = 0.0;
+      if (r0 >= SW.clamp_r0 && !(r0 & 1)) {
+        // interior blocks: neighbour p at the constant staged offset t + kfix[p]
+        const double* xt = xw + t;
 #pragma unroll
-      for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
-        if (NP == 0 && p >= npts) break;
-        if ((vm >> p) & 1u) {
-          const int col = (int)(i + S.foff[p]);
-          acc = add(acc, mul(S.coef[p], xw[col - wsb[SW.pw[p]]]));
+        for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
+          if (NP == 0 && p >= npts) break;
+          if ((vm >> p) & 1u) acc = add(acc, mul(S.coef[p], xt[SW.kfix[p]]));
+        }
+      } else {
+        // window base per cluster: x[col] = xw[col - wsb[w]]
+        int wsb[kMaxWin];
+        {
+          int soff = 0;
+#pragma unroll
+          for (int cc = 0; cc < kMaxWin; ++cc) {
+            wsb[cc] = cc < W.nwin ? (int)bhp->ws[cc] - soff : 0;
+            soff += cc < W.nwin ? W.cap[cc] : 0;
+          }
+        }
+#pragma unroll
+        for (int p = 0; p < (NP > 0 ? NP : kMaxStencil); ++p) {
+          if (NP == 0 && p >= npts) break;
+          if ((vm >> p) & 1u) {
+            const int col = (int)(i + S.foff[p]);
+            acc = add(acc, mul(S.coef[p], xw[col - wsb[SW.pw[p]]]));
+          }
         }
       }
       double inr[Epi::kIn > 0 ? Epi::kIn : 1];

@@ -8,3 +8,4 @@ run "" "--operator stencil"
 for e in "" "PBS_STENCIL_ENGINE=direct" "PBS_STENCIL_ENGINE=pipe"; do
   runt "$e" "--operator stencil --config c4 --iters 10"
 done
+run "" "--iters 300"
