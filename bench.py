@@ -256,38 +256,52 @@ def run_ours(args):
     # nonzero (f64 value + int32 column) + row_ptr; the staged engine actually
     # streams 10 B (u16 window-local columns), so `traffic` can sit below it.
     peak, peak_src = peaks()
-    m_a = 12 * nnz + 8 * (n + 1)
-    k3_bytes = m_a + 11 * 8 * n     # w gather, As l g s y r r0s reads, l g s writes (+ dots a c d g)
-    k12_bytes = m_a + 21 * 8 * n    # s gather, r p u t y l g w z x r0s reads, As p u w t z y x r writes (+ b e f h r)
-    it_bytes = 2 * m_a + 34 * 8 * n  # SURVEY 8(d) three-phase minimum (K1, K2, K3)
-    it_bytes_fused = 2 * m_a + 32 * 8 * n  # this schedule: K1+K2 fused (As not re-read)
+    part = dsys is not None
+    # bytes per rank: the row slab this GPU owns (the whole system at N = 1)
+    nr, nz = (n_loc, int(dm.nnz)) if part else (n, nnz)
+    m_a = 12 * nz + 8 * (nr + 1)
+    if part:
+        # multi-GPU schedule (csrc/pbsafe.cu dist_iter): K1 As = A s alone so the
+        # all-gather overlaps it, K2 the row-local update, K3 with all nine dots
+        k12_bytes = m_a + 2 * 8 * nr   # s gather, As write
+        k2_bytes = 20 * 8 * nr         # r p u s t y As l g w z x reads, p u w t z y x r writes
+        k3_bytes = m_a + 12 * 8 * nr   # w gather, As l g s y r r0s t reads, l g s writes
+        it_bytes_fused = 2 * m_a + 34 * 8 * nr
+    else:
+        k3_bytes = m_a + 11 * 8 * nr    # w gather, As l g s y r r0s reads, l g s writes (+ dots a c d g)
+        k12_bytes = m_a + 21 * 8 * nr   # s gather, r p u t y l g w z x r0s reads, As p u w t z y x r writes (+ b e f h r)
+        it_bytes_fused = 2 * m_a + 32 * 8 * nr  # this schedule: K1+K2 fused (As not re-read)
+    it_bytes = 2 * m_a + 34 * 8 * nr  # SURVEY 8(d) three-phase minimum (K1, K2, K3)
     kms = {name: sum(r.kernel_ms[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
     kcnt = {name: sum(r.kernel_count[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
     k3_avg = kms["K3_Aw_epilogue"] / max(kcnt["K3_Aw_epilogue"], 1)
     k3_gbs = k3_bytes / (k3_avg * 1e-3) / 1e9
     k12_avg = kms["K1_As"] / max(kcnt["K1_As"], 1)
     k12_gbs = k12_bytes / (k12_avg * 1e-3) / 1e9
+    k1_label = ("K1 (As = A s on the halo-exchanged s; the all-gather overlaps it)" if part else
+                "K12 (As CSR SpMV + fused p u w t z y x r updates + dots b e f h r)")
     if kms["K1_As"] > kms["K3_Aw_epilogue"]:  # dominant kernel = larger share of the step
-        dom = ("K12 (As CSR SpMV + fused p u w t z y x r updates + dots b e f h r)", k12_bytes, k12_avg,
-               k12_gbs, "K1_As")
+        dom = (k1_label, k12_bytes, k12_avg, k12_gbs, "K1_As")
     else:
-        dom = ("K3 (Aw CSR SpMV + l,g,s updates + dots a c d g + fused check)", k3_bytes, k3_avg, k3_gbs,
+        dom = ("K3 (Aw CSR SpMV + l,g,s updates + all nine dots; all-gather + finalize follow)" if part else
+               "K3 (Aw CSR SpMV + l,g,s updates + dots a c d g + fused check)", k3_bytes, k3_avg, k3_gbs,
                "K3_Aw_epilogue")
     tim_ms = sum(r.device_ms for r in tres)
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")  # from the committed ncu --set full capture
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and not part:  # the capture is of the single-GPU fused kernels
         try:
             traffic = json.load(open(tr_path)).get(dom[4], {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     kernels = {}
-    for name, byt in (("K1_As", k12_bytes), ("K3_Aw_epilogue", k3_bytes)):
+    per_kind = [("K1_As", k12_bytes), ("K3_Aw_epilogue", k3_bytes)] + ([("K2_update", k2_bytes)] if part else [])
+    for name, byt in per_kind:
         if kcnt[name]:
             avg = kms[name] / kcnt[name]
             kernels[name] = {"avg_us": avg * 1e3, "alg_bytes": byt, "GBps": byt / (avg * 1e-3) / 1e9,
                              "frac": byt / (avg * 1e-3) / 1e9 / peak, "share_of_step": kms[name] / tim_ms}
-    kernels["K1_As"]["name"] = "K12: As = A s fused with the row-local p u w t z y x r updates"
+    kernels["K1_As"]["name"] = k1_label
     if kcnt["F_finalize"]:
         fin = kms["F_finalize"] / kcnt["F_finalize"]
         kernels["F_finalize"] = {"avg_us": fin * 1e3, "share_of_step": kms["F_finalize"] / tim_ms}
@@ -365,7 +379,7 @@ def run_ours(args):
             "config": {"workload": WORKLOAD, "operator": "csr", "iterations_per_solve": avg_it,
                        "time_to_tol_ms": total_ms / args.steps,
                        "parallelism": (f"row partition x{world} (NCCL halo + compensated all-gather)"
-                                       if world > 1 else "single GPU"),
+                                       if part else "single GPU"),
                        "l2": "inputs larger than L2: CSR 192 MB + 18 workspace vectors 302 MB per solve "
                              "vs 126 MB L2",
                        "graphs": True},
@@ -376,8 +390,11 @@ def run_ours(args):
             "iteration_roofline": {"alg_bytes_per_iter": it_bytes,
                                    "achieved_GBps": it_bytes * iters_per_s / world / 1e9,
                                    "frac": it_bytes * iters_per_s / world / 1e9 / peak,
-                                   "note": "B_iter = 2*(12 nnz + 8(n+1)) + 34*8n (SURVEY 8(d)); this "
-                                           "schedule moves 2*(12 nnz+8(n+1)) + 32*8n (K1+K2 fused)",
+                                   "note": ("per rank: B_iter = 2*(12 nnz + 8(n+1)) + 34*8n over the rank's "
+                                            "row slab (SURVEY 8(d)); the multi-GPU schedule moves exactly that"
+                                            if part else
+                                            "B_iter = 2*(12 nnz + 8(n+1)) + 34*8n (SURVEY 8(d)); this "
+                                            "schedule moves 2*(12 nnz+8(n+1)) + 32*8n (K1+K2 fused)"),
                                    "frac_own_schedule": it_bytes_fused * iters_per_s / world / 1e9 / peak},
             "kernels": kernels,
             "comparators": comparators,
