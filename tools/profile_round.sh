@@ -10,6 +10,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:csr_
   -o /tmp/${TAG}_k12_k3 -f python tools/prof_solve.py --iters 10 > $O/ncu_full_$TAG.log 2>&1
 ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page details --csv > $O/${TAG}_k12_k3_details.csv 2>&1
 ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page raw --csv > $O/${TAG}_k12_k3_raw.csv 2>&1
-ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page source --csv --print-source sass > $O/${TAG}_k12_k3_source.csv 2>/dev/null
+ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page source --csv --print-source sass > /tmp/${TAG}_k12_k3_source.csv 2>/dev/null
+python tools/ncu_hot_sass.py /tmp/${TAG}_k12_k3_source.csv > $O/${TAG}_k12_k3_hot_sass.txt 2>&1
 ls -la /tmp/${TAG}_k12_k3.ncu-rep
-cp /tmp/${TAG}_k12_k3.ncu-rep $O/ 2>/dev/null
+# the report itself stays on the box: gpurun copies back at most 64 MiB
