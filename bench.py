@@ -364,7 +364,7 @@ def run_ours(args):
                        "int64->int32 narrowing, solve, x + history D2H"}
 
     cpu = None
-    if rank == 0 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
         threads = os.cpu_count() or 1
         b_host_np = b_dev.cpu().numpy()
         cpu = cpu_baseline(rp, ci, v, b_host_np, iters=args.cpu_iters, threads=threads)
