@@ -15,7 +15,9 @@
  *                                solve_pbicgsafe_rr(), solve_ssbicgsafe2(),
  *                                solve_bicgstab(), solve_gpbicg()
  *                                (solvers.py:791-803, 742-779, 485-592,
- *                                210-327, 330-460), with
+ *                                210-327, 330-460), plus the paper's
+ *                                p-BiCGStab comparator (not in
+ *                                the reference — PBS_METHOD_PBICGSTAB), with
  *                                SolverConfig fields (solvers.py:51-78) in
  *                                pbs_config and SolveOutcome / IterationRecord
  *                                (solvers.py:81-114) in pbs_result + history

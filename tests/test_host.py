@@ -157,3 +157,26 @@ def test_csr_matrix_validate():
 
     with pytest.raises(NonFiniteVectorError):
         bad.validate()
+
+
+def test_pbicgstab_counters_follow_the_oracle_stages():
+    """synthesize('pbicgstab', ...) ticks what the oracle's solve_pstab does:
+    setup Ax + Ar and one 2-dot batch, then per completed iteration t = A w,
+    v = A z and batches of 3 and 5 dots; a stop at stage s ticks the stages
+    before it (1 alpha: none, 2 omega: both products + the 3-dot batch,
+    3 beta: the x r w update and the 5-dot batch too)."""
+    from oracle import oracle as orc
+    from paper_2108_10591_b200.instrument import synthesize
+
+    spec, A, b, x0, g = gc.load_case("bs_maxiters5", orc.spmv)
+    o = orc.solve(A.row_ptr, A.col_idx, A.values, b, method="pbicgstab", tol=spec["tol"], max_iters=5)
+    c = synthesize("pbicgstab", o["iterations"], False, set())
+    assert c.n_spmv == o["n_spmv"] == 12
+    assert (c.n_dots, c.n_reductions) == (2 + 8 * 5, 1 + 2 * 5)
+    for stage, extra_spmv in ((1, 0), (2, 2), (3, 2), (4, 2)):
+        c = synthesize("pbicgstab", 3, True, set(), stop_stage=stage)
+        assert c.n_spmv == 2 + 2 * 3 + extra_spmv, stage
+    o = orc.solve(np.array([0, 1, 2]), np.array([1, 0]), np.array([1.0, 1.0]), np.array([1.0, 0.0]),
+                  method="pbicgstab", tol=1e-10, max_iters=10)
+    assert o["status"] == "breakdown" and o["failure_iter"] == 0 and o["n_spmv"] == 2
+    assert synthesize("pbicgstab", 0, True, set(), stop_stage=1).n_spmv == 2
