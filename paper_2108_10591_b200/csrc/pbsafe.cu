@@ -105,6 +105,10 @@ struct pbs_dist {
   ncclComm_t halo = nullptr, red = nullptr;
   cudaStream_t comm = nullptr;  // all-gather + finalize, overlapping the As SpMV
   cudaEvent_t ev_part = nullptr, ev_coef = nullptr;
+  // halo exchange of s / w on its own stream, overlapping the interior rows
+  // of the SpMV that consumes it (Partition::split)
+  cudaStream_t hstream = nullptr;
+  cudaEvent_t ev_vec = nullptr, ev_halo = nullptr;
   double* sendbuf = nullptr;  // this rank's 9 compensated pairs
   double* recvbuf = nullptr;  // all ranks' pairs, rank order
 };
@@ -114,6 +118,12 @@ struct Partition {
   pbs_dist* dist = nullptr;
   long long n_global = 0, row_lo = 0, hl = 0, hr = 0;
   std::vector<long long> sends, recvs;  // triples
+  // interior rows [L0, L1) read no halo column; both bounds are multiples of
+  // the 256-row block, so all three launches keep the staged engine's
+  // window-local columns.  split: the SpMVs after a halo exchange run the
+  // interior while the exchange is in flight, then the boundary rows.
+  bool split = false;
+  long long L0 = 0, L1 = 0;
 };
 
 struct Workspace;
@@ -676,8 +686,9 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
   } else if (!m->stencil) {
-    // window-local columns describe the row blocks of a launch starting at row 0
-    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, lo == 0 ? m->wc : nullptr};
+    // window-local columns describe the 256-row blocks counted from row 0, so
+    // any launch starting on a block boundary can use them
+    CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, (lo % kPipeRows) == 0 ? m->wc : nullptr};
     // staged x windows need the window-local columns; otherwise gather x
     const XWin W = A.wc ? m->xwin : XWin{};
     int bslots, cstages, ctas, chunk, stage_in;
@@ -1342,16 +1353,17 @@ static int get_graph(pbs_ctx* ctx, pbs_mat* m, long long key, IterFn fn, const M
 // The all-gather + check of iteration j overlaps the As SpMV: the pipelined
 // method's single reduction hides behind one SpMV.
 
-static void halo_exchange(Launcher& L, Workspace* ws, pbs_mat* m, int k) {
+static void halo_exchange(Launcher& L, Workspace* ws, pbs_mat* m, int k, cudaStream_t st = nullptr) {
   Partition& P = m->part;
   pbs_dist* D = P.dist;
+  if (!st) st = L.s;
   if (L.err || D->nranks == 1 || (P.sends.empty() && P.recvs.empty())) return;
   NcclApi& A = nccl();
   ncclResult_t r = A.GroupStart();
   for (size_t i = 0; r == ncclSuccess && i < P.recvs.size(); i += 3)
-    r = A.Recv(ws->X.v[k] + P.recvs[i + 1], (size_t)P.recvs[i + 2], ncclDouble, (int)P.recvs[i], D->halo, L.s);
+    r = A.Recv(ws->X.v[k] + P.recvs[i + 1], (size_t)P.recvs[i + 2], ncclDouble, (int)P.recvs[i], D->halo, st);
   for (size_t i = 0; r == ncclSuccess && i < P.sends.size(); i += 3)
-    r = A.Send(ws->V.v[k] + P.sends[i + 1], (size_t)P.sends[i + 2], ncclDouble, (int)P.sends[i], D->halo, L.s);
+    r = A.Send(ws->V.v[k] + P.sends[i + 1], (size_t)P.sends[i + 2], ncclDouble, (int)P.sends[i], D->halo, st);
   ncclResult_t r2 = A.GroupEnd();
   if (r == ncclSuccess) r = r2;
   if (r != ncclSuccess) L.err = set_err(L.ctx, PBS_ERR_NCCL, std::string("halo exchange: ") + A.GetErrorString(r));
@@ -1387,20 +1399,47 @@ static void dist_setup(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md) {
   dist_check(L, ws, m, np, 0);
 }
 
+// Halo exchange of vector k, then an SpMV over all rows with epilogue factory
+// mk(partial_offset).  With Partition::split the exchange runs on the halo
+// stream while the interior rows [L0, L1) compute, and the boundary rows
+// follow once it has landed; dot partial records of the pieces are stored
+// one after another.  Returns the number of partial records.
+template <class MakeEpi>
+static int halo_spmv(Launcher& L, Workspace* ws, pbs_mat* m, int k, int kind, int tag, MakeEpi mk) {
+  Partition& P = m->part;
+  pbs_dist* D = P.dist;
+  if (!P.split) {
+    halo_exchange(L, ws, m, k);
+    L.mark(L.s, L.iter, 2, tag);
+    const int np = spmv_launch(L, ws->X.v[k], mk(0), 0, ws->n, kind);
+    L.mark(L.s, L.iter, 3, tag);
+    return np;
+  }
+  cudaEventRecord(D->ev_vec, L.s);  // the vector is final on the compute stream
+  cudaStreamWaitEvent(D->hstream, D->ev_vec, 0);
+  halo_exchange(L, ws, m, k, D->hstream);
+  cudaEventRecord(D->ev_halo, D->hstream);
+  L.mark(L.s, L.iter, 2, tag);
+  int np = spmv_launch(L, ws->X.v[k], mk(0), P.L0, P.L1, kind);
+  cudaStreamWaitEvent(L.s, D->ev_halo, 0);
+  if (P.L0 > 0) np += spmv_launch(L, ws->X.v[k], mk(np), 0, P.L0, kind);
+  if (P.L1 < ws->n) np += spmv_launch(L, ws->X.v[k], mk(np), P.L1, ws->n, kind);
+  L.mark(L.s, L.iter, 3, tag);
+  return np;
+}
+
 static void dist_iter(Launcher& L, Workspace* ws, pbs_mat* m, const Mode& md, bool replace) {
   pbs_dist* D = m->part.dist;
-  halo_exchange(L, ws, m, VS);
-  L.mark(L.s, L.iter, 2, PBS_TAG_AS);
-  spmv_launch(L, ws->X.v[VS], epi_store(ws, VAS, PBS_TAG_AS, 1), 0, ws->n, KK1);
-  L.mark(L.s, L.iter, 3, PBS_TAG_AS);
+  halo_spmv(L, ws, m, VS, KK1, PBS_TAG_AS, [&](int) { return epi_store(ws, VAS, PBS_TAG_AS, 1); });
   cudaStreamWaitEvent(L.s, D->ev_coef, 0);  // coefficients of this check
   int np;
   if (!replace) {
     vec_launch(L, k2_update_kernel, ws->n, KK2, ws->V, ws->n, ws->st, md.store_temps);
-    halo_exchange(L, ws, m, VW);
-    L.mark(L.s, L.iter, 2, PBS_TAG_AW);
-    np = spmv_launch(L, ws->X.v[VW], epi_k3(ws, md, 0), 0, ws->n, KK3);
-    L.mark(L.s, L.iter, 3, PBS_TAG_AW);
+    np = halo_spmv(L, ws, m, VW, KK3, PBS_TAG_AW, [&](int off) {
+      EpiK3 e = epi_k3(ws, md, 0);
+      if (e.sink.partials) e.sink.partials += off;
+      return e;
+    });
   } else {
     vec_launch(L, pou_kernel, ws->n, KR, ws->V, ws->n, ws->st);
     halo_exchange(L, ws, m, VO);
@@ -2753,6 +2792,9 @@ PBS_EXPORT int pbs_dist_init(pbs_ctx* ctx, int32_t nranks, int32_t rank, const v
   CK(cudaStreamCreateWithPriority(&d->comm, cudaStreamNonBlocking, hi));  // reduction first
   CK(cudaEventCreateWithFlags(&d->ev_part, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&d->ev_coef, cudaEventDisableTiming));
+  CK(cudaStreamCreateWithPriority(&d->hstream, cudaStreamNonBlocking, hi));
+  CK(cudaEventCreateWithFlags(&d->ev_vec, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&d->ev_halo, cudaEventDisableTiming));
   CK(cudaMalloc(&d->sendbuf, sizeof(double) * kPartStride));
   CK(cudaMalloc(&d->recvbuf, sizeof(double) * kPartStride * nranks));
   *out = d;
@@ -2768,10 +2810,30 @@ PBS_EXPORT int pbs_dist_destroy(pbs_dist* d) {
   cudaStreamDestroy(d->comm);
   cudaEventDestroy(d->ev_part);
   cudaEventDestroy(d->ev_coef);
+  cudaStreamSynchronize(d->hstream);
+  cudaStreamDestroy(d->hstream);
+  cudaEventDestroy(d->ev_vec);
+  cudaEventDestroy(d->ev_halo);
   cudaFree(d->sendbuf);
   cudaFree(d->recvbuf);
   delete d;
   return PBS_OK;
+}
+
+// Last row reading a left-halo column and first row reading a right-halo
+// column of a slab's extended-space CSR (out[0] starts at -1, out[1] at n).
+__global__ void halo_rows_kernel(const long long* rp, const int* ci, long long n, long long own_lo,
+                                 long long own_hi, unsigned long long* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    bool left = false, right = false;
+    for (long long k = rp[i]; k < rp[i + 1]; ++k) {
+      left = left || ci[k] < own_lo;
+      right = right || ci[k] >= own_hi;
+    }
+    if (left) atomicMax(&out[0], (unsigned long long)(i + 1));  // stored +1 (0 = none)
+    if (right) atomicMin(&out[1], (unsigned long long)i);
+  }
 }
 
 PBS_EXPORT int pbs_mat_set_partition(pbs_mat* m, pbs_dist* dist, int64_t n_global, int64_t row_lo, int64_t hl,
@@ -2801,5 +2863,31 @@ PBS_EXPORT int pbs_mat_set_partition(pbs_mat* m, pbs_dist* dist, int64_t n_globa
   for (size_t i = 0; i < P.recvs.size(); i += 3)
     if (P.recvs[i + 1] < 0 || P.recvs[i + 1] + P.recvs[i + 2] > m->n_cols)
       return set_err(ctx, PBS_ERR_INVALID, "halo receive outside the extended space");
+  // interior / boundary split of the SpMVs that follow a halo exchange
+  {
+    const long long n = m->n_rows, own_lo = pad + hl, own_hi = own_lo + n;
+    unsigned long long* d = nullptr;
+    unsigned long long h[2] = {0ULL, (unsigned long long)n};
+    CK(cudaMalloc(&d, sizeof(h)));
+    CK(cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice));
+    if (n > 0) halo_rows_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(m->rp, m->ci, n, own_lo, own_hi, d);
+    CK(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    long long b0 = (long long)h[0], b1 = (long long)h[1];  // rows [b0, b1) read no halo column
+    // PBS_SPLIT_TEST=k (tests): treat the first and last k blocks as boundary
+    // rows even without halos, so one GPU exercises the split schedule
+    const char* st = getenv("PBS_SPLIT_TEST");
+    const long long force = st ? atoll(st) : 0;
+    if (force > 0) {
+      b0 = std::max(b0, force * kPipeRows);
+      b1 = std::min(b1, n - force * kPipeRows);
+    }
+    P.L0 = (b0 + kPipeRows - 1) / kPipeRows * kPipeRows;
+    P.L1 = b1 >= n ? n : b1 / kPipeRows * kPipeRows;
+    const char* sp = getenv("PBS_SPLIT");  // PBS_SPLIT=0: exchange first, then one SpMV over all rows
+    const bool allow = !(sp && atoi(sp) == 0);
+    P.split = allow && (dist->nranks > 1 || force > 0) && P.L1 > P.L0 && (P.L0 > 0 || P.L1 < n);
+  }
   return PBS_OK;
 }
