@@ -173,6 +173,21 @@ _TRACE_NAMES_BY_METHOD = {"bicgstab": ("x", "r", "p", "t", "Ap", "At"),
                           "pbicgstab": ("x", "r", "p", "s", "z", "q", "y", "w", "t", "v")}
 
 
+def _host_result(n):
+    """The returned x: page-locked host memory from torch's caching host
+    allocator (reused once the caller drops an earlier result), so the
+    device->host copy of x runs at DMA speed with no page faults.  The array
+    keeps its block alive; the caller owns it like any other ndarray."""
+    try:
+        import torch
+
+        if torch.cuda.is_available():
+            return torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:  # pragma: no cover - pinned memory unavailable
+        pass
+    return np.empty(n)
+
+
 def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
@@ -216,7 +231,7 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
             cb_keep = _lib.TRACE_FN(_cb)
             cfg.trace_fn = cb_keep
         slots = config.max_iters + 1
-        x = np.empty(n)
+        x = _host_result(n)
         rel = np.empty(slots)
         flags = np.zeros(slots, dtype=np.uint8)
         coef = np.empty((slots, 4))

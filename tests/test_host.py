@@ -180,3 +180,28 @@ def test_pbicgstab_counters_follow_the_oracle_stages():
                   method="pbicgstab", tol=1e-10, max_iters=10)
     assert o["status"] == "breakdown" and o["failure_iter"] == 0 and o["n_spmv"] == 2
     assert synthesize("pbicgstab", 0, True, set(), stop_stage=1).n_spmv == 2
+
+
+@pytest.mark.parametrize("bad", [np.nan, np.inf, -np.inf])
+@pytest.mark.parametrize("pos", [0, 17, 4095])
+def test_check_finite_names_first_bad_index(bad, pos):
+    """linalg.py:142-146: the v.v fast path must not hide any non-finite entry,
+    and the error names the first bad index."""
+    from paper_2108_10591_b200.linalg import NonFiniteVectorError, check_finite
+
+    v = np.random.default_rng(pos).standard_normal(4096)
+    v[pos] = bad
+    v[-1] = np.nan  # a later bad entry: the first one is reported
+    with pytest.raises(NonFiniteVectorError) as ei:
+        check_finite(v, "right-hand side")
+    assert ei.value.index == pos
+
+
+def test_check_finite_passes_finite_overflowing_and_empty():
+    from paper_2108_10591_b200.linalg import check_finite
+
+    huge = np.full(8, 1e300)  # v.v overflows to inf: the exact scan clears it
+    assert check_finite(huge) is huge
+    assert check_finite(np.empty(0)).size == 0
+    ints = np.arange(5)
+    assert check_finite(ints) is ints
