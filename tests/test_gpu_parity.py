@@ -606,3 +606,21 @@ def test_workspace_reuse_across_uploads(pb):
     assert np.array_equal(graphed.x, eager.x)
     assert graphed.iterations == eager.iterations
     assert not np.array_equal(graphed.x, first.x)
+
+
+def test_result_x_owned_across_solves(pb):
+    """The returned x lives in page-locked host memory from torch's caching
+    host allocator: each outcome owns its block while it is alive, so later
+    solves (which reuse freed blocks) never overwrite an earlier x."""
+    spec, A, b, x0, g = gc.load_case("cd3d16_pbicgsafe", orc.spmv)
+    cfg = _cfg(pb, spec)
+    first = pb.solve(A, b, config=cfg)
+    keep = first.x.copy()
+    second = pb.solve(A, 2.0 * b, config=cfg)
+    for _ in range(3):  # churn the allocator: freed blocks come back
+        pb.solve(A, 3.0 * b, config=cfg)
+    assert first.x.ctypes.data != second.x.ctypes.data
+    assert np.array_equal(first.x, keep)
+    assert first.x.flags.writeable and first.x.shape == (A.n_rows,)
+    first.x[:] = 0.0  # the caller may write it
+    assert not np.array_equal(second.x, first.x)
