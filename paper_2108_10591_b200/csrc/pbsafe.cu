@@ -508,17 +508,6 @@ static int pipe_slots_cap() {
   static int v = env_int("PBS_PIPE_SLOTS", 2, 2, kMaxStages);
   return v;
 }
-// PBS_PIPE_CAHEAD=1: single-chunk blocks issue their matrix chunk ahead of
-// the block-slot wait, into the extra chunk stages the budget allows
-static int pipe_chunk_ahead() {
-  static int v = env_int("PBS_PIPE_CAHEAD", 0, 0, 1);
-  return v;
-}
-// PBS_PIPE_ESPLIT=1: staged epilogue inputs on their own barrier
-static int pipe_ein_split() {
-  static int v = env_int("PBS_PIPE_ESPLIT", 0, 0, 1);
-  return v;
-}
 static int pipe_extra_chunks() {  // chunk stages beyond the block slots
   static int v = env_int("PBS_PIPE_XCHUNK", 0, 0, 4);
   return v;
@@ -701,9 +690,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     // any launch starting on a block boundary can use them
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, (lo % kPipeRows) == 0 ? m->wc : nullptr};
     // staged x windows need the window-local columns; otherwise gather x
-    XWin W = A.wc ? m->xwin : XWin{};
-    W.cahead = pipe_chunk_ahead();
-    W.esplit = pipe_ein_split();
+    const XWin W = A.wc ? m->xwin : XWin{};
     int bslots, cstages, ctas, chunk, stage_in;
     size_t smem;
     int rc = pipe_config<Epi>(L.ctx, W, A.wc ? 2 : 4, m->blk_nnz_max, &bslots, &cstages, &smem, &ctas, &chunk,

@@ -613,14 +613,6 @@ struct XWin {
   // block's new columns.
   int band_s;
   int band_lo, band_hi;
-  // 1: a single-chunk block's matrix chunk is issued as soon as its chunk
-  // stage frees, ahead of the wait for the block slot (PBS_PIPE_CAHEAD)
-  int cahead;
-  // 1: the staged epilogue inputs complete their own barrier (efull), so the
-  // consumers start a block's products once row_ptr, x windows and the chunk
-  // have landed and wait for the epilogue inputs only at the row's end
-  // (PBS_PIPE_ESPLIT)
-  int esplit;
 };
 
 struct BlockHdr {
@@ -679,7 +671,6 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
   uint64_t* cempty = cfull + kMaxStages;
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
-  uint64_t* efull = bempty + kMaxStages;  // staged epilogue inputs (W.esplit)
   // stage_in = 0: the epilogue inputs are not staged (their slot space goes
   // to a second resident CTA when x windows are wide, e.g. 27-point rows);
   // consumers load them from global memory while the row's products run
@@ -697,13 +688,10 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
     for (int s = 0; s < bslots; ++s) {
       mbar_init(&bfull[s], 1);
       mbar_init(&bempty[s], kConsumerWarps);
-      mbar_init(&efull[s], 1);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  // epilogue inputs on their own barrier
-  const bool esplit = stage_in && Epi::kInStaged > 0 && W.esplit;
   const long long nrows = A.row_hi - A.row_lo;
   const long long nblk_all = (nrows + kPipeRows - 1) / kPipeRows;
   // blocks of this CTA: strided (blockIdx.x, + gridDim.x, ...) or, in band
@@ -797,14 +785,10 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
         issued = (int)cfirst;
         if (!gate()) return;
       }
-      if (W.cahead && !band && nch == 1 && cfirst == 0) {
-        issue_chunk(0);
-        cfirst = 1;
-      }
       // x windows of this block (every lane computes them; lane 1+c copies window c)
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = brp + (stage_in && !esplit ? Epi::kInStaged * bin : 0u);
+      uint32_t total = brp + (stage_in ? Epi::kInStaged * bin : 0u);
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0x7fffffff;
@@ -860,7 +844,6 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
 #pragma unroll
         for (int c = 0; c < kMaxWin; ++c) bh->ws[c] = wlo[c];
         mbar_arrive_expect_tx(&bfull[bs], total);
-        if (esplit) mbar_arrive_expect_tx(&efull[bs], Epi::kInStaged * bin);
       }
       __syncwarp();
       if (lane == 0) {
@@ -882,8 +865,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
         }
       } else if (stage_in && lane >= 8 && lane < 8 + Epi::kInStaged) {
         const int e = lane - 8;
-        bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin,
-                 esplit ? &efull[bs] : &bfull[bs]);
+        bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
       }
       if (++bs == bslots) {
         bs = 0;
@@ -981,7 +963,6 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
     if (t < nr) {
       const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
       if (stage_in) {
-        if (esplit) mbar_wait(&efull[bs], bph);
 #pragma unroll
         for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
       }
