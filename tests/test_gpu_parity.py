@@ -624,3 +624,48 @@ def test_result_x_owned_across_solves(pb):
     assert first.x.flags.writeable and first.x.shape == (A.n_rows,)
     first.x[:] = 0.0  # the caller may write it
     assert not np.array_equal(second.x, first.x)
+
+
+def _convdiff2d(pb, k):
+    from paper_2108_10591_b200 import problems
+
+    st = problems.convdiff_stencil(2, k, (1.0, 1.0))
+    rp, ci, v = problems.stencil_csr(st)
+    n = len(rp) - 1
+    return pb.CsrMatrix(n, n, rp, ci, v), orc.spmv(rp, ci, v, np.ones(n))
+
+
+def test_pipelined_matches_single_reduction_early_fast_path(pb):
+    """test_solvers.py:129-136 on the device fast path (tree-mode dots, graphs):
+    p-BiCGSafe and ssBiCGSafe2 give the same iterates in exact arithmetic, so
+    their first 20 recurrence residuals agree to 1e-6."""
+    A, b = _convdiff2d(pb, 30)
+    cfg = pb.SolverConfig(tol=1e-30, max_iters=20)
+    o1 = pb.solve(A, b, method="ssbicgsafe2", config=cfg)
+    o2 = pb.solve(A, b, method="pbicgsafe", config=cfg)
+    assert len(o1.history) == len(o2.history) == 21
+    for r1, r2 in zip(o1.history, o2.history):
+        assert r2.rel_res_recur == pytest.approx(r1.rel_res_recur, rel=1e-6), r1.iter
+
+
+def test_pipelined_recurrences_track_true_products_fast_path(pb):
+    """test_solvers.py:142-158 on the device fast path: the carried products
+    s = A r, q = A o, w = A u, l = A t, g = A y stay within
+    1e-8 (1 + ||A||_inf ||source||) of the true products for 30 iterations."""
+    A, b = _convdiff2d(pb, 20)
+    rp, ci, v = A.row_ptr, A.col_idx, A.values
+    row_abs = np.add.reduceat(np.abs(v), rp[:-1])
+    norm_a = float(row_abs.max())
+    failures = []
+
+    def hook(i, ws):
+        if i > 30:
+            return
+        for carried, source in (("s", "r"), ("q", "o"), ("w", "u"), ("l", "t"), ("g", "y")):
+            err = np.linalg.norm(ws[carried] - orc.spmv(rp, ci, v, ws[source]))
+            scale = 1.0 + norm_a * np.linalg.norm(ws[source])
+            if err > 1e-8 * scale:
+                failures.append((i, carried, err, scale))
+
+    pb.solve(A, b, config=pb.SolverConfig(tol=1e-12, max_iters=31), trace_hook=hook)
+    assert not failures, failures[:5]
