@@ -162,7 +162,7 @@ def run_reference(args):
                                    f"{threads} threads"},
         "e2e": {"value": val, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -408,7 +408,7 @@ def run_ours(args):
             "gpu_launches": launches,
             "clocks": clocks,
         }
-        print(json.dumps(line))
+        emit(line)
     if dsys is not None:
         dsys.close()
     if world > 1:
@@ -416,7 +416,24 @@ def run_ours(args):
     return 0
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line, on the process's original stdout.  Everything else
+    native code prints (NCCL's version banner under NCCL_DEBUG, driver
+    messages) goes to stderr, so stdout carries exactly one line."""
+    out = _JSON_OUT if _JSON_OUT is not None else sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)  # fd 1 -> stderr for native libraries and stray prints
+    sys.stdout = sys.stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
