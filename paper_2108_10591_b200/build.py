@@ -18,10 +18,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpbsafe.so")
-SOURCES = [os.path.join(CSRC, "pbsafe.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("common.cuh", "spmv.cuh", "vec.cuh", "finalize.cuh",
+# one translation unit per part of the library, compiled in parallel
+SOURCES = [os.path.join(CSRC, f) for f in ("core.cu", "solve.cu", "prod.cu", "pstab.cu", "dist.cu")]
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("host.h", "common.cuh", "spmv.cuh", "vec.cuh", "finalize.cuh",
                                                   "ptx.cuh")] + [
     os.path.join(ROOT, "include", "pbsafe.h")]
+OBJDIR = os.path.join(ROOT, "build", "pbsafe")
 
 
 def nvcc() -> str:
@@ -35,7 +37,7 @@ def flags() -> list[str]:
     return [
         "-O3", "-std=c++17", "-lineinfo", "-fmad=false",
         "-gencode", "arch=compute_100a,code=sm_100a",
-        "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared",
+        "-Xcompiler", "-fPIC,-fvisibility=hidden",
         "-Xptxas", "-v",
         "-I", os.path.join(ROOT, "include"),
     ]
@@ -51,16 +53,34 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJDIR, exist_ok=True)
+
+    def compile_one(src):
+        obj = os.path.join(OBJDIR, os.path.basename(src) + ".o")
+        cmd = [nvcc(), *flags(), "-c", "-o", obj, src]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        results = list(pool.map(compile_one, SOURCES))
+    info = []
+    for (obj, proc), src in zip(results, SOURCES):
+        if proc.returncode != 0:
+            sys.stderr.write(proc.stdout + proc.stderr)
+            raise RuntimeError(f"nvcc failed compiling {os.path.basename(src)}")
+        info.append(proc.stderr)
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *flags(), "-o", tmp, *SOURCES]
+    cmd = [nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
+           "-o", tmp, *[obj for obj, _ in results]]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         sys.stderr.write(proc.stdout + proc.stderr)
-        raise RuntimeError("nvcc failed building libpbsafe.so")
+        raise RuntimeError("nvcc failed linking libpbsafe.so")
     with open(os.path.join(HERE, "ptxas_info.txt"), "w") as fh:
-        fh.write(proc.stderr)
+        fh.write("".join(info))
     if verbose:
-        sys.stderr.write(proc.stderr)
+        sys.stderr.write("".join(info))
     os.replace(tmp, LIB)
     return LIB
 

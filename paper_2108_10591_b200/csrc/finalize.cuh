@@ -93,7 +93,7 @@ __device__ __forceinline__ void check_ze(bool first, const double* d, CheckVals*
 
 // Bookkeeping of check j (solvers.py:645-674, 736-739) on precomputed values.
 // One thread.
-__device__ void check_commit(SolverState* st, long long j, const CheckVals& cv, int replaced) {
+static __device__ void check_commit(SolverState* st, long long j, const CheckVals& cv, int replaced) {
   const bool first = j == 0;
   if (first) st->r0_norm = cv.r0_norm;
   const double rel = cv.rel;
@@ -240,7 +240,7 @@ __device__ __forceinline__ double prod_rel(const SolverState* ss, double rr) {  
 }
 
 // the loop-top record and tests of check j (solvers.py:258-263, 324-327)
-__device__ void prod_check(SolverState* ss, long long j) {
+static __device__ void prod_check(SolverState* ss, long long j) {
   const double rel = prod_rel(ss, ss->rr);
   if (ss->record_history) {
     const long long slot = ss->n_records;
@@ -255,7 +255,7 @@ __device__ void prod_check(SolverState* ss, long long j) {
 }
 
 // rec.coefficients of iteration i, then the non-finite test (solvers.py:310-313, 443-446)
-__device__ bool prod_record_coef(SolverState* ss, long long i, double a, double b, double z, double e,
+static __device__ bool prod_record_coef(SolverState* ss, long long i, double a, double b, double z, double e,
                                  bool has_eta) {
   if (ss->record_history) {
     const long long slot = ss->n_records - 1;
@@ -271,7 +271,7 @@ __device__ bool prod_record_coef(SolverState* ss, long long i, double a, double 
 }
 
 // compute_zeta_eta_gpbicg (coefficients.py:109-135); returns a PBS_BD_* or 0
-__device__ int zeta_eta_gpbicg(double a, double b, double c, double d, double e, bool first, double* zeta,
+static __device__ int zeta_eta_gpbicg(double a, double b, double c, double d, double e, bool first, double* zeta,
                                double* eta) {
   if (first || (a == 0.0 && c == 0.0 && d == 0.0)) {
     if (e == 0.0) {
@@ -295,7 +295,7 @@ __device__ int zeta_eta_gpbicg(double a, double b, double c, double d, double e,
 // p-BiCGStab's alpha for the iteration whose loop-top check just passed
 // (ss->iter == i + 1): f / ((r0*, w) + beta*((r0*, s) - omega*(r0*, z))),
 // the recurrence for (r0*, A p), with beta and omega of iteration i - 1
-__device__ void ps_alpha(SolverState* ss) {
+static __device__ void ps_alpha(SolverState* ss) {
   if (!ss->run_all) return;
   const long long i = ss->iter - 1;
   const double gw = ss->dots[DG], sd = ss->dots[DA], zd = ss->dots[DH];
@@ -311,7 +311,7 @@ __device__ void ps_alpha(SolverState* ss) {
 
 // One phase on the shared state copy (thread 0).  i = the iteration whose
 // body is running: its loop-top check was check i, so ss->iter == i + 1.
-__device__ void prod_phase(SolverState* ss, int phase, const double* d) {
+static __device__ void prod_phase(SolverState* ss, int phase, const double* d) {
   const long long i = ss->iter - 1;
   auto brk = [&](int q, int stage) {
     ss->breakdown = q;
@@ -547,7 +547,7 @@ __device__ void reduce_parts(const double* partials, int nparts, int chain, doub
 
 // Multi-GPU local step: reduce this rank's CTA partial records to ONE record
 // of 9 compensated pairs (not rounded), the payload of the all-gather.
-__global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partials, int nparts, double* out) {
+static __global__ void __launch_bounds__(288) reduce_pairs_kernel(const double* partials, int nparts, double* out) {
   constexpr int T = 288 / kNumDots;
   __shared__ Ddbl team[kNumDots][T];
   const int t = threadIdx.x, j = t / T, l = t % T;
@@ -597,7 +597,7 @@ __device__ void finalize_tail(SolverState* st, const double* partials, int npart
 
 // Standalone finalize (1 CTA, 288 threads): reduce (tree or plan chain), then
 // the check for j = st->iter, then advance st->iter.
-__global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const double* partials, int nparts,
+static __global__ void __launch_bounds__(288) finalize_kernel(SolverState* st, const double* partials, int nparts,
                                                        int chain, int replaced, const double* partials2 = nullptr,
                                                        int nparts2 = 0, unsigned mask2 = 0, int rs = 1,
                                                        int fs = kMaxParts, int phase = kPhSafe) {

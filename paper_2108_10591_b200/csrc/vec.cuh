@@ -30,7 +30,7 @@ __device__ __forceinline__ bool gate_after_spine(SolverState* st) {
 // K2: block 1 of the pipelined iteration (solvers.py:678-701, 715) in one
 // pass.  Reads r p u s t y As l g w z x (12 vectors), writes p u w t z y x r
 // (8); o and q stay in registers unless the single-step seam asks for them.
-__global__ void __launch_bounds__(kThreads) k2_update_kernel(VecPtrs V, long long n, SolverState* st,
+static __global__ void __launch_bounds__(kThreads) k2_update_kernel(VecPtrs V, long long n, SolverState* st,
                                                              int store_temps) {
   if (!gate_after_spine(st)) return;
   const double alpha = st->alpha, beta = st->beta, zeta = st->zeta, eta = st->eta;
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kThreads) k2_update_kernel(VecPtrs V, long lon
 }
 
 // p, o, u (solvers.py:678-683; also ssBiCGSafe2 solvers.py:563-568)
-__global__ void __launch_bounds__(kThreads) pou_kernel(VecPtrs V, long long n, SolverState* st) {
+static __global__ void __launch_bounds__(kThreads) pou_kernel(VecPtrs V, long long n, SolverState* st) {
   if (!gate_after_spine(st)) return;
   const double beta = st->beta, zeta = st->zeta, eta = st->eta;
   double *__restrict__ p = V.v[VP], *__restrict__ u = V.v[VU], *__restrict__ o = V.v[VO];
@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(kThreads) pou_kernel(VecPtrs V, long long n, S
 }
 
 // t, z, y, x after q = A o, w = A u were recomputed (solvers.py:694-701)
-__global__ void __launch_bounds__(kThreads) tzyx_kernel(VecPtrs V, long long n, SolverState* st) {
+static __global__ void __launch_bounds__(kThreads) tzyx_kernel(VecPtrs V, long long n, SolverState* st) {
   if (!gate_all(st)) return;
   const double alpha = st->alpha, zeta = st->zeta, eta = st->eta;
   double *__restrict__ t = V.v[VT], *__restrict__ z = V.v[VZ], *__restrict__ y = V.v[VY],
@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(kThreads) tzyx_kernel(VecPtrs V, long long n, 
 // after r0 = b - A x0: p0 = r + 0*(p - ...) on the zeroed workspace (the
 // first iteration's p update, solvers.py:265 / 381) and the partials of
 // (r, r) (solvers.py:244 / 365) -> r0_norm, f, check 0
-__global__ void __launch_bounds__(kThreads) prod_setup_kernel(VecPtrs V, long long n, SolverState* st, int gp,
+static __global__ void __launch_bounds__(kThreads) prod_setup_kernel(VecPtrs V, long long n, SolverState* st, int gp,
                                                               double* partials, int fuse) {
   __shared__ int go;
   if (threadIdx.x == 0) go = gate_all(st);
@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) prod_setup_kernel(VecPtrs V, long lo
 }
 
 // BiCGStab t = r - alpha*Ap (solvers.py:279)
-__global__ void __launch_bounds__(kThreads) stab_t_kernel(VecPtrs V, long long n, SolverState* st) {
+static __global__ void __launch_bounds__(kThreads) stab_t_kernel(VecPtrs V, long long n, SolverState* st) {
   if (!gate_all(st)) return;
   const double alpha = st->alpha;
   double *__restrict__ t = V.v[VT];
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kThreads) stab_t_kernel(VecPtrs V, long long n
 // then (with_p) the next iteration's p = r + beta*(p - omega*Ap)
 // (solvers.py:265).  Gated on the omega phase's go-ahead: the update runs
 // even when the beta guard or check i+1 stops the solve.
-__global__ void __launch_bounds__(kThreads) stab_xrp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
+static __global__ void __launch_bounds__(kThreads) stab_xrp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
   if (dev_err(st) || !st->upd) return;
   const double alpha = st->alpha, omega = st->omega, beta = st->beta;
   double *__restrict__ x = V.v[VX], *__restrict__ r = V.v[VR], *__restrict__ p = V.v[VP];
@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kThreads) stab_xrp_kernel(VecPtrs V, long long
 // the p update at the top of the next iteration, when a trace hook had to
 // see the old p: BiCGStab p = r + beta*(p - omega*Ap), GPBi-CG
 // p = r + beta*(p - u) (solvers.py:265, 381)
-__global__ void __launch_bounds__(kThreads) prod_p_kernel(VecPtrs V, long long n, SolverState* st, int gp) {
+static __global__ void __launch_bounds__(kThreads) prod_p_kernel(VecPtrs V, long long n, SolverState* st, int gp) {
   if (!gate_all(st)) return;
   const double beta = st->beta, omega = st->omega;
   double *__restrict__ p = V.v[VP];
@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(kThreads) prod_p_kernel(VecPtrs V, long long n
 
 // GPBi-CG y = t - r - alpha*w + alpha*Ap; u = t - r + beta*u (stash);
 // t = r - alpha*Ap (solvers.py:394-399) in one pass
-__global__ void __launch_bounds__(kThreads) gp_yut_kernel(VecPtrs V, long long n, SolverState* st) {
+static __global__ void __launch_bounds__(kThreads) gp_yut_kernel(VecPtrs V, long long n, SolverState* st) {
   if (!gate_all(st)) return;
   const double alpha = st->alpha, beta = st->beta;
   double *__restrict__ y = V.v[VY], *__restrict__ u = V.v[VU], *__restrict__ t = V.v[VT];
@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(kThreads) gp_yut_kernel(VecPtrs V, long long n
 // GPBi-CG u = zeta*Ap + eta*u; z = zeta*r + eta*z - alpha*u; x = x + alpha*p
 // + z; r = t - eta*y - zeta*At (solvers.py:416-419), with the partials of
 // the third phase f = (r0*, r), rr = (r, r) (solvers.py:421-423)
-__global__ void __launch_bounds__(kThreads) gp_uzxr_kernel(VecPtrs V, long long n, SolverState* st,
+static __global__ void __launch_bounds__(kThreads) gp_uzxr_kernel(VecPtrs V, long long n, SolverState* st,
                                                            double* partials, int fuse, int phase) {
   __shared__ int go;
   if (threadIdx.x == 0) go = gate_all(st);
@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(kThreads) gp_uzxr_kernel(VecPtrs V, long long 
 
 // GPBi-CG w = At + beta*Ap (solvers.py:440), then (with_p) the next
 // iteration's p = r + beta*(p - u) (solvers.py:381)
-__global__ void __launch_bounds__(kThreads) gp_wp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
+static __global__ void __launch_bounds__(kThreads) gp_wp_kernel(VecPtrs V, long long n, SolverState* st, int with_p) {
   if (!gate_all(st)) return;
   const double beta = st->beta;
   double *__restrict__ w = V.v[VW], *__restrict__ p = V.v[VP];
@@ -248,7 +248,7 @@ struct DotPairs {
   const double* y[kNumDots];
   unsigned mask;
 };
-__global__ void dots_pairs_plan_kernel(const long long* bounds, DotPairs P, double* partials,
+static __global__ void dots_pairs_plan_kernel(const long long* bounds, DotPairs P, double* partials,
                                        const SolverState* st) {
   if (st && !gate_all(st)) return;
   const int j = threadIdx.x;
@@ -264,7 +264,7 @@ __global__ void dots_pairs_plan_kernel(const long long* bounds, DotPairs P, doub
 
 // ---------------------------------------------------------------------------
 // kernel-table entry points (kernels.py:110-137), kinds as in pbsafe.h
-__global__ void __launch_bounds__(kThreads) lincomb_kernel(int kind, long long n, double* out, double s0,
+static __global__ void __launch_bounds__(kThreads) lincomb_kernel(int kind, long long n, double* out, double s0,
                                                            double s1, double s2, double s3,
                                                            const double* a, const double* b,
                                                            const double* c, const double* d) {
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads) lincomb_kernel(int kind, long long n
 
 // tree dot over [lo, hi): per-thread strided partial, block tree, written to
 // partials[blockIdx]; finished by dot_final_kernel (deterministic shape)
-__global__ void __launch_bounds__(kThreads) dot_partial_kernel(const double* x, const double* y, long long lo,
+static __global__ void __launch_bounds__(kThreads) dot_partial_kernel(const double* x, const double* y, long long lo,
                                                                long long hi, double* partials) {
   double acc = 0.0;
   const long long stride = (long long)gridDim.x * kThreads;
@@ -305,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) dot_partial_kernel(const double* x, 
   }
 }
 
-__global__ void dot_final_kernel(const double* partials, int nparts, double* out) {
+static __global__ void dot_final_kernel(const double* partials, int nparts, double* out) {
   double acc = 0.0;
   for (int i = threadIdx.x; i < nparts; i += 32) acc = add(acc, partials[i]);
   for (int o = 16; o > 0; o >>= 1) acc = add(acc, __shfl_xor_sync(0xffffffffu, acc, o));
@@ -313,7 +313,7 @@ __global__ void dot_final_kernel(const double* partials, int nparts, double* out
 }
 
 // batch of the 9 safe dots, compensated tree, into record blk of partials
-__global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const double* s, const double* y,
+static __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const double* s, const double* y,
                                                               const double* r, const double* r0s,
                                                               const double* t, double* partials,
                                                               const SolverState* st) {
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads) dots9_tree_kernel(long long n, const
 
 // The batch of the next check as its own streaming kernel (s y r r0s t ->
 // 9 compensated dots), with the check fused into the last CTA's tail.
-__global__ void __launch_bounds__(kThreads) dots9_check_kernel(long long n, const double* __restrict__ s,
+static __global__ void __launch_bounds__(kThreads) dots9_check_kernel(long long n, const double* __restrict__ s,
                                                                const double* __restrict__ y,
                                                                const double* __restrict__ r,
                                                                const double* __restrict__ r0s,
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads) dots9_check_kernel(long long n, cons
 // PartitionPlan chains (reduction.py:282-283 with kernels.py:103-107): block w
 // handles range [bounds[w], bounds[w+1]); thread j < 9 sums pair j
 // sequentially in ascending index order -> field 2j of record w.
-__global__ void dots9_plan_kernel(const long long* bounds, const double* s, const double* y,
+static __global__ void dots9_plan_kernel(const long long* bounds, const double* s, const double* y,
                                   const double* r, const double* r0s, const double* t,
                                   double* partials, const SolverState* st) {
   if (st && !gate_all(st)) return;
