@@ -140,6 +140,13 @@ typedef struct {
   double* events_out;
   int64_t events_cap;
   int64_t* events_count;
+  /* multi-GPU schedule evidence from the device clock (%globaltimer): per
+   * partition and iteration i < stamps_cap, 8 doubles in ns from the solve's
+   * first stamp (-1: absent): As start/end, Aw start/end, publish of check i
+   * start/end, finalize of check i start/end.  NULL: off. */
+  double* stamps_out;
+  int64_t stamps_cap;
+  int64_t* stamps_count;
 } pbs_config;
 
 #define PBS_NUM_KERNEL_KINDS 8 /* K1 As, K2 update, K3 Aw+epilogue, F finalize,
@@ -245,17 +252,50 @@ int pbs_k_lincomb(pbs_ctx* ctx, int32_t kind, int64_t n, double* out, const doub
  * iteration count are identical on every rank.  NCCL is loaded at run time
  * (libnccl.so.2, e.g. the copy torch already loaded). */
 typedef struct pbs_dist pbs_dist;
+#define PBS_TRANSPORT_P2P 0  /* halos: copy-engine pushes into IPC-mapped peer
+                                memory + stream-memory-op flags; reduction:
+                                peer stores of each rank's record + flags */
+#define PBS_TRANSPORT_NCCL 1 /* ncclSend/Recv halos, ncclAllGather of the records */
+#define PBS_DIST_BLOB_BYTES 256
 int pbs_nccl_unique_id(void* out128);
-/* two NCCL communicators: halo exchange and the dot all-gather (they run on
- * different streams concurrently, so they must not share a communicator) */
-int pbs_dist_init(pbs_ctx* ctx, int32_t nranks, int32_t rank, const void* id_halo128,
+/* a partition's link to its group of nranks (at most 64).  The NCCL
+ * transport needs two unique ids (halo exchange and the record all-gather run
+ * on different streams, so they must not share a communicator); P2P ignores
+ * them (NULL). */
+int pbs_dist_init(pbs_ctx* ctx, int32_t nranks, int32_t rank, int32_t transport, const void* id_halo128,
                   const void* id_reduce128, pbs_dist** dist);
 int pbs_dist_destroy(pbs_dist* dist);
-/* sends: nsend triples (peer, offset within the own segment, length);
- * recvs: nrecv triples (peer, extended-space offset, length) */
+/* SMs this partition's kernels may fill (0: all): a loopback group of N on
+ * one device gives each partition sms / N, like N smaller GPUs */
+int pbs_dist_set_sm_limit(pbs_dist* dist, int32_t sms);
+/* sends: nsend quadruples (peer, offset within the own segment, length,
+ * extended-space offset on the peer); recvs: nrecv triples (peer,
+ * extended-space offset, length).  Allocates the partition's workspace. */
 int pbs_mat_set_partition(pbs_mat* mat, pbs_dist* dist, int64_t n_global, int64_t row_lo, int64_t hl,
                           int64_t hr, int32_t nsend, const int64_t* sends, int32_t nrecv,
                           const int64_t* recvs);
+/* one process per GPU: export this partition (PBS_DIST_BLOB_BYTES: IPC
+ * handles of its workspace and mailbox), gather every rank's blob (rank
+ * order), connect (maps the peers), then barrier before the first solve */
+int pbs_dist_export(pbs_mat* mat, void* blob_out);
+int pbs_dist_connect(pbs_mat* mat, const void* blobs);
+/* loopback group: partitions 0..n-1 of one system held by this process on
+ * one device, linked directly (the same schedule, kernels and transport) */
+int pbs_dist_connect_local(pbs_mat** mats, int32_t n);
+/* solve on a loopback group: per-partition device pointers to the own
+ * segments of b, x0 (NULL: zero) and x; history and result as pbs_solve.
+ * (One process per GPU: pbs_solve / pbs_solve_dev on its partition.) */
+int pbs_solve_group(pbs_mat** mats, int32_t n, int32_t method, const double* const* d_b,
+                    const double* const* d_x0, const pbs_config* cfg, double* const* d_x, double* hist_rel,
+                    uint8_t* hist_flags, double* hist_coef, pbs_result* result);
+/* partitioned SpMV y = A x (own segments; halos exchanged by the group's
+ * transport); nonfinite_index[p]: first non-finite local row or -1 */
+int pbs_spmv_group(pbs_mat** mats, int32_t n, const double* const* d_x, double* const* d_y,
+                   int64_t* nonfinite_index);
+/* rows [row_lo, row_hi) of a whole-grid stencil operator as a partition slab:
+ * SpMV inputs in the extended space [pad | hl | own | hr] (like a CSR slab);
+ * pbs_stencil_to_csr of a slab gives its CSR with extended-space columns */
+int pbs_stencil_slab(pbs_mat* stencil, int64_t row_lo, int64_t row_hi, int64_t hl, int64_t hr, pbs_mat** slab);
 
 /* ---- device batch reduction --------------------------------------------- */
 /* 9 dots of the safe batch over device vectors s y r r0s t, packed a..h,r */

@@ -36,8 +36,13 @@ EXPORTS = (
     "pbs_csr_upload", "pbs_stencil_create", "pbs_mat_free", "pbs_mat_info", "pbs_spmv_dev",
     "pbs_solve", "pbs_solve_dev", "pbs_step_dev", "pbs_k_spmv_range", "pbs_k_dot_range",
     "pbs_k_lincomb", "pbs_dot_batch_dev", "pbs_nccl_unique_id", "pbs_dist_init", "pbs_dist_destroy",
-    "pbs_mat_set_partition", "pbs_stencil_to_csr",
+    "pbs_mat_set_partition", "pbs_stencil_to_csr", "pbs_dist_set_sm_limit", "pbs_dist_export",
+    "pbs_dist_connect", "pbs_dist_connect_local", "pbs_solve_group", "pbs_spmv_group", "pbs_stencil_slab",
 )
+TRANSPORTS = {"p2p": 0, "nccl": 1}
+DIST_BLOB_BYTES = 256
+# schedule-evidence stamp words per iteration (pbs_config.stamps_out)
+STAMP_WORDS = ("as_start", "as_end", "aw_start", "aw_end", "pub_start", "pub_end", "fin_start", "fin_end")
 
 
 class NativeUnavailable(RuntimeError):
@@ -60,6 +65,7 @@ class Config(C.Structure):
         ("plan_workers", C.c_int32), ("use_graphs", C.c_int32), ("timing", C.c_int32),
         ("pad", C.c_int32), ("trace_fn", TRACE_FN), ("trace_user", C.c_void_p),
         ("events_out", C.c_void_p), ("events_cap", C.c_int64), ("events_count", C.POINTER(C.c_int64)),
+        ("stamps_out", C.c_void_p), ("stamps_cap", C.c_int64), ("stamps_count", C.POINTER(C.c_int64)),
     ]
 
 
@@ -120,7 +126,14 @@ def load(build_if_missing: bool = True):
             "pbs_k_lincomb": ([p, i32, i64, p, p, p, p, p, p], C.c_int),
             "pbs_dot_batch_dev": ([p, i64, p, p, p, p, p, i32, i32, p], C.c_int),
             "pbs_nccl_unique_id": ([p], C.c_int),
-            "pbs_dist_init": ([p, i32, i32, p, p, pp], C.c_int),
+            "pbs_dist_init": ([p, i32, i32, i32, p, p, pp], C.c_int),
+            "pbs_dist_set_sm_limit": ([p, i32], C.c_int),
+            "pbs_dist_export": ([p, p], C.c_int),
+            "pbs_dist_connect": ([p, p], C.c_int),
+            "pbs_dist_connect_local": ([p, i32], C.c_int),
+            "pbs_solve_group": ([p, i32, i32, p, p, C.POINTER(Config), p, p, p, p, C.POINTER(Result)], C.c_int),
+            "pbs_spmv_group": ([p, i32, p, p, p], C.c_int),
+            "pbs_stencil_slab": ([p, i64, i64, i64, i64, pp], C.c_int),
             "pbs_dist_destroy": ([p], C.c_int),
             "pbs_mat_set_partition": ([p, p, i64, i64, i64, i64, i32, p, i32, p], C.c_int),
             "pbs_stencil_to_csr": ([p, pp], C.c_int),

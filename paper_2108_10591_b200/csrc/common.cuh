@@ -54,6 +54,11 @@ struct HostMirror {
   volatile long long iter;
   volatile int run_all;
   volatile int err;
+  // the check that stopped the solve (-1 while running).  The multi-GPU
+  // schedule writes it before iter (with a system fence), so a host that has
+  // seen iter > c knows whether the solve stopped at a check <= c; every
+  // rank's device state is identical, so every rank takes the same decision.
+  volatile long long stop_check;
 };
 
 // Device-resident solver state.  Written by the single-CTA finalize kernel
@@ -85,9 +90,16 @@ struct SolverState {
   long long failure_iter;
   long long iterations;
   long long n_records;
+  long long stop_check;  // the check that stopped the solve (-1 while running)
   // non-finite SpMV output (NonFiniteVectorError): first row, tag
   unsigned long long nf_row;
   int nf_tag;
+  // multi-GPU: the group's first non-finite SpMV output (every partition
+  // learns it from the records of the next check): its encoded tag and
+  // global row
+  int remote_err;
+  int err_tag;
+  long long err_row;
   unsigned int done_ctas;  // last-CTA ticket of the fused finalize (reset by the last CTA)
   // history (device arrays, max_iters+1 slots)
   double* hist_rel;
@@ -121,6 +133,13 @@ __device__ __forceinline__ void report_nonfinite(SolverState* st, int tag, long 
 // ticket; take the ticket, then read every record — need no more than
 // acq_rel; __threadfence() is the stronger, slower fence.sc)
 __device__ __forceinline__ void fence_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// device-wide nanosecond clock (schedule evidence stamps)
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }

@@ -17,7 +17,10 @@ void free_ws(Workspace* ws) {
   if (!ws) return;
   free_graphs(ws);
   pbs_ctx* ctx = ws->ctx;
-  pool_free(ctx, ws->base);
+  if (ws->base_ipc)
+    cudaFree(ws->base);
+  else
+    pool_free(ctx, ws->base);
   pool_free(ctx, ws->partials);
   pool_free(ctx, ws->partials12);
   pool_free(ctx, ws->plan_bounds);
@@ -77,7 +80,12 @@ int ensure_ws(pbs_mat* m, long long hist_slots) {
     ws->own_off = m->part.dist ? m->part.hl + (m->part.hl & 1) : 0;  // even: 16-byte aligned
     // +2: aligned bulk-copy over-read; even own offset keeps 16-byte alignment
     ws->stride = ((size_t)ws->n_ext + 4 + 31) / 32 * 32;
-    CK(pool_alloc(ctx, &ws->base, sizeof(double) * ws->stride * kNumVecs));
+    if (m->part.dist) {  // peers copy halos straight into it (CUDA IPC)
+      CK(cudaMalloc(&ws->base, sizeof(double) * ws->stride * kNumVecs));
+      ws->base_ipc = true;
+    } else {
+      CK(pool_alloc(ctx, &ws->base, sizeof(double) * ws->stride * kNumVecs));
+    }
     CK(cudaMemsetAsync(ws->base, 0, sizeof(double) * ws->stride * kNumVecs, ctx->stream));
     for (int k = 0; k < kNumVecs; ++k) {
       ws->X.v[k] = ws->base + ws->stride * k;
@@ -255,7 +263,7 @@ int collect_result(pbs_mat* m, int method, const pbs_config* cfg, pbs_result* re
   res->r0_norm = out.r0_norm;
   res->nonfinite_index = -1;
   if (out.nf_row != (unsigned long long)kNoError) {
-    res->nonfinite_tag = out.nf_tag;
+    res->nonfinite_tag = out.nf_tag & 0xff;  // the multi-GPU schedule adds the launch sequence above
     res->nonfinite_index = (long long)out.nf_row + (m->part.dist ? m->part.row_lo : 0);
     return set_err(ctx, PBS_ERR_NONFINITE, "non-finite SpMV output");
   }
@@ -649,6 +657,9 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
   m->n_rows = m->n_cols = n;
   StencilView& S = m->sv;
   S.n = n;
+  S.g0 = 0;
+  S.xlo = 0;
+  S.xhi = n;
   S.k = k;
   S.k2 = k * k;
   S.dk = make_fastdiv(S.k);
@@ -754,7 +765,8 @@ PBS_EXPORT int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t 
 
 
 // ---- stencil -> CSR on the device
-__device__ __forceinline__ bool stencil_in(const StencilView& S, long long i, int p) {
+__device__ __forceinline__ bool stencil_in(const StencilView& S, long long li, int p) {
+  const long long i = li + S.g0;  // grid row of slab-local row li
   int c[3] = {0, 0, 0};
   if (S.dim == 3) {
     const long long z = S.dk2.div(i), rem = i - z * S.k2, yy = S.dk.div(rem);
@@ -786,14 +798,15 @@ __global__ void stencil_count_kernel(const __grid_constant__ StencilView S, long
   if (blockIdx.x == 0 && threadIdx.x == 0) counts[0] = 0;
 }
 
+// col_off: a slab's columns are extended-space indices, own segment at col_off
 __global__ void stencil_fill_kernel(const __grid_constant__ StencilView S, const long long* rp, int* ci,
-                                    double* v) {
+                                    double* v, long long col_off) {
   const long long stride = (long long)gridDim.x * blockDim.x;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.n; i += stride) {
     long long k = rp[i];
     for (int p = 0; p < S.npts; ++p)
       if (stencil_in(S, i, p)) {
-        ci[k] = (int)(i + S.foff[p]);
+        ci[k] = (int)(col_off + i + S.foff[p]);
         v[k] = S.coef[p];
         ++k;
       }
@@ -820,8 +833,10 @@ PBS_EXPORT int pbs_stencil_to_csr(pbs_mat* st, pbs_mat** out) {
   if (nnz > 0x7fffffffffffLL) return set_err(ctx, PBS_ERR_INVALID, "too many nonzeros");
   pbs_mat* m = new pbs_mat();
   m->ctx = ctx;
-  m->n_rows = m->n_cols = n;
+  m->n_rows = n;
+  m->n_cols = st->n_cols;  // a slab's extended space (pbs_stencil_slab)
   m->nnz = nnz;
+  const long long hl = -st->sv.xlo, col_off = hl + (hl & 1);
   CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n + 4)));
   CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
   CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
@@ -836,7 +851,7 @@ PBS_EXPORT int pbs_stencil_to_csr(pbs_mat* st, pbs_mat** out) {
   CK(pool_alloc(ctx, &tmp, tmp_bytes));
   cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, m->rp, m->rp, n + 1, s);
   pool_free(ctx, tmp);
-  stencil_fill_kernel<<<ctx->sms * 8, 256, 0, s>>>(S, m->rp, m->ci, m->v);
+  stencil_fill_kernel<<<ctx->sms * 8, 256, 0, s>>>(S, m->rp, m->ci, m->v, col_off);
   unsigned long long* bmax = nullptr;
   CK(pool_alloc(ctx, &bmax, sizeof(unsigned long long)));
   CK(cudaMemsetAsync(bmax, 0, sizeof(unsigned long long), s));
@@ -858,6 +873,58 @@ PBS_EXPORT int pbs_stencil_to_csr(pbs_mat* st, pbs_mat** out) {
     pbs_mat_free(m);
     return rc;
   }
+  *out = m;
+  return PBS_OK;
+}
+
+// nonzeros of a stencil operator's rows (a slab's share of the grid's)
+__global__ void stencil_nnz_kernel(const __grid_constant__ StencilView S, unsigned long long* out) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < S.n; i += stride)
+    for (int p = 0; p < S.npts; ++p) c += stencil_in(S, i, p);
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
+}
+
+// Rows [row_lo, row_hi) of a whole-grid stencil operator as a slab of a
+// row-partitioned system (reduction.py:55-87, linalg.py:164-172):
+// local row i is grid row row_lo + i, and SpMV inputs live in the slab's
+// extended space [pad | hl | own | hr] like a CSR slab's (distributed.py).
+// hl / hr must cover every column the rows reach outside [row_lo, row_hi).
+PBS_EXPORT int pbs_stencil_slab(pbs_mat* st, int64_t row_lo, int64_t row_hi, int64_t hl, int64_t hr,
+                                pbs_mat** out) {
+  if (!st || !out || !st->stencil || st->sv.g0 != 0 || st->sv.xlo != 0)
+    return set_err(st ? st->ctx : nullptr, PBS_ERR_INVALID, "need a whole-grid stencil operator");
+  pbs_ctx* ctx = st->ctx;
+  const long long n = st->n_rows;
+  if (row_lo < 0 || row_hi > n || row_lo >= row_hi) return set_err(ctx, PBS_ERR_INVALID, "slab rows out of range");
+  if (hl < 0 || hr < 0 || hl > row_lo || hr > n - row_hi) return set_err(ctx, PBS_ERR_INVALID, "halo out of range");
+  CK(cudaSetDevice(ctx->device));
+  pbs_mat* m = new pbs_mat();
+  *m = *st;
+  m->ws = nullptr;
+  m->part = Partition{};
+  const long long n_own = row_hi - row_lo;
+  m->n_rows = n_own;
+  m->n_cols = (hl & 1) + hl + n_own + hr;
+  StencilView& S = m->sv;
+  S.n = n_own;
+  S.g0 = row_lo;
+  S.xlo = -hl;
+  S.xhi = n_own + hr;
+  // blocks whose windows all start inside [xlo, xhi) use the constant staged
+  // offsets (StencilWin::kfix); the clamp moves left by the halo
+  if (m->xwin.nwin) m->swin.clamp_r0 = st->swin.clamp_r0 - hl;
+  unsigned long long* d = nullptr;
+  CK(pool_alloc(ctx, &d, sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream));
+  stencil_nnz_kernel<<<ctx->sms * 4, 256, 0, ctx->stream>>>(S, d);
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  pool_free(ctx, d);
+  m->nnz = (long long)h;
   *out = m;
   return PBS_OK;
 }

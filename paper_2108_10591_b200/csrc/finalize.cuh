@@ -107,6 +107,7 @@ static __device__ void check_commit(SolverState* st, long long j, const CheckVal
     st->status = status;
     st->iterations = iters;
     if (failure) st->failure_iter = j;
+    st->stop_check = j;
     st->run_all = 0;
     if (st->spine_done) st->run_spine = 0;
   };

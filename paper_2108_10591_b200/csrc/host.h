@@ -133,7 +133,8 @@ static inline void pool_free(pbs_ctx* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
-static inline int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int cap_per_sm = 8) {
+static inline int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int cap_per_sm = 8,
+                           int sms = 0) {
   auto it = ctx->occ.find(kernel);
   int per_sm;
   if (it == ctx->occ.end()) {
@@ -145,7 +146,7 @@ static inline int grid_for(pbs_ctx* ctx, const void* kernel, long long work_bloc
     per_sm = it->second;
   }
   if (per_sm > cap_per_sm) per_sm = cap_per_sm;
-  long long g = (long long)ctx->sms * per_sm;
+  long long g = (long long)(sms > 0 ? sms : ctx->sms) * per_sm;
   if (work_blocks < g) g = work_blocks;
   if (g < 1) g = 1;
   return (int)g;
@@ -159,6 +160,7 @@ struct Workspace {
   long long n = 0;
   size_t stride = 0;  // padded elements per vector
   double* base = nullptr;
+  bool base_ipc = false;  // cudaMalloc'd (IPC-exportable: peers map it), not from the pool
   VecPtrs V{};  // own segments (elementwise kernels, SpMV outputs, epilogue inputs)
   VecPtrs X{};  // extended-space bases (SpMV inputs: [left halo | own | right halo])
   long long n_ext = 0, own_off = 0;
@@ -209,6 +211,17 @@ struct Launcher {
   long long iter = 0;
   int trace_rc = 0;
   int err = 0;  // first launch-configuration failure (sticky)
+  // multi-GPU schedule: SMs the launches may fill (0: all; the reduction's
+  // kernels need one left free beside a persistent SpMV grid, and a loopback
+  // partition emulating one GPU of N gets sms / N), and a cap on one launch's
+  // grid (its partial records must fit the buffer after earlier pieces')
+  int sm_limit = 0;
+  long long grid_cap = 0;
+  int sms() const { return sm_limit > 0 ? sm_limit : ctx->sms; }
+  int cap_grid(long long g) const {
+    if (grid_cap > 0 && g > grid_cap) g = grid_cap;
+    return (int)(g > 0 ? g : 1);
+  }
   // schedule evidence: (iter, kind, tag, event) — resolved to times at the end
   struct Ev {
     long long iter;
@@ -449,10 +462,10 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   if (!m->stencil && csr_engine_tpr()) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, nullptr};
     if (csr_engine_tpr() == 2) {
-      grid = grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, true>, nblk);
+      grid = L.cap_grid(grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, true>, nblk, 8, L.sms()));
       csr_tpr_kernel<Epi, true><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     } else {
-      grid = grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, false>, nblk);
+      grid = L.cap_grid(grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, false>, nblk, 8, L.sms()));
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
   } else if (!m->stencil) {
@@ -469,8 +482,8 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       L.err = rc;
       return 0;
     }
-    const long long cap = (long long)L.ctx->sms * ctas;
-    grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
+    const long long cap = (long long)L.sms() * ctas;
+    grid = L.cap_grid(nblk < cap ? nblk : cap);
     // programmatic dependent launch: overlaps this CTA's prologue and first
     // matrix chunks with the previous kernel's drain
     if (stage_in && ctas == 1)  // 1-CTA layout: the instantiation with more products in flight
@@ -494,8 +507,8 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       L.err = rc;
       return 0;
     }
-    const long long cap = (long long)L.ctx->sms * ctas;
-    grid = (int)(nblk < cap ? (nblk > 0 ? nblk : 1) : cap);
+    const long long cap = (long long)L.sms() * ctas;
+    grid = L.cap_grid(nblk < cap ? nblk : cap);
 #define PBS_SPIPE(D, NP)                                                                                   \
   launch_pdl(L, kPdlStencilPipe, stencil_pipe_kernel<Epi, D, NP>, grid, kPipeThreads, smem, S, x, epi, m->xwin, \
              m->swin, bslots);
@@ -513,7 +526,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     S.row_hi = hi;
 #define PBS_STENCIL(D, NP)                                                                 \
   {                                                                                        \
-    grid = grid_for(L.ctx, (const void*)stencil_spmv_kernel<Epi, D, NP>, nblk);            \
+    grid = L.cap_grid(grid_for(L.ctx, (const void*)stencil_spmv_kernel<Epi, D, NP>, nblk, 8, L.sms())); \
     launch_pdl(L, kPdlStencilDirect, stencil_spmv_kernel<Epi, D, NP>, grid, kThreads, 0, S, x, epi); \
   }
     if (S.dim == 3 && S.npts == 7) PBS_STENCIL(3, 7)
@@ -532,7 +545,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
 template <class K, class... Args>
 static void vec_launch(Launcher& L, K kernel, long long n, int kind, Args... args) {
   long long nblk = (n + kThreads - 1) / kThreads;
-  int grid = grid_for(L.ctx, (const void*)kernel, nblk);
+  int grid = L.cap_grid(grid_for(L.ctx, (const void*)kernel, nblk, 8, L.sms()));
   kernel<<<grid, kThreads, 0, L.s>>>(args...);
   L.done(kind);
 }
@@ -559,6 +572,7 @@ static inline EpiResid epi_resid(Workspace* ws, bool with_r0s) {
   e.r = ws->V.v[VR];
   e.r0s = with_r0s ? ws->V.v[VR0S] : nullptr;
   e.st = ws->st;
+  e.tag = PBS_TAG_AX;
   e.in[0] = ws->V.v[VB];
   return e;
 }
@@ -623,6 +637,7 @@ static inline EpiK3n epi_k3n(Workspace* ws, const Mode& md) {
   e.s = V[VS];
   e.q_out = md.store_temps ? V[VQ] : nullptr;
   e.st = ws->st;
+  e.tag = PBS_TAG_AW;
   const int in[4] = {VAS, VL, VG, VS};
   for (int k = 0; k < 4; ++k) e.in[k] = V[in[k]];
   return e;
@@ -659,6 +674,7 @@ static inline EpiK3 epi_k3(Workspace* ws, const Mode& md, int fuse) {
   e.s = V[VS];
   e.q_out = md.store_temps ? V[VQ] : nullptr;
   e.st = ws->st;
+  e.tag = PBS_TAG_AW;
   e.sink = sink_for(ws, md, fuse, 0);
   const int in[8] = {VAS, VL, VG, VS, VY, VR, VR0S, VT};
   for (int k = 0; k < 8; ++k) e.in[k] = V[in[k]];
@@ -675,6 +691,7 @@ static inline EpiK3s epi_k3s(Workspace* ws, const Mode& md, int fuse, int np12) 
   e.s = V[VS];
   e.q_out = md.store_temps ? V[VQ] : nullptr;
   e.st = ws->st;
+  e.tag = PBS_TAG_AW;
   e.sink = sink_for(ws, md, fuse, 0);
   e.sink.partials2 = ws->partials12;
   e.sink.nparts2 = np12;
@@ -710,6 +727,7 @@ static inline EpiSS3 epi_ss3(Workspace* ws) {
   e.x = V[VX];
   e.r = V[VR];
   e.st = ws->st;
+  e.tag = PBS_TAG_AU;
   const int in[8] = {VO, VS, VU, VP, VY, VZ, VX, VR};
   for (int k = 0; k < 8; ++k) e.in[k] = V[in[k]];
   return e;

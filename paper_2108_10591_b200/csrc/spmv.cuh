@@ -100,6 +100,10 @@ struct StencilView {
   long long foff[kMaxStencil];  // flattened offset
   double coef[kMaxStencil];
   long long row_lo, row_hi;
+  // row slab of a partitioned grid (pbs_stencil_slab): local row i is grid
+  // row i + g0, and x is addressed relative to the slab's own segment, valid
+  // on [xlo, xhi) = [-left halo, n + right halo).  Whole grid: 0, [0, n).
+  long long g0, xlo, xhi;
   // neighbours of the row at grid coordinates c (padded to 3 axes) that lie
   // in the grid, as a bit mask over the points
   __device__ __forceinline__ unsigned valid_mask(const int (&c)[3], int dim) const {
@@ -172,16 +176,25 @@ struct EpiStore {
   SolverState* st;
   int tag;
   int spine;  // gate on run_spine instead of run_all
+  // nullable: [start, end] of this product over all CTAs (schedule
+  // evidence; the start is stored complemented so both take atomicMax)
+  unsigned long long* stamp;
   const double* in[1];
   __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
   __device__ void on_skip() const {}
-  __device__ void init() {}
+  __device__ void init() {
+    if (stamp && threadIdx.x == 0) atomicMax(stamp, ~gtime());
+  }
   __device__ void row(long long i, double v, const double*) {
     y[i] = v;
     if (tag && !isfinite(v)) report_nonfinite(st, tag, i);
   }
   template <int NT, bool NAMED>
-  __device__ void finish() {}
+  __device__ void finish() {
+    if (!stamp) return;
+    block_bar<NT, NAMED>();
+    if (threadIdx.x == 0) atomicMax(stamp + 1, gtime());
+  }
 };
 
 struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
@@ -194,12 +207,13 @@ struct EpiResid {  // lincomb2(r, 1.0, b, -1.0, ax) after check_finite(ax)
   double* r;
   double* r0s;  // nullable: also r0s = r (solvers.py:617)
   SolverState* st;
+  int tag;  // PBS_TAG_AX (| launch sequence << 8 in the multi-GPU schedule)
   const double* in[kIn];  // b
   __device__ bool active() const { return gate_all(st); }
   __device__ void on_skip() const {}
   __device__ void init() {}
   __device__ void row(long long i, double ax, const double* v) {
-    if (!isfinite(ax)) report_nonfinite(st, PBS_TAG_AX, i);
+    if (!isfinite(ax)) report_nonfinite(st, tag, i);
     const double rv = lc2(1.0, v[0], -1.0, ax);
     r[i] = rv;
     if (r0s) r0s[i] = rv;
@@ -315,8 +329,10 @@ struct EpiK3T {
   double *l, *g, *s;
   double* q_out;  // nullable (single-step parity: expose q)
   SolverState* st;
+  int tag;  // PBS_TAG_AW (| launch sequence << 8 in the multi-GPU schedule)
   DotSink sink;
   const double* in[8];  // As l g s (y r r0s (t))
+  unsigned long long* stamp;  // nullable: [~start, end] of the product (see EpiStore)
   double alpha, beta, zeta, eta;
   DotsT<M> d;
   __device__ bool active() const { return gate_all(st); }
@@ -326,6 +342,7 @@ struct EpiK3T {
     if (!dev_err(st) && !st->run_all) st->run_spine = 0;
   }
   __device__ void init() {
+    if (stamp && threadIdx.x == 0) atomicMax(stamp, ~gtime());
     if (M) d.zero();
     alpha = st->alpha;
     beta = st->beta;
@@ -333,7 +350,7 @@ struct EpiK3T {
     eta = st->eta;
   }
   __device__ void row(long long i, double aw, const double* v) {
-    if (!isfinite(aw)) report_nonfinite(st, PBS_TAG_AW, i);
+    if (!isfinite(aw)) report_nonfinite(st, tag, i);
     const double asv = v[0];
     const double q = lc2(1.0, asv, beta, v[1]);               // q = As + beta*l
     const double lv = lc2(1.0, q, -1.0, aw);                  // l = q - A w
@@ -351,6 +368,10 @@ struct EpiK3T {
   }
   template <int NT, bool NAMED>
   __device__ void finish() {
+    if (stamp) {
+      block_bar<NT, NAMED>();
+      if (threadIdx.x == 0) atomicMax(stamp + 1, gtime());
+    }
     if constexpr (M != 0) sink.finish<NT, NAMED>(d, st);
   }
 };
@@ -368,6 +389,7 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
   static constexpr int kGatherBatch = 8;  // x gathers in flight per row
   double *w, *t, *z, *y, *x, *r;
   SolverState* st;
+  int tag;  // PBS_TAG_AU (| launch sequence << 8 in the multi-GPU schedule)
   const double* in[kIn];  // o s u p y z x r
   double alpha, zeta, eta;
   __device__ bool active() const { return gate_all(st); }
@@ -378,7 +400,7 @@ struct EpiSS3 {  // ssBiCGSafe2 tail: w = A u, then t, z, y, x, r (solvers.py:56
     eta = st->eta;
   }
   __device__ void row(long long i, double wv, const double* v) {
-    if (!isfinite(wv)) report_nonfinite(st, PBS_TAG_AU, i);
+    if (!isfinite(wv)) report_nonfinite(st, tag, i);
     const double ov = v[0];
     const double yv = lc3(zeta, v[1], eta, v[4], -alpha, wv);  // y = zeta s + eta y - alpha w
     const double zv = lc3(zeta, v[7], eta, v[5], -alpha, v[2]);  // z = zeta r + eta z - alpha u
@@ -1048,8 +1070,8 @@ __global__ void __launch_bounds__(kPipeThreads, PBS_SPIPE_MINB) stencil_pipe_ker
         wbytes[c] = 0;
         if (c < W.nwin) {
           long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
-          if (lo < 0) lo = 0;
-          if (hi > S.n) hi = S.n;
+          if (lo < S.xlo) lo = S.xlo;
+          if (hi > S.xhi) hi = S.xhi;
           if (hi > lo) {
             const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
             wlo[c] = loa;
@@ -1106,20 +1128,21 @@ __global__ void __launch_bounds__(kPipeThreads, PBS_SPIPE_MINB) stencil_pipe_ker
     const long long r0 = bhp->r0;
     if (t < nr) {
       const long long i = r0 + t;
+      const long long gi = i + S.g0;  // grid row (slab-local rows are offset)
       int c[3] = {0, 0, 0};
       if (DIM == 3) {
-        const long long z = S.dk2.div(i);
-        const long long rem = i - z * S.k2;
+        const long long z = S.dk2.div(gi);
+        const long long rem = gi - z * S.k2;
         const long long yy = S.dk.div(rem);
         c[0] = (int)z;
         c[1] = (int)yy;
         c[2] = (int)(rem - yy * S.k);
       } else if (DIM == 2) {
-        const long long yy = S.dk.div(i);
+        const long long yy = S.dk.div(gi);
         c[1] = (int)yy;
-        c[2] = (int)(i - yy * S.k);
+        c[2] = (int)(gi - yy * S.k);
       } else {
-        c[2] = (int)i;
+        c[2] = (int)gi;
       }
       const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
       const unsigned vm = S.valid_mask(c, DIM);
@@ -1246,20 +1269,21 @@ __global__ void __launch_bounds__(kThreads, Epi::kMinBlocks) stencil_spmv_kernel
   e.init();
   const long long stride = (long long)gridDim.x * kThreads;
   for (long long i = S.row_lo + (long long)blockIdx.x * kThreads + threadIdx.x; i < S.row_hi; i += stride) {
+    const long long gi = i + S.g0;  // grid row (slab-local rows are offset)
     int c[3] = {0, 0, 0};
     if (DIM == 3) {
-      const long long z = S.dk2.div(i);
-      const long long rem = i - z * S.k2;
+      const long long z = S.dk2.div(gi);
+      const long long rem = gi - z * S.k2;
       const long long yy = S.dk.div(rem);
       c[0] = (int)z;
       c[1] = (int)yy;
       c[2] = (int)(rem - yy * S.k);
     } else if (DIM == 2) {
-      const long long yy = S.dk.div(i);
+      const long long yy = S.dk.div(gi);
       c[1] = (int)yy;
-      c[2] = (int)(i - yy * S.k);
+      c[2] = (int)(gi - yy * S.k);
     } else {
-      c[2] = (int)i;
+      c[2] = (int)gi;
     }
     double inr[Epi::kIn > 0 ? Epi::kIn : 1];
 #pragma unroll

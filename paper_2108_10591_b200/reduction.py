@@ -109,10 +109,34 @@ _KINDS = {0: REDUCE_START, 1: REDUCE_END, 2: SPMV_START, 3: SPMV_END, 4: COEFF_R
 _TAGS = {0: None, 1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay"}
 
 
-def events_to_log(records) -> EventLog:
-    """Device schedule records (iter, kind, tag, t_ms) -> the reference's EventLog.
+def stamps_to_records(stamps) -> list[tuple[int, int, int, float]]:
+    """Device-clock stamps of one partition ([iterations, 8]: As start/end, Aw
+    start/end, publish start/end and finalize start/end of check i, ns; -1
+    absent) -> schedule records (iter, kind, tag, t) in the reference's
+    vocabulary: the reduction of check i starts when its record is published
+    and ends (coefficients ready) when its finalize has run; the products are
+    the As and Aw SpMVs of iteration i."""
+    recs = []
+    for i, row in enumerate(np.asarray(stamps)):
+        as0, as1, aw0, aw1, pub0, _pub1, _fin0, fin1 = (float(v) for v in row)
+        if pub0 >= 0:
+            recs.append((i, 0, 0, pub0))
+        if fin1 >= 0:
+            recs.append((i, 1, 0, fin1))
+            recs.append((i, 4, 0, fin1))
+        if as0 >= 0 and as1 >= 0:
+            recs.append((i, 2, 3, as0))
+            recs.append((i, 3, 3, as1))
+        if aw0 >= 0 and aw1 >= 0:
+            recs.append((i, 2, 4, aw0))
+            recs.append((i, 3, 4, aw1))
+    return recs
 
-    seq follows the CUDA-event timestamps (ties keep issue order), so the
+
+def events_to_log(records) -> EventLog:
+    """Schedule records (iter, kind, tag, t) -> the reference's EventLog.
+
+    seq follows the device timestamps (ties keep record order), so the
     reference's verify_phase_order (reduction.py:486-563) can be re-run on it.
     """
     recs = [(float(t), k, int(i), int(kind), int(tag)) for k, (i, kind, tag, t) in enumerate(records)]
@@ -123,25 +147,17 @@ def events_to_log(records) -> EventLog:
     return log
 
 
-def overlap_report(records) -> dict:
-    """Per iteration: the reduction's [start, end] vs the As SpMV's [start, end]
-    (CUDA-event ms).  overlapped = the intervals intersect, i.e. the
-    all-gather + check really ran while A s was computed."""
-    per: dict[int, dict] = {}
-    for i, kind, tag, t in records:
-        d = per.setdefault(int(i), {})
-        if kind == 0:
-            d["r0"] = t
-        elif kind == 1:
-            d["r1"] = t
-        elif kind == 2 and int(tag) == 3:
-            d["a0"] = t
-        elif kind == 3 and int(tag) == 3:
-            d["a1"] = t
+def overlap_report(stamps) -> dict:
+    """Per iteration i of one partition's device-clock stamps: the reduction of
+    check i ([publish start, finalize end]) against the As SpMV of iteration
+    i.  overlapped: the intervals intersect; hidden: the coefficients were
+    ready before A s finished, i.e. the reduction cost the iteration nothing."""
     out = {}
-    for i, d in sorted(per.items()):
-        if {"r0", "r1", "a0", "a1"} <= d.keys():
-            inter = min(d["r1"], d["a1"]) - max(d["r0"], d["a0"])
-            out[i] = {"reduce_ms": d["r1"] - d["r0"], "as_ms": d["a1"] - d["a0"],
-                      "overlap_ms": max(inter, 0.0), "overlapped": inter > 0}
+    for i, row in enumerate(np.asarray(stamps)):
+        as0, as1, _aw0, _aw1, pub0, _pub1, _fin0, fin1 = (float(v) for v in row)
+        if min(as0, as1, pub0, fin1) < 0:
+            continue
+        inter = min(fin1, as1) - max(pub0, as0)
+        out[i] = {"reduce_us": (fin1 - pub0) / 1e3, "as_us": (as1 - as0) / 1e3,
+                  "overlap_us": max(inter, 0.0) / 1e3, "overlapped": inter > 0, "hidden": fin1 <= as1}
     return out

@@ -124,7 +124,7 @@ class DeviceEngine:
     workers: int = 1
     use_graphs: bool = True
     timing: bool = False
-    evidence: bool = False  # record the schedule as an EventLog (multi-GPU schedule)
+    evidence: bool = False  # multi-GPU schedule: device-clock stamps of every product and reduction
 
     def __post_init__(self):
         if self.reduce not in ("tree", "plan"):
@@ -192,63 +192,46 @@ def _ptr(a):
     return None if a is None else a.ctypes.data_as(C.c_void_p)
 
 
-def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
-    config = config or SolverConfig()
-    b, x0 = _prepare(A, b, x0)
-    n = A.n_rows
-    if config.monitor_every > 0:
-        raise NotImplementedError("monitor_every (DriftMonitor) is not available on the device path")
-    eng = _engine_params(engine, n)
-    own = not isinstance(A, DeviceMatrix)
-    dm = DeviceMatrix.from_csr(A, device=eng.device) if own else A
-    try:
-        cfg = _lib.Config()
-        cfg.tol = config.tol
-        cfg.max_iters = config.max_iters
-        cfg.rr_epoch = config.rr_epoch
-        cfg.rr_cutoff = -1 if config.rr_cutoff is None else config.rr_cutoff
-        cfg.record_history = 1 if config.record_history else 0
-        cfg.reduce_mode = _lib.REDUCE_PLAN if eng.reduce == "plan" else _lib.REDUCE_TREE
-        cfg.plan_workers = eng.workers
-        cfg.use_graphs = 1 if eng.use_graphs else 0
-        cfg.timing = 1 if (eng.timing or eng.evidence) else 0
-        ev_buf = ev_cnt = None
-        if eng.evidence:
-            ev_cap = 8 * (config.max_iters + 2)
-            ev_buf = np.zeros((ev_cap, 4))
-            ev_cnt = C.c_int64(0)
-            cfg.events_out = ev_buf.ctypes.data_as(C.c_void_p)
-            cfg.events_cap = ev_cap
-            cfg.events_count = C.pointer(ev_cnt)
-        cb_keep = None
-        if trace_hook is not None:
-            names = _TRACE_NAMES_BY_METHOD.get(method, _TRACE_NAMES)
+def _make_config(config: SolverConfig, eng: DeviceEngine, nparts: int = 1):
+    """pbs_config for a solve (+ the host buffers its evidence outputs land in)."""
+    cfg = _lib.Config()
+    cfg.tol = config.tol
+    cfg.max_iters = config.max_iters
+    cfg.rr_epoch = config.rr_epoch
+    cfg.rr_cutoff = -1 if config.rr_cutoff is None else config.rr_cutoff
+    cfg.record_history = 1 if config.record_history else 0
+    cfg.reduce_mode = _lib.REDUCE_PLAN if eng.reduce == "plan" else _lib.REDUCE_TREE
+    cfg.plan_workers = eng.workers
+    cfg.use_graphs = 1 if eng.use_graphs else 0
+    cfg.timing = 1 if eng.timing else 0
+    keep = {}
+    if eng.evidence:
+        # multi-GPU schedule: %globaltimer stamps per partition and iteration
+        cap = config.max_iters + 2
+        keep["stamps"] = np.full((nparts, cap, len(_lib.STAMP_WORDS)), -1.0)
+        keep["stamps_count"] = C.c_int64(0)
+        cfg.stamps_out = keep["stamps"].ctypes.data_as(C.c_void_p)
+        cfg.stamps_cap = cap
+        cfg.stamps_count = C.pointer(keep["stamps_count"])
+    return cfg, keep
 
-            def _cb(i, vecs, _user):
-                ws = {name: np.ctypeslib.as_array(vecs[k], shape=(n,))
-                      for k, name in enumerate(names)}
-                trace_hook(int(i), ws)
-            cb_keep = _lib.TRACE_FN(_cb)
-            cfg.trace_fn = cb_keep
-        slots = config.max_iters + 1
-        x = _host_result(n)
-        rel = np.empty(slots)
-        flags = np.zeros(slots, dtype=np.uint8)
-        coef = np.empty((slots, 4))
-        res = _lib.Result()
-        rc = _lib.load().pbs_solve(dm.handle, _lib.METHOD_IDS[method], _ptr(b), _ptr(x0), C.byref(cfg),
-                                   _ptr(x), _ptr(rel), _ptr(flags), _ptr(coef), C.byref(res))
-    finally:
-        if own:
-            dm.free()
+
+def _history_buffers(config: SolverConfig):
+    slots = config.max_iters + 1
+    return np.empty(slots), np.zeros(slots, dtype=np.uint8), np.empty((slots, 4))
+
+
+def _raise_for(rc, res, ctx_handle):
     if rc == _lib.PBS_ERR_NONFINITE:
         tag = _lib.SPMV_TAGS.get(res.nonfinite_tag, "?")
         idx = int(res.nonfinite_index)
         raise NonFiniteVectorError(f"matvec {tag!r} output row has non-finite entry at index {idx}", idx)
     if rc == _lib.PBS_ERR_INVALID:
-        raise ValueError(_lib.last_error(dm.ctx.handle))
-    _lib.check(rc, dm.ctx.handle)
+        raise ValueError(_lib.last_error(ctx_handle))
+    _lib.check(rc, ctx_handle)
 
+
+def _build_outcome(method, config, eng, res, x, rel, flags, coef, keep) -> SolveOutcome:
     k = int(res.n_records)
     history = []
     for i in range(k):
@@ -279,8 +262,9 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
         "kernel_count": {name: int(res.kernel_count[j]) for j, name in enumerate(_lib.KERNEL_KINDS)},
         "reduce": eng.reduce,
     }
-    if ev_buf is not None:
-        device["events"] = ev_buf[: ev_cnt.value].copy()
+    if "stamps" in keep:
+        # as many iterations as the solve ran (+ the final check)
+        device["stamps"] = keep["stamps"][:, : int(res.n_records) + 1].copy()
     return SolveOutcome(
         status=status,
         iterations=iterations,
@@ -294,6 +278,63 @@ def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
         failure_iter=None if res.failure_iter < 0 else int(res.failure_iter),
         device=device,
     )
+
+
+def _solve_device(A, b, method, x0, config, engine, trace_hook) -> SolveOutcome:
+    config = config or SolverConfig()
+    b, x0 = _prepare(A, b, x0)
+    n = A.n_rows
+    if config.monitor_every > 0:
+        raise NotImplementedError("monitor_every (DriftMonitor) is not available on the device path")
+    eng = _engine_params(engine, n)
+    own = not isinstance(A, DeviceMatrix)
+    dm = DeviceMatrix.from_csr(A, device=eng.device) if own else A
+    try:
+        cfg, keep = _make_config(config, eng)
+        cb_keep = None
+        if trace_hook is not None:
+            names = _TRACE_NAMES_BY_METHOD.get(method, _TRACE_NAMES)
+
+            def _cb(i, vecs, _user):
+                ws = {name: np.ctypeslib.as_array(vecs[k], shape=(n,))
+                      for k, name in enumerate(names)}
+                trace_hook(int(i), ws)
+            cb_keep = _lib.TRACE_FN(_cb)
+            cfg.trace_fn = cb_keep
+        x = _host_result(n)
+        rel, flags, coef = _history_buffers(config)
+        res = _lib.Result()
+        rc = _lib.load().pbs_solve(dm.handle, _lib.METHOD_IDS[method], _ptr(b), _ptr(x0), C.byref(cfg),
+                                   _ptr(x), _ptr(rel), _ptr(flags), _ptr(coef), C.byref(res))
+    finally:
+        if own:
+            dm.free()
+    _raise_for(rc, res, dm.ctx.handle)
+    return _build_outcome(method, config, eng, res, x, rel, flags, coef, keep)
+
+
+def solve_group(mats, b_ptrs, x_ptrs, method="pbicgsafe", x0_ptrs=None, config=None, engine=None) -> SolveOutcome:
+    """A solve on a loopback group (include/pbsafe.h pbs_solve_group): mats are
+    the partitions' DeviceMatrix objects, b_ptrs / x_ptrs / x0_ptrs device
+    pointers to their own segments.  The outcome's x is None (the caller owns
+    the segments)."""
+    config = config or SolverConfig()
+    if method not in METHODS:
+        raise ValueError(f"unknown method {method!r}; choose from {sorted(METHODS)}")
+    eng = engine if isinstance(engine, DeviceEngine) else DeviceEngine()
+    n = len(mats)
+    cfg, keep = _make_config(config, eng, nparts=n)
+    rel, flags, coef = _history_buffers(config)
+    res = _lib.Result()
+    P = C.c_void_p * n
+    hm = P(*[m.handle for m in mats])
+    hb = P(*b_ptrs)
+    hx = P(*x_ptrs)
+    h0 = P(*x0_ptrs) if x0_ptrs is not None else None
+    rc = _lib.load().pbs_solve_group(hm, n, _lib.METHOD_IDS[method], hb, h0, C.byref(cfg), hx, _ptr(rel),
+                                     _ptr(flags), _ptr(coef), C.byref(res))
+    _raise_for(rc, res, mats[0].ctx.handle)
+    return _build_outcome(method, config, eng, res, None, rel, flags, coef, keep)
 
 
 def solve_pbicgsafe(A, b, x0=None, config=None, engine=None, trace_hook=None) -> SolveOutcome:

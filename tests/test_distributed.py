@@ -131,7 +131,70 @@ def test_halo_plan_for_grid_slabs():
     plan = D.halo_plan(slabs)
     assert all(s.pad == 0 for s in slabs)
     assert plan.recvs[1] == [(0, 0, k * k), (2, k * k + 2 * k * k, k * k)]
-    assert plan.sends[1] == [(0, 0, k * k), (2, k * k, k * k)]
+    # (peer, own offset, length, the peer's extended offset): rank 1's first
+    # plane fills rank 0's right halo, its last plane rank 2's left halo
+    assert plan.sends[1] == [(0, 0, k * k, 2 * k * k), (2, k * k, k * k, 0)]
+    # every send lands exactly where the receiver expects it
+    for src in slabs:
+        for peer, off, ln, dst in plan.sends[src.rank]:
+            assert (src.rank, dst, ln) in plan.recvs[peer]
+
+
+@pytest.mark.parametrize("spec", [
+    problems.convdiff_stencil(3, 12, (100.0, 50.0, 25.0)),
+    problems.convdiff27_stencil(10, (1.0, 0.5, 0.25)),
+    problems.convdiff_stencil(2, 7, (1.0, 1.0)),
+    problems.convdiff27_stencil(9, (1.0, 0.5, 0.25)),
+])
+@pytest.mark.parametrize("nranks", [1, 2, 3, 4, 8])
+def test_stencil_slab_halos_equal_the_csr_slab(spec, nranks):
+    """stencil_slab (no matrix) gives exactly the slab local_csr measures on
+    the stencil's CSR: the device builds slabs from the spec alone."""
+    rp, ci, v = problems.stencil_csr(spec)
+    for r in range(nranks):
+        assert D.stencil_slab(spec, r, nranks) == D.local_csr(rp, ci, v, spec.n, r, nranks)[0]
+
+
+def test_c4_slabs_are_planes_with_one_plane_halos():
+    """Config 4 (384^3, 27-point) over 2, 4, 8 ranks: axis-0 plane slabs
+    (48 planes at 8), one-plane halos, computed without the 1.5e9-nonzero CSR."""
+    spec = problems.config_stencil("c4")
+    k = spec.k
+    for nranks in (2, 4, 8):
+        for r in range(nranks):
+            s = D.stencil_slab(spec, r, nranks)
+            assert s.lo % (k * k) == 0 and s.n_own == (k // nranks) * k * k
+            assert s.hl == (0 if r == 0 else k * k) and s.hr == (0 if r == nranks - 1 else k * k)
+
+
+def _blob_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        blob = bytes([rank]) * 256
+        q.put((rank, D.gather_blobs(blob, world)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_blobs_gather_in_rank_order():
+    """The IPC-handle exchange of DistributedSystem: every rank gets every
+    rank's 256-byte blob, concatenated in rank order (gloo, world 3)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_blob_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(3)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = b"".join(bytes([r]) * 256 for r in range(3))
+    assert all(b == want for _, b in res)
 
 
 def test_odd_halo_gets_an_alignment_pad():
