@@ -1,17 +1,27 @@
 #!/usr/bin/env python
 """Benchmark: p-BiCGSafe iterations/s and time-to-tolerance on B200 (BASELINE.json metric).
 
-One step = one full p-BiCGSafe solve of BASELINE config 2 (3D 7-point
-convection-diffusion, 128^3, b = A·1, x0 = 0) to rel. residual 1e-10, with the
-CSR operator resident in HBM.  ``value`` = iterations/s over the K timed
-solves (CUDA events on the solver stream, max over ranks); ``e2e`` = the same
-metric through the public API ``solve(CsrMatrix, b)`` from pinned host
-buffers, CSR + b uploaded and x + history read back every step.
+One step = one full p-BiCGSafe solve of a BASELINE config to its tolerance,
+b = A·1, x0 = 0, the operator resident in HBM.  ``value`` = iterations/s over
+the K timed solves (CUDA events on the solver stream, max over ranks);
+``e2e`` = the same metric through the public API from pinned host buffers.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c2|c4] [--operator csr|stencil] [--loopback P]
 
-``--impl reference`` times the reference algorithm's CPU restatement
-(oracle/, bitwise equal to the reference's numba path) on this host's cores.
+* default (N = 1): config 2 (3D 7-point 128^3) CSR on one GPU, the fused
+  single-GPU schedule; e2e through ``solve(CsrMatrix, b)`` (CSR + b uploaded,
+  x + history read back every step).
+* ``--gpus N`` (N > 1): one process per GPU, row-partitioned (strong scaling
+  of the one global system).  Without torchrun's environment, bench.py
+  launches itself under ``torch.distributed.run`` with N processes.  The
+  scaling series of the north star is ``--config c4`` (3D 27-point 384^3,
+  slabs built on each GPU from the stencil, no global matrix anywhere).
+* ``--loopback P``: the partitioned schedule with P partitions in this one
+  process on one GPU (each limited to sms / P SMs): schedule and overlap
+  evidence on a single device, not a scaling measurement.
+* ``--impl reference``: the reference algorithm's CPU restatement (oracle/,
+  bitwise equal to the reference's numba path) on this host's cores.
 """
 
 from __future__ import annotations
@@ -19,6 +29,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -30,9 +41,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "p-BiCGSafe iterations/s and time-to-tol; achieved HBM GB/s vs roofline"
-WORKLOAD = ("BASELINE config 2: 3D 7-point convection-diffusion 128^3 (n=2,097,152, "
-            "nnz=14,581,760), beta=(1,0.5,0.25)*h, b=A*1, x0=0, p-BiCGSafe to rel. residual 1e-10, "
-            "fp64 CSR (int64 row_ptr, int32 col_idx)")
+WORKLOADS = {
+    "c2": ("BASELINE config 2: 3D 7-point convection-diffusion 128^3 (n=2,097,152, nnz=14,581,760), "
+           "beta=(1,0.5,0.25)*h, b=A*1, x0=0, p-BiCGSafe to rel. residual 1e-10"),
+    "c4": ("BASELINE config 4: 3D 27-point convection-diffusion 384^3 (n=56,623,104, nnz=1,520,875,000), "
+           "beta=(1,0.5,0.25)*h, b=A*1, x0=0, p-BiCGSafe to rel. residual 1e-10"),
+}
 
 
 def peaks() -> tuple[float, str]:
@@ -42,6 +56,16 @@ def peaks() -> tuple[float, str]:
             return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -104,7 +128,7 @@ def dist_env():
     return rank, world, local
 
 
-def build_problem(cfg_name: str = "c2"):
+def host_csr(cfg_name: str):
     from paper_2108_10591_b200 import problems
 
     st = problems.config_stencil(cfg_name)
@@ -122,9 +146,10 @@ def cpu_baseline(rp, ci, v, b, iters: int, threads: int) -> dict:
     out = orc.solve(rp, ci, v, b, tol=1e-30, max_iters=iters, workers=threads, threads=threads)
     dt = time.perf_counter() - t0
     return {"value": out["iterations"] / dt, "unit": "it/s", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"{iters}-iteration p-BiCGSafe window on config 2 (n={n}), tol=1e-30, "
-                      f"PartitionPlan.balanced(n,{threads}) dot chains, {threads} OpenMP threads; "
-                      f"{dt:.2f} s"}
+                      f"PartitionPlan.balanced(n,{threads}) dot chains, {threads} OpenMP threads "
+                      f"(oracle/pbsafe_oracle.c, the C restatement of the reference's numba path); {dt:.2f} s"}
 
 
 def run_reference(args):
@@ -133,7 +158,11 @@ def run_reference(args):
         return 0
     import paper_2108_10591_b200  # noqa: F401  (generators only)
 
-    st, rp, ci, v = build_problem()
+    if args.config != "c2":
+        emit({"impl": "reference", "unavailable": "the CPU reference arm runs config 2 (config 4's CSR is 25 GB on "
+                                                  "the host)"})
+        return 0
+    st, rp, ci, v = host_csr("c2")
     from oracle import oracle as orc
 
     n = len(rp) - 1
@@ -154,9 +183,9 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "step": f"{window}-iteration window (bounded CPU sample)",
+        "config": {"workload": WORKLOADS["c2"] + ", fp64 CSR", "step": f"{window}-iteration window (bounded CPU sample)",
                    "operator": "csr"},
-        "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": val, "unit": "it/s", "cores": threads, "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"{args.steps} x {window}-iteration p-BiCGSafe windows on config 2, "
                                    f"tol=1e-30, oracle/ restatement (bitwise = reference numba path), "
                                    f"{threads} threads"},
@@ -166,7 +195,201 @@ def run_reference(args):
     return 0
 
 
-def run_ours(args):
+def _cfg_c(_lib, cfgpb, timing=False, graphs=True, max_iters=None, stamps=None):
+    import ctypes as C
+
+    cfg = _lib.Config()
+    mi = max_iters or cfgpb.max_iters
+    cfg.tol, cfg.max_iters, cfg.rr_epoch, cfg.rr_cutoff = cfgpb.tol, mi, 100, -1
+    cfg.record_history, cfg.reduce_mode, cfg.plan_workers = 1, _lib.REDUCE_TREE, 1
+    cfg.use_graphs, cfg.timing = int(graphs), int(timing)
+    if stamps is not None:
+        cfg.stamps_out = stamps.ctypes.data_as(C.c_void_p)
+        cfg.stamps_cap = stamps.shape[-2]
+    return cfg
+
+
+def _status_name(st):
+    return {0: "converged", 1: "max_iters", 2: "breakdown", 3: "non_finite"}.get(int(st), str(st))
+
+
+def run_single(args):
+    """N = 1: the fused single-GPU schedule (K12 + K3 per iteration, CUDA graphs)."""
+    import ctypes as C
+
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_2108_10591_b200 as pb
+    from paper_2108_10591_b200 import _lib, problems
+    from paper_2108_10591_b200.operators import DeviceMatrix
+
+    dev = torch.cuda.current_device()
+    ctx = _lib.context(dev)
+    cfg_name = args.config
+    st = problems.config_stencil(cfg_name)
+    n = st.n
+    rp = ci = v = None
+    if cfg_name == "c2" and args.operator == "csr":
+        st, rp, ci, v = host_csr("c2")
+        dm = DeviceMatrix.from_csr((rp, ci.astype(np.int32), v), ctx=ctx)
+    else:
+        stm = DeviceMatrix.from_stencil(st, ctx=ctx)
+        if args.operator == "csr":
+            dm = stm.to_csr()  # config 4: the 18 GB CSR built on the device
+            stm.free()
+        else:
+            dm = stm
+    nnz = int(dm.nnz)
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    b_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    dm.spmv_dev(ones.data_ptr(), b_dev.data_ptr())  # b = A*1
+    del ones
+    x_dev = torch.empty(n, dtype=torch.float64, device="cuda")
+    cfgpb = pb.SolverConfig(tol=problems.CONFIGS[cfg_name]["tol"], max_iters=2000)
+
+    def solve_dev(timing=False, graphs=True, method="pbicgsafe", max_iters=None):
+        cfg = _cfg_c(_lib, cfgpb, timing, graphs, max_iters)
+        res = _lib.Result()
+        rel = np.empty(cfg.max_iters + 1)
+        rc = _lib.load().pbs_solve_dev(dm.handle, _lib.METHOD_IDS[method], C.c_void_p(b_dev.data_ptr()), None,
+                                       C.byref(cfg), C.c_void_p(x_dev.data_ptr()),
+                                       rel.ctypes.data_as(C.c_void_p), None, None, C.byref(res))
+        _lib.check(rc, ctx.handle)
+        if method == "pbicgsafe":
+            assert res.status == 0, f"solve did not converge: status {res.status}"
+        return res
+
+    for _ in range(max(args.warmup, 3)):
+        solve_dev()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    total_it, total_ms, launches = 0, 0.0, 0
+    for _ in range(args.steps):
+        res = solve_dev()
+        total_it += res.iterations
+        total_ms += res.device_ms
+        launches += res.kernel_launches
+    torch.cuda.synchronize()
+    tres = [solve_dev(timing=True) for _ in range(max(1, min(args.steps, 5)))]
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    iters_per_s = total_it / (total_ms / 1e3)
+
+    peak, peak_src = peaks()
+    stencil = args.operator == "stencil"
+    m_a = 0 if stencil else 12 * nnz + 8 * (n + 1)  # SURVEY 8(d): 12 B per nonzero + int64 row_ptr
+    m_eng = 0 if stencil else 10 * nnz + 8 * (n + 1)  # the staged engine's u16 window-local columns
+    k3_bytes = m_a + 11 * 8 * n    # w gather, As l g s y r r0s reads, l g s writes (+ dots a c d g)
+    k12_bytes = m_a + 21 * 8 * n   # s gather, r p u t y l g w z x r0s reads, As p u w t z y x r writes
+    it_bytes = 2 * m_a + 34 * 8 * n  # SURVEY 8(d) three-phase minimum
+    it_bytes_own = 2 * m_a + 32 * 8 * n  # this schedule: K1+K2 fused (As not re-read)
+    kms = {name: sum(r.kernel_ms[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
+    kcnt = {name: sum(r.kernel_count[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
+    tim_ms = sum(r.device_ms for r in tres)
+    kernels = {}
+    for name, byt, eng in (("K1_As", k12_bytes, k12_bytes - m_a + m_eng), ("K3_Aw_epilogue", k3_bytes,
+                                                                         k3_bytes - m_a + m_eng)):
+        if kcnt[name]:
+            avg = kms[name] / kcnt[name]
+            kernels[name] = {"avg_us": avg * 1e3, "alg_bytes": byt, "GBps": byt / (avg * 1e-3) / 1e9,
+                             "frac": byt / (avg * 1e-3) / 1e9 / peak, "engine_bytes": eng,
+                             "engine_frac": eng / (avg * 1e-3) / 1e9 / peak, "share_of_step": kms[name] / tim_ms}
+    kernels["K1_As"]["name"] = "K12 (As SpMV + fused p u w t z y x r updates + dots b e f h r)"
+    kernels["K3_Aw_epilogue"]["name"] = "K3 (Aw SpMV + l,g,s updates + dots a c d g + fused check)"
+    dom_key = max(("K1_As", "K3_Aw_epilogue"), key=lambda k: kms[k])
+    dom = kernels[dom_key]
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")  # the committed ncu --set full capture
+    if os.path.exists(tr_path) and cfg_name == "c2" and not stencil:
+        try:
+            traffic = json.load(open(tr_path)).get(dom_key, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    comparators = None
+    if cfg_name == "c2" and not args.no_comparators:
+        comparators = {}
+        for mname in ("pbicgsafe", "ssbicgsafe2", "pbicgstab", "bicgstab", "gpbicg"):
+            solve_dev(method=mname, max_iters=4000)  # warm (graph capture)
+            rr_ = solve_dev(method=mname, max_iters=4000)
+            comparators[mname] = {"status": _status_name(rr_.status), "iterations": int(rr_.iterations),
+                                  "time_to_tol_ms": rr_.device_ms,
+                                  "it_per_s": rr_.iterations / (rr_.device_ms * 1e-3)}
+        comparators["note"] = ("one device solve each to 1e-10, CSR resident; pbicgstab is the pipelined "
+                               "BiCGStab of Cools & Vanroose BASELINE names (not in the reference; restated in "
+                               "oracle/pbsafe_oracle.c solve_pstab, parity unpinned against reference outputs); "
+                               "bicgstab is the reference's two-reduction BiCGStab (solvers.py:210-327)")
+
+    # e2e through the public API, pinned host buffers
+    pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+    b_host = pin(b_dev.cpu().numpy())
+    if rp is not None:
+        A_host = pb.CsrMatrix(n, n, pin(rp), pin(ci), pin(v))
+        call, h2d = (lambda: pb.solve(A_host, b_host, config=cfgpb)), rp.nbytes + ci.nbytes + v.nbytes + b_host.nbytes
+        note = ("wall clock around solve(CsrMatrix, b): CSR (int64 col_idx) + b H2D, int64->int32 narrowing, "
+                "solve, x + history D2H")
+    else:
+        call, h2d = (lambda: pb.solve(dm, b_host, config=cfgpb)), b_host.nbytes
+        note = ("wall clock around solve(DeviceMatrix, b): b H2D, solve, x + history D2H; the operator is "
+                "generated on the device once (config 4's CSR has no host form here: 25 GB)")
+    for _ in range(max(2, args.warmup)):
+        out = call()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e_it = 0
+    for _ in range(args.steps):
+        out = call()
+        e_it += out.iterations
+    dt = time.perf_counter() - t0
+    e2e = {"value": e_it / dt, "unit": "it/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": int(8 * n + out.iterations * (8 + 1 + 32)), "ms_per_step": dt / args.steps * 1e3,
+           "note": note}
+
+    cpu = None
+    if not args.no_cpu and cfg_name == "c2":
+        threads = os.cpu_count() or 1
+        if rp is None:
+            _, rp, ci, v = host_csr("c2")
+        cpu = cpu_baseline(rp, ci, v, b_dev.cpu().numpy(), iters=args.cpu_iters, threads=threads)
+    avg_it = total_it / args.steps
+    line = {
+        "metric": METRIC, "value": iters_per_s, "unit": "it/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[cfg_name] + (", matrix-free stencil" if stencil else
+                                                      ", fp64 CSR (int64 row_ptr, int32 col_idx)"),
+                   "operator": args.operator, "iterations_per_solve": avg_it, "time_to_tol_ms": total_ms / args.steps,
+                   "parallelism": "single GPU",
+                   "l2": "inputs larger than L2 (operator + 18 workspace vectors >> 126 MB)", "graphs": True},
+        "roofline": {"bound": "hbm", "achieved": dom["GBps"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
+                     "traffic": traffic, "kernel": dom["name"], "alg_bytes_per_launch": dom["alg_bytes"],
+                     "engine_bytes_per_launch": dom["engine_bytes"], "engine_frac": dom["engine_frac"],
+                     "avg_launch_us": dom["avg_us"], "peak_source": peak_src,
+                     "bytes_note": ("alg = SURVEY 8(d) 12 B per nonzero (f64 value + int32 column) + int64 row_ptr; "
+                                    "engine = what the staged engine streams (u16 window-local columns, 10 B)")},
+        "iteration_roofline": {"alg_bytes_per_iter": it_bytes, "achieved_GBps": it_bytes * iters_per_s / 1e9,
+                               "frac": it_bytes * iters_per_s / 1e9 / peak,
+                               "frac_own_schedule": it_bytes_own * iters_per_s / 1e9 / peak,
+                               "note": "B_iter = 2*M_A + 34*8n (SURVEY 8(d)); this schedule moves 2*M_A + 32*8n"},
+        "kernels": kernels,
+        "comparators": comparators,
+        "timing_mode_it_per_s": sum(r.iterations for r in tres) / (tim_ms / 1e3),
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    emit(line)
+    return 0
+
+
+def run_partitioned(args):
+    """N > 1 (one process per GPU) or a loopback group: the row-partitioned
+    schedule (csrc/dist.cu)."""
     import torch
 
     rank, world, local = dist_env()
@@ -178,242 +401,201 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     import paper_2108_10591_b200 as pb
-    from paper_2108_10591_b200 import _lib
-    from paper_2108_10591_b200.operators import DeviceMatrix
+    from paper_2108_10591_b200 import _lib, problems
+    from paper_2108_10591_b200.distributed import DistributedSystem, LoopbackSystem, SystemSource, local_csr
+    from paper_2108_10591_b200.reduction import overlap_report
 
-    dev = torch.cuda.current_device()
-    ctx = _lib.context(dev)
-    st, rp, ci, v = build_problem()
-    n = len(rp) - 1
-    nnz = int(rp[-1])
-    if world > 1 or args.partitioned:
-        # strong scaling: the global config-2 system row-partitioned over the ranks
-        from paper_2108_10591_b200.distributed import DistributedSystem
-
-        dsys = DistributedSystem(rp, ci.astype(np.int32), v, n)
-        dm = dsys.matrix
-        n_loc = dsys.n_own
-        ones = torch.ones(dsys.slab.n_ext, dtype=torch.float64, device="cuda")
+    cfg_name = args.config
+    spec = problems.config_stencil(cfg_name)
+    n = spec.n
+    host = None
+    if cfg_name == "c2" and args.operator == "csr":
+        # the host CSR every rank slices (config 2 is small); e2e re-uploads the slab per step
+        _, rp, ci, v = host_csr("c2")
+        source = SystemSource.from_csr(rp, ci, v, n)
+        host = (rp, ci, v)
     else:
-        dsys = None
-        dm = DeviceMatrix.from_csr((rp, ci.astype(np.int32), v), ctx=ctx)
-        n_loc = n
-        ones = torch.ones(n, dtype=torch.float64, device="cuda")
-    b_dev = torch.empty(n_loc, dtype=torch.float64, device="cuda")
+        source = SystemSource.from_stencil(spec)  # each GPU builds its slab from the stencil
+    loop = world == 1 and args.loopback > 1
+    nparts = args.loopback if loop else world
+    if loop:
+        sysd = LoopbackSystem(nparts, source=source, operator=args.operator)
+        slabs = sysd.slabs
+        mats = sysd.mats
+    else:
+        sysd = DistributedSystem(source=source, operator=args.operator, transport=args.transport)
+        slabs = [sysd.slab]
+        mats = [sysd.matrix]
+    ctx = _lib.context(torch.cuda.current_device())
+    # b = A*1 through the partitioned SpMV
+    if loop:
+        b_parts = [torch.from_numpy(np.ascontiguousarray(seg)).cuda() for seg in
+                   np.split(sysd.spmv(np.ones(n)), np.cumsum([s.n_own for s in slabs])[:-1])]
+    else:
+        ones = torch.ones(slabs[0].n_own, dtype=torch.float64, device="cuda")
+        b_parts = [torch.empty(slabs[0].n_own, dtype=torch.float64, device="cuda")]
+        sysd.spmv_dev(ones.data_ptr(), b_parts[0].data_ptr())
+    x_parts = [torch.empty_like(t) for t in b_parts]
     torch.cuda.synchronize()
-    dm.spmv_dev(ones.data_ptr(), b_dev.data_ptr())  # b = A*1 (this rank's rows)
-    x_dev = torch.empty(n_loc, dtype=torch.float64, device="cuda")
-    cfgpb = pb.SolverConfig(tol=1e-10, max_iters=2000)
+    cfgpb = pb.SolverConfig(tol=problems.CONFIGS[cfg_name]["tol"], max_iters=3000)
+    eng = pb.DeviceEngine()
+    eng_ev = pb.DeviceEngine(evidence=True)
 
-    import ctypes as C
+    def solve_once(engine=eng):
+        if loop:
+            return pb.solvers.solve_group(mats, [t.data_ptr() for t in b_parts], [t.data_ptr() for t in x_parts],
+                                          config=cfgpb, engine=engine)
+        return _solve_dev_partition(_lib, ctx, mats[0], b_parts[0], x_parts[0], cfgpb, engine)
 
-    def solve_dev(timing=False, graphs=True, method="pbicgsafe", max_iters=None):
-        cfg = _lib.Config()
-        mi = max_iters or cfgpb.max_iters
-        cfg.tol, cfg.max_iters, cfg.rr_epoch, cfg.rr_cutoff = cfgpb.tol, mi, 100, -1
-        cfg.record_history, cfg.reduce_mode, cfg.plan_workers = 1, _lib.REDUCE_TREE, 1
-        cfg.use_graphs, cfg.timing = int(graphs), int(timing)
-        res = _lib.Result()
-        rel = np.empty(mi + 1)
-        rc = _lib.load().pbs_solve_dev(dm.handle, _lib.METHOD_IDS[method], C.c_void_p(b_dev.data_ptr()), None,
-                                       C.byref(cfg), C.c_void_p(x_dev.data_ptr()),
-                                       rel.ctypes.data_as(C.c_void_p), None, None, C.byref(res))
-        _lib.check(rc, ctx.handle)
-        if method == "pbicgsafe":
-            assert res.status == 0, f"solve did not converge: status {res.status}"
-        return res
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
 
-    # warm-up (graph capture, occupancy queries, clocks)
     for _ in range(max(args.warmup, 3)):
-        solve_dev()
-    # timed region: K solves, HBM-resident inputs, CUDA events on the solver stream
-    sampler = ClockSampler(dev)
+        out = solve_once()
+    sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     time.sleep(0.3)
-    if world > 1:
-        torch.distributed.barrier()
+    barrier()
     torch.cuda.synchronize()
     total_it, total_ms, launches = 0, 0.0, 0
-    results = []
     for _ in range(args.steps):
-        res = solve_dev()
-        total_it += res.iterations
-        total_ms += res.device_ms
-        launches += res.kernel_launches
-        results.append(res)
+        out = solve_once()
+        total_it += out.iterations
+        total_ms += out.device["device_ms"]
+        launches += out.device["kernel_launches"]
     torch.cuda.synchronize()
-    # per-kernel durations, same workload, event-bracketed launches
-    tres = [solve_dev(timing=True) for _ in range(args.steps)]
-    torch.cuda.synchronize()
+    barrier()
     clocks = sampler.stop()
+    # schedule evidence (device clock), outside the timed region
+    ev = solve_once(eng_ev)
+    stamps = ev.device["stamps"]  # [parts on this process, iterations, 8]
     if world > 1:
         t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    iters_per_s = total_it / (total_ms / 1e3)  # iterations of the one global solve
+    iters_per_s = total_it / (total_ms / 1e3)
 
-    # roofline of the dominant kernel.  Matrix bytes at SURVEY 8(d)'s 12 B per
-    # nonzero (f64 value + int32 column) + row_ptr; the staged engine actually
-    # streams 10 B (u16 window-local columns), so `traffic` can sit below it.
     peak, peak_src = peaks()
-    part = dsys is not None
-    # bytes per rank: the row slab this GPU owns (the whole system at N = 1)
-    nr, nz = (n_loc, int(dm.nnz)) if part else (n, nnz)
-    m_a = 12 * nz + 8 * (nr + 1)
-    if part:
-        # multi-GPU schedule (csrc/pbsafe.cu dist_iter): K1 As = A s alone so the
-        # all-gather overlaps it, K2 the row-local update, K3 with all nine dots
-        k12_bytes = m_a + 2 * 8 * nr   # s gather, As write
-        k2_bytes = 20 * 8 * nr         # r p u s t y As l g w z x reads, p u w t z y x r writes
-        k3_bytes = m_a + 12 * 8 * nr   # w gather, As l g s y r r0s t reads, l g s writes
-        it_bytes_fused = 2 * m_a + 34 * 8 * nr
-    else:
-        k3_bytes = m_a + 11 * 8 * nr    # w gather, As l g s y r r0s reads, l g s writes (+ dots a c d g)
-        k12_bytes = m_a + 21 * 8 * nr   # s gather, r p u t y l g w z x r0s reads, As p u w t z y x r writes (+ b e f h r)
-        it_bytes_fused = 2 * m_a + 32 * 8 * nr  # this schedule: K1+K2 fused (As not re-read)
-    it_bytes = 2 * m_a + 34 * 8 * nr  # SURVEY 8(d) three-phase minimum (K1, K2, K3)
-    kms = {name: sum(r.kernel_ms[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
-    kcnt = {name: sum(r.kernel_count[j] for r in tres) for j, name in enumerate(_lib.KERNEL_KINDS)}
-    k3_avg = kms["K3_Aw_epilogue"] / max(kcnt["K3_Aw_epilogue"], 1)
-    k3_gbs = k3_bytes / (k3_avg * 1e-3) / 1e9
-    k12_avg = kms["K1_As"] / max(kcnt["K1_As"], 1)
-    k12_gbs = k12_bytes / (k12_avg * 1e-3) / 1e9
-    k1_label = ("K1 (As = A s on the halo-exchanged s; the all-gather overlaps it)" if part else
-                "K12 (As CSR SpMV + fused p u w t z y x r updates + dots b e f h r)")
-    if kms["K1_As"] > kms["K3_Aw_epilogue"]:  # dominant kernel = larger share of the step
-        dom = (k1_label, k12_bytes, k12_avg, k12_gbs, "K1_As")
-    else:
-        dom = ("K3 (Aw CSR SpMV + l,g,s updates + all nine dots; all-gather + finalize follow)" if part else
-               "K3 (Aw CSR SpMV + l,g,s updates + dots a c d g + fused check)", k3_bytes, k3_avg, k3_gbs,
-               "K3_Aw_epilogue")
-    tim_ms = sum(r.device_ms for r in tres)
-    traffic = None
-    tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")  # from the committed ncu --set full capture
-    if os.path.exists(tr_path) and not part:  # the capture is of the single-GPU fused kernels
-        try:
-            traffic = json.load(open(tr_path)).get(dom[4], {}).get("dram_bytes_per_launch")
-        except Exception:
-            traffic = None
+    stencil = args.operator == "stencil"
+    # per-partition algorithmic bytes over the largest slab
+    sl = max(slabs, key=lambda s: s.n_own)
+    pm = max(mats, key=lambda m: m.n_rows)
+    nloc, nz = sl.n_own, int(pm.nnz)
+    m_a = 0 if stencil else 12 * nz + 8 * (nloc + 1)
+    k1_bytes = m_a + 2 * 8 * nloc      # s gather, As write
+    k3_bytes = m_a + 11 * 8 * nloc     # w gather, As l g s y r r0s reads, l g s writes (dots a c d g)
+    it_bytes = 2 * m_a + 34 * 8 * nloc
+    p0 = stamps[0]
+    k1 = [(r[1] - r[0]) * 1e-9 for r in p0[1:] if r[0] >= 0 and r[1] >= 0]
+    k3 = [(r[3] - r[2]) * 1e-9 for r in p0[1:] if r[2] >= 0 and r[3] >= 0]
     kernels = {}
-    per_kind = [("K1_As", k12_bytes), ("K3_Aw_epilogue", k3_bytes)] + ([("K2_update", k2_bytes)] if part else [])
-    for name, byt in per_kind:
-        if kcnt[name]:
-            avg = kms[name] / kcnt[name]
-            kernels[name] = {"avg_us": avg * 1e3, "alg_bytes": byt, "GBps": byt / (avg * 1e-3) / 1e9,
-                             "frac": byt / (avg * 1e-3) / 1e9 / peak, "share_of_step": kms[name] / tim_ms}
-    kernels["K1_As"]["name"] = k1_label
-    if kcnt["F_finalize"]:
-        fin = kms["F_finalize"] / kcnt["F_finalize"]
-        kernels["F_finalize"] = {"avg_us": fin * 1e3, "share_of_step": kms["F_finalize"] / tim_ms}
+    for name, durs, byt in (("K1_As", k1, k1_bytes), ("K3_Aw_epilogue", k3, k3_bytes)):
+        if durs:
+            avg = float(np.mean(durs))
+            kernels[name] = {"avg_us": avg * 1e6, "alg_bytes": byt, "GBps": byt / avg / 1e9,
+                             "frac": byt / avg / 1e9 / peak}
+    kernels["K1_As"]["name"] = "K1 (As = A s, interior rows before the halo wait, boundary rows after)"
+    kernels["K3_Aw_epilogue"]["name"] = "K3 (Aw SpMV + l,g,s updates + dots a c d g)"
+    dom = max(kernels.values(), key=lambda k: k["avg_us"])
+    rep = overlap_report(p0)
+    steady = [r for i, r in rep.items() if i >= 1]
+    overlap = {"iterations": len(steady),
+               "overlapped_frac": sum(r["overlapped"] for r in steady) / max(len(steady), 1),
+               "hidden_frac": sum(r["hidden"] for r in steady) / max(len(steady), 1),
+               "reduce_us_median": float(np.median([r["reduce_us"] for r in steady])) if steady else None,
+               "as_us_median": float(np.median([r["as_us"] for r in steady])) if steady else None,
+               "source": "device %globaltimer stamps of partition 0 (csrc/dist.cu), one extra solve"}
 
-    # BASELINE config 2's comparison (outside the timed region): every method
-    # of the drop-in on the same resident operator and right-hand side
-    comparators = None
-    if dsys is None:
-        comparators = {}
-        for mname in ("pbicgsafe", "ssbicgsafe2", "pbicgstab", "bicgstab", "gpbicg"):
-            solve_dev(method=mname, max_iters=4000)  # warm (graph capture)
-            rr_ = solve_dev(method=mname, max_iters=4000)
-            comparators[mname] = {"status": {0: "converged", 1: "max_iters", 2: "breakdown",
-                                             3: "non_finite"}[rr_.status],
-                                  "iterations": int(rr_.iterations), "time_to_tol_ms": rr_.device_ms,
-                                  "it_per_s": rr_.iterations / (rr_.device_ms * 1e-3)}
-        comparators["note"] = ("one device solve each to 1e-10, CSR resident; pbicgstab is the pipelined "
-                               "BiCGStab of Cools & Vanroose BASELINE names (not in the reference; restated in "
-                               "oracle/pbsafe_oracle.c solve_pstab, parity unpinned against reference outputs); "
-                               "bicgstab is the reference's two-reduction BiCGStab (solvers.py:210-327)")
-
-    # e2e through the public API, pinned host buffers, upload + solve + readback per step
+    # e2e through the public API from pinned host buffers
     e2e = None
-    if dsys is not None:
-        # public API of the partitioned path: solve(b_own) from pinned host
-        # memory (the slab stays resident), x_own + history read back
-        b_own = torch.from_numpy(b_dev.cpu().numpy()).pin_memory().numpy()
-        dsys.solve(b_own, config=cfgpb)
-        if world > 1:
-            torch.distributed.barrier()
+    if not loop:
+        b_host = torch.from_numpy(b_parts[0].cpu().numpy()).pin_memory().numpy()
+        slab_host = None
+        if host is not None:
+            _, lrp, lci, lv = local_csr(*host, n, sysd.rank, sysd.nranks)
+            pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
+            slab_host = (pin(lrp), pin(lci.astype(np.int64)), pin(lv))
+
+        def e2e_step():
+            if slab_host is not None:
+                mats[0].update_csr(*slab_host)  # the rank's slab from the host, like solve(CsrMatrix, b)
+            return sysd.solve(b_host, config=cfgpb)
+
+        e2e_step()
+        barrier()
         t0 = time.perf_counter()
         e_it = 0
         for _ in range(args.steps):
-            out = dsys.solve(b_own, config=cfgpb)
-            e_it += out.iterations
+            o = e2e_step()
+            e_it += o.iterations
+        barrier()
+        dt = time.perf_counter() - t0
         if world > 1:
-            torch.distributed.barrier()
-        dt = time.perf_counter() - t0
-        e2e = {"value": e_it / dt, "unit": "it/s", "h2d_bytes_per_step": int(b_own.nbytes),
-               "d2h_bytes_per_step": int(8 * n_loc + out.iterations * 41),
-               "ms_per_step": dt / args.steps * 1e3,
-               "note": "wall clock around DistributedSystem.solve(b_own) on every rank; slab resident"}
-    elif world == 1:
-        pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
-        A_host = pb.CsrMatrix(n, n, pin(rp), pin(ci), pin(v))
-        b_host = pin(b_dev.cpu().numpy())
-        # warm-up steps: graphs, the workspace cache and the two page-locked
-        # result blocks the loop alternates between (x of step k is alive
-        # while step k+1 allocates its own)
-        for _ in range(max(2, args.warmup)):
-            out = pb.solve(A_host, b_host, config=cfgpb)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e_it = 0
-        for _ in range(args.steps):
-            out = pb.solve(A_host, b_host, config=cfgpb)
-            e_it += out.iterations
-        dt = time.perf_counter() - t0
-        h2d = rp.nbytes + ci.nbytes + v.nbytes + b_host.nbytes
-        d2h = 8 * n + out.iterations * (8 + 1 + 32)
+            t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            dt = float(t.item())
+        h2d = b_host.nbytes + (sum(a.nbytes for a in slab_host) if slab_host else 0)
         e2e = {"value": e_it / dt, "unit": "it/s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h), "ms_per_step": dt / args.steps * 1e3,
-               "note": "wall clock around solve(CsrMatrix, b): CSR (int64 col_idx) + b H2D, "
-                       "int64->int32 narrowing, solve, x + history D2H"}
-
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:  # the CPU baseline: rank 0 at N = 1 only
-        threads = os.cpu_count() or 1
-        b_host_np = b_dev.cpu().numpy()
-        cpu = cpu_baseline(rp, ci, v, b_host_np, iters=args.cpu_iters, threads=threads)
-
+               "d2h_bytes_per_step": int(8 * slabs[0].n_own + o.iterations * 41), "ms_per_step": dt / args.steps * 1e3,
+               "note": ("per rank: the slab's CSR (int64 columns) re-uploaded into the resident partition "
+                        "(pbs_csr_update) + b_own H2D, solve, x_own + history D2H" if slab_host else
+                        "per rank: b_own H2D, solve, x_own + history D2H; the slab operator is generated on "
+                        "its GPU once from the stencil") + "; wall clock, max over ranks"}
     if rank == 0:
-        avg_it = total_it / args.steps
         line = {
             "metric": METRIC, "value": iters_per_s, "unit": "it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": WORKLOAD, "operator": "csr", "iterations_per_solve": avg_it,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[cfg_name] + (", matrix-free stencil slabs" if stencil else
+                                                          ", fp64 CSR slabs"),
+                       "operator": args.operator, "iterations_per_solve": total_it / args.steps,
                        "time_to_tol_ms": total_ms / args.steps,
-                       "parallelism": (f"row partition x{world} (NCCL halo + compensated all-gather)"
-                                       if part else "single GPU"),
-                       "l2": "inputs larger than L2: CSR 192 MB + 18 workspace vectors 302 MB per solve "
-                             "vs 126 MB L2",
-                       "graphs": True},
-            "roofline": {"bound": "hbm", "achieved": dom[3], "peak": peak, "unit": "GB/s",
-                         "frac": dom[3] / peak, "traffic": traffic, "kernel": dom[0],
-                         "alg_bytes_per_launch": dom[1], "avg_launch_us": dom[2] * 1e3,
-                         "peak_source": peak_src},
-            "iteration_roofline": {"alg_bytes_per_iter": it_bytes,
-                                   "achieved_GBps": it_bytes * iters_per_s / world / 1e9,
-                                   "frac": it_bytes * iters_per_s / world / 1e9 / peak,
-                                   "note": ("per rank: B_iter = 2*(12 nnz + 8(n+1)) + 34*8n over the rank's "
-                                            "row slab (SURVEY 8(d)); the multi-GPU schedule moves exactly that"
-                                            if part else
-                                            "B_iter = 2*(12 nnz + 8(n+1)) + 34*8n (SURVEY 8(d)); this "
-                                            "schedule moves 2*(12 nnz+8(n+1)) + 32*8n (K1+K2 fused)"),
-                                   "frac_own_schedule": it_bytes_fused * iters_per_s / world / 1e9 / peak},
+                       "parallelism": (f"loopback: {nparts} row partitions in one process on one GPU "
+                                       f"(sms/{nparts} each; not a scaling measurement)" if loop else
+                                       f"row partition x{world} ({args.transport}: "
+                                       + ("copy-engine halo pushes into IPC-mapped peers + published records"
+                                          if args.transport == "p2p" else "NCCL send/recv + all-gather") + ")"),
+                       "slab_rows": [s.n_own for s in slabs] if loop else sl.n_own,
+                       "l2": "operator + workspace per GPU >> 126 MB L2" if cfg_name == "c4" else
+                             "per-GPU working set may approach L2 at large N (config 2 is 494 MB in total)"},
+            "roofline": {"bound": "hbm", "achieved": dom["GBps"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
+                         "traffic": None, "kernel": dom["name"], "alg_bytes_per_launch": dom["alg_bytes"],
+                         "avg_launch_us": dom["avg_us"], "peak_source": peak_src,
+                         "timing": "device %globaltimer: first CTA start to last CTA end, per launch"},
+            "iteration_roofline": {"alg_bytes_per_iter_per_gpu": it_bytes,
+                                   "achieved_GBps_per_gpu": it_bytes * iters_per_s / 1e9,
+                                   "frac": it_bytes * iters_per_s / 1e9 / peak,
+                                   "note": "B_iter = 2*M_A + 34*8n over the largest slab (SURVEY 8(d)); the "
+                                           "multi-GPU schedule moves exactly that"},
             "kernels": kernels,
-            "comparators": comparators,
-            "timing_mode_it_per_s": sum(r.iterations for r in tres) / (tim_ms / 1e3),
+            "overlap": overlap,
             "e2e": e2e,
-            "cpu_baseline": cpu,
+            "cpu_baseline": None,
             "gpu_launches": launches,
             "clocks": clocks,
         }
         emit(line)
-    if dsys is not None:
-        dsys.close()
+    sysd.close()
     if world > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def _solve_dev_partition(_lib, ctx, mat, b_dev, x_dev, cfgpb, engine):
+    """One partitioned solve on this rank's partition, device b / x (pbs_solve_dev)."""
+    import ctypes as C
+
+    from paper_2108_10591_b200.solvers import _build_outcome, _history_buffers, _make_config, _raise_for
+
+    cfg, keep = _make_config(cfgpb, engine)
+    rel, flags, coef = _history_buffers(cfgpb)
+    res = _lib.Result()
+    rc = _lib.load().pbs_solve_dev(mat.handle, _lib.METHOD_IDS["pbicgsafe"], C.c_void_p(b_dev.data_ptr()), None,
+                                   C.byref(cfg), C.c_void_p(x_dev.data_ptr()), rel.ctypes.data_as(C.c_void_p),
+                                   flags.ctypes.data_as(C.c_void_p), coef.ctypes.data_as(C.c_void_p), C.byref(res))
+    _raise_for(rc, res, ctx.handle)
+    return _build_outcome("pbicgsafe", cfgpb, engine, res, None, rel, flags, coef, keep)
 
 
 _JSON_OUT = None
@@ -428,6 +610,28 @@ def emit(line):
     out.flush()
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without torchrun's environment: run this script under
+    torch.distributed.run with N processes (one per GPU) and pass rank 0's
+    JSON line through."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    p = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=None, text=True, env={**os.environ})
+    for ln in p.stdout.splitlines():
+        if ln.strip().startswith("{"):
+            emit(json.loads(ln))
+    return p.returncode
+
+
 def main():
     global _JSON_OUT
     sys.stdout.flush()
@@ -439,13 +643,26 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="c2", choices=("c2", "c4"))
+    ap.add_argument("--operator", default="csr", choices=("csr", "stencil"))
+    ap.add_argument("--loopback", type=int, default=0, help="P partitions in this process on one GPU")
+    ap.add_argument("--partitioned", action="store_true", help="the multi-GPU schedule even at N=1")
+    ap.add_argument("--transport", default="p2p", choices=("p2p", "nccl"))
     ap.add_argument("--cpu-iters", type=int, default=600)  # ~10 s on a 16-core host
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--partitioned", action="store_true", help="use the multi-GPU schedule even at N=1")
+    ap.add_argument("--no-comparators", action="store_true")
     args = ap.parse_args()
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # compute, halo and comm streams on separate queues
+    rank, world, _ = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
-    return run_ours(args)
+    if world > 1 or args.loopback > 1 or args.partitioned:
+        return run_partitioned(args)
+    return run_single(args)
 
 
 if __name__ == "__main__":

@@ -194,6 +194,11 @@ int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
 /* constant-coefficient stencil on a k^dim grid, C order (last axis fastest);
  * offsets int32[npts*dim] ((dz,)dy,dx per point) sorted by flattened offset,
  * coeffs f64[npts].  npts <= 27. */
+/* upload new arrays of the same shape (n_rows, nnz) into an existing CSR
+ * operator (e.g. a resident partition slab): its workspace and halo plan
+ * stay */
+int pbs_csr_update(pbs_mat* mat, const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
+                   const double* values);
 int pbs_stencil_create(pbs_ctx* ctx, int32_t dim, int64_t k, int32_t npts,
                        const int32_t* offsets, const double* coeffs, pbs_mat** mat);
 /* CSR of a stencil operator built on the device (rows in C order, columns

@@ -573,30 +573,12 @@ int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   return m->stencil ? PBS_OK : build_window_cols(ctx, m);
 }
 
-PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
-                              const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
-                              const double* values, pbs_mat** out) {
-  if (!ctx || !out) return set_err(ctx, PBS_ERR_INVALID, "NULL argument");
-  if (n_rows < 0 || n_cols < 0 || nnz < 0) return set_err(ctx, PBS_ERR_INVALID, "negative matrix dimension");
-  if (n_cols > 0x7fffffffLL) return set_err(ctx, PBS_ERR_INVALID, "n_cols exceeds the int32 column index range");
-  if (col_bytes != 4 && col_bytes != 8) return set_err(ctx, PBS_ERR_INVALID, "col_bytes must be 4 or 8");
-  if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
-    return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with nnz arrays");
-  CK(cudaSetDevice(ctx->device));
-  if (ctx->ws_cache && ctx->ws_cache->n != n_rows) drop_ws_cache(ctx);  // cannot match: release it now
-  pbs_mat* m = new pbs_mat();
-  m->ctx = ctx;
-  m->n_rows = n_rows;
-  m->n_cols = n_cols;
-  m->nnz = nnz;
+// copy a host CSR into m's device buffers (int64 indices narrowed on the
+// device, with a range check), then the x windows / window-local columns
+static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
+                         const double* values) {
+  const long long n_rows = m->n_rows, n_cols = m->n_cols, nnz = m->nnz;
   cudaStream_t s = ctx->stream;
-  // padding: the pipelined SpMV bulk-copies 16-byte-aligned windows
-  CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n_rows + 4)));
-  CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
-  CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
-  CK(cudaMemsetAsync(m->rp + n_rows + 1, 0, sizeof(long long) * 3, s));
-  CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
-  CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
   CK(cudaMemcpyAsync(m->rp, row_ptr, sizeof(long long) * (n_rows + 1), cudaMemcpyHostToDevice, s));
   if (nnz > 0) {
     CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
@@ -621,24 +603,68 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
       CK(cudaStreamSynchronize(s));
       pool_free(ctx, tmp);
       pool_free(ctx, bad);
-      if (hbad) {
-        pbs_mat_free(m);
-        return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
-      }
+      if (hbad) return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
     }
   }
   CK(cudaStreamSynchronize(s));
+  m->blk_nnz_max = 0;
   for (long long r0 = 0; r0 < n_rows; r0 += kPipeRows) {
     const long long r1 = r0 + kPipeRows < n_rows ? r0 + kPipeRows : n_rows;
     const long long bn = row_ptr[r1] - row_ptr[r0];
     if (bn > m->blk_nnz_max) m->blk_nnz_max = bn;
   }
-  int rc = compute_xwin(ctx, m);
+  return compute_xwin(ctx, m);
+}
+
+PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                              const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
+                              const double* values, pbs_mat** out) {
+  if (!ctx || !out) return set_err(ctx, PBS_ERR_INVALID, "NULL argument");
+  if (n_rows < 0 || n_cols < 0 || nnz < 0) return set_err(ctx, PBS_ERR_INVALID, "negative matrix dimension");
+  if (n_cols > 0x7fffffffLL) return set_err(ctx, PBS_ERR_INVALID, "n_cols exceeds the int32 column index range");
+  if (col_bytes != 4 && col_bytes != 8) return set_err(ctx, PBS_ERR_INVALID, "col_bytes must be 4 or 8");
+  if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
+    return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with nnz arrays");
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->ws_cache && ctx->ws_cache->n != n_rows) drop_ws_cache(ctx);  // cannot match: release it now
+  pbs_mat* m = new pbs_mat();
+  m->ctx = ctx;
+  m->n_rows = n_rows;
+  m->n_cols = n_cols;
+  m->nnz = nnz;
+  cudaStream_t s = ctx->stream;
+  // padding: the pipelined SpMV bulk-copies 16-byte-aligned windows
+  CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n_rows + 4)));
+  CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
+  CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
+  CK(cudaMemsetAsync(m->rp + n_rows + 1, 0, sizeof(long long) * 3, s));
+  CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
+  CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
+  int rc = upload_arrays(ctx, m, row_ptr, col_idx, col_bytes, values);
   if (rc) {
     pbs_mat_free(m);
     return rc;
   }
   *out = m;
+  return PBS_OK;
+}
+
+// Upload new CSR arrays of the same shape (n_rows, nnz) into an existing
+// operator: the end-to-end step of a resident, partitioned operator (its
+// workspace, halo plan and peer mappings stay; the window-local columns are
+// rebuilt).
+PBS_EXPORT int pbs_csr_update(pbs_mat* m, const int64_t* row_ptr, const void* col_idx, int32_t col_bytes,
+                              const double* values) {
+  if (!m || m->stencil) return set_err(m ? m->ctx : nullptr, PBS_ERR_INVALID, "need a CSR operator");
+  pbs_ctx* ctx = m->ctx;
+  if (col_bytes != 4 && col_bytes != 8) return set_err(ctx, PBS_ERR_INVALID, "col_bytes must be 4 or 8");
+  if (row_ptr[0] != 0 || row_ptr[m->n_rows] != m->nnz)
+    return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with the operator's nnz");
+  CK(cudaSetDevice(ctx->device));
+  const XWin old = m->xwin;
+  int rc = upload_arrays(ctx, m, row_ptr, col_idx, col_bytes, values);
+  if (rc) return rc;
+  if (m->ws && memcmp(&old, &m->xwin, sizeof(XWin)) != 0) free_graphs(m->ws);  // graphs bake the windows in
   return PBS_OK;
 }
 

@@ -88,6 +88,24 @@ class DeviceMatrix:
         _lib.check(_lib.load().pbs_stencil_to_csr(self.handle, C.byref(h)), self.ctx.handle)
         return DeviceMatrix(h, self.ctx, self.n_rows, self.n_cols, self.nnz, False, self.source + "->csr")
 
+    def update_csr(self, row_ptr, col_idx, values) -> None:
+        """Upload new arrays of the same shape into this CSR operator (its
+        workspace and, for a partition slab, its halo plan and peer mappings
+        stay): pbs_csr_update."""
+        rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        if col_idx.dtype == np.int32:
+            ci, cb = np.ascontiguousarray(col_idx), 4
+        else:
+            ci, cb = np.ascontiguousarray(col_idx, dtype=np.int64), 8
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        if rp.shape != (self.n_rows + 1,) or ci.shape != (self.nnz,) or v.shape != (self.nnz,):
+            raise ValueError("update_csr needs arrays of the operator's shape")
+        rc = _lib.load().pbs_csr_update(self.handle, rp.ctypes.data_as(C.c_void_p), ci.ctypes.data_as(C.c_void_p),
+                                         cb, v.ctypes.data_as(C.c_void_p))
+        if rc == _lib.PBS_ERR_INVALID:
+            raise ValueError(_lib.last_error(self.ctx.handle))
+        _lib.check(rc, self.ctx.handle)
+
     def spmv_dev(self, x_ptr: int, y_ptr: int) -> int:
         """y = A x on device pointers; returns the first non-finite row or -1."""
         bad = C.c_int64()
