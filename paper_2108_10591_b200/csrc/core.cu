@@ -930,6 +930,7 @@ PBS_EXPORT int pbs_stencil_slab(pbs_mat* st, int64_t row_lo, int64_t row_hi, int
   pbs_mat* m = new pbs_mat();
   *m = *st;
   m->ws = nullptr;
+  m->zm_maps.clear();  // tensor maps describe the whole grid's vectors
   m->part = Partition{};
   const long long n_own = row_hi - row_lo;
   m->n_rows = n_own;

@@ -15,6 +15,7 @@
 #include "common.cuh"
 #include "spmv.cuh"
 #include "vec.cuh"
+#include "zmarch.cuh"
 
 using namespace pbs;
 
@@ -40,6 +41,10 @@ struct EventPool {
 };
 
 struct pbs_dist;  // dist.cu
+
+struct ZmMap {  // a CUtensorMap that std::map can hold (64-byte aligned)
+  CUtensorMap map;
+};
 
 // Multi-GPU row partition of an operator (dist.cu, include/pbsafe.h).  The
 // partition's SpMV inputs live in an extended space [pad | left halo | own |
@@ -106,6 +111,7 @@ struct pbs_mat {
   long long blk_nnz_max = 0;  // most nonzeros in one 256-row block (chunk sizing)
   Partition part;  // multi-GPU row partition (part.dist == nullptr: single GPU)
   Workspace* ws = nullptr;
+  std::map<const double*, ZmMap> zm_maps;  // z-marching engine: tensor map per input vector
 };
 
 static inline int set_err(pbs_ctx* ctx, int code, const std::string& msg) {
@@ -282,9 +288,9 @@ static inline int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-
 // 1 staged CSR, 2 staged stencil, 4 direct stencil.  Default 1: the staged
 // CSR engine gains (its producer streams matrix chunks before the wait);
 // the direct stencil engine loses (profiles/sweeps/r1_pdl.log).
-enum { kPdlCsrPipe = 1, kPdlStencilPipe = 2, kPdlStencilDirect = 4 };
+enum { kPdlCsrPipe = 1, kPdlStencilPipe = 2, kPdlStencilDirect = 4, kPdlStencilZm = 8 };
 static inline bool use_pdl(int engine) {
-  static int v = env_int("PBS_PDL", kPdlCsrPipe, 0, 7);
+  static int v = env_int("PBS_PDL", kPdlCsrPipe | kPdlStencilZm, 0, 15);
   return (v & engine) != 0;
 }
 static inline int pipe_slots_cap() {
@@ -389,6 +395,99 @@ static bool stencil_engine_pipe(int npts) {
   return v == 2 ? (Epi::kStencilPipe || npts > 7) : v == 1;
 }
 
+// The z-marching engine (zmarch.cuh) takes every 3D 7- and 27-point stencil
+// product whose rows are whole planes of a grid with an even edge
+// (PBS_STENCIL_ENGINE=pipe|direct forces the older engines for A/B runs).
+// PBS_ZM_RING: plane stages per CTA; PBS_ZM_WAVES: work items per CTA
+// (the z-chunk length follows).
+static inline bool stencil_zm_ok(const pbs_mat* m, long long lo, long long hi) {
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("PBS_STENCIL_ENGINE");
+    forced = (e && (std::string(e) == "pipe" || std::string(e) == "direct")) ? 1 : 0;
+  }
+  if (!m->stencil) return false;
+  const StencilView& S = m->sv;
+  if (forced || S.dim != 3 || (S.npts != 7 && S.npts != 27) || (S.k & 1) || S.k < 4) return false;
+  for (int p = 0; p < S.npts; ++p)  // the engine's compile-time neighbour table
+    for (int a = 0; a < 3; ++a)
+      if (S.off[p][a] != (S.npts == 27 ? zm_off<27>(p, a) : zm_off<7>(p, a))) return false;
+  const long long k2 = S.k2;
+  return !(lo % k2 || hi % k2 || S.g0 % k2 || (-S.xlo) % k2 || S.xhi % k2 || hi <= lo);
+}
+
+static inline bool stencil_zm_geom(pbs_ctx* ctx, int sms, const pbs_mat* m, long long lo, long long hi,
+                                   const void* kernel, size_t* smem, int* grid, ZmGeom* G) {
+  if (!stencil_zm_ok(m, lo, hi)) return false;
+  const StencilView& S = m->sv;
+  const long long k2 = S.k2;
+  static int ring_env = env_int("PBS_ZM_RING", 8, 4, kZmMaxRing);
+  static int waves_env = env_int("PBS_ZM_WAVES", 8, 1, 64);
+  G->tiles_y = (int)((S.k + kZmTY - 1) / kZmTY);
+  G->tiles_x = (int)((S.k + kZmTX - 1) / kZmTX);
+  G->z_lo = (int)(lo / k2);
+  G->z_hi = (int)(hi / k2);
+  G->zx_lo = (int)(S.xlo / k2);
+  G->zx_hi = (int)(S.xhi / k2);
+  G->gz0 = S.g0 / k2;
+  G->ring = ring_env;
+  *smem = 256 + sizeof(double) * (size_t)kZmStage * G->ring;
+  auto it = ctx->occ.find(kernel);
+  if (it == ctx->occ.end() || (size_t)it->second < *smem) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
+      return false;
+    ctx->occ[kernel] = (int)*smem;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kZmCTA, *smem);
+  if (per_sm < 1) per_sm = 1;
+  const long long ntiles = (long long)G->tiles_y * G->tiles_x, nz = G->z_hi - G->z_lo;
+  const long long cap = (long long)sms * per_sm;
+  // about waves_env work items per CTA, each a run of >= 2 planes
+  long long zc = (nz * ntiles + cap * waves_env - 1) / (cap * waves_env);
+  if (zc < 2) zc = 2;
+  if (zc > nz) zc = nz;
+  G->zchunk = (int)zc;
+  const long long items = ntiles * ((nz + zc - 1) / zc);
+  *grid = (int)(items < cap ? items : cap);
+  return true;
+}
+
+// The 3-D tensor map of a stencil operator's input vector x for the
+// z-marching engine: dims (k, k, planes present), box (TX+4, TY+2, 1), zeros
+// out of range.  Encoded once per (operator, x) and kept in the operator.
+typedef CUresult (*PfnTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                            CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                            CUtensorMapFloatOOBfill);
+static inline const CUtensorMap* stencil_zm_map(pbs_mat* m, const double* x, const ZmGeom& G) {
+  auto it = m->zm_maps.find(x);
+  if (it != m->zm_maps.end()) return &it->second.map;
+  if (m->zm_maps.size() >= 64) m->zm_maps.clear();  // callers' temporary x buffers
+  static PfnTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", (void**)&encode, 12000, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess) {
+      encode = nullptr;
+      return nullptr;
+    }
+  }
+  const StencilView& S = m->sv;
+  const cuuint64_t dims[3] = {(cuuint64_t)S.k, (cuuint64_t)S.k, (cuuint64_t)(G.zx_hi - G.zx_lo)};
+  const cuuint64_t strides[2] = {(cuuint64_t)S.k * sizeof(double), (cuuint64_t)S.k2 * sizeof(double)};
+  const cuuint32_t box[3] = {kZmRowW, kZmTY + 2, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  ZmMap zm;
+  void* base = (void*)(x + (long long)G.zx_lo * S.k2);
+  if (encode(&zm.map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return nullptr;
+  return &m->zm_maps.emplace(x, zm).first->second.map;
+}
+
 template <class Epi, int DIM, int NP>
 static int stencil_pipe_set_smem(pbs_ctx* ctx, size_t smem) {
   const void* k = (const void*)stencil_pipe_kernel<Epi, DIM, NP>;
@@ -459,6 +558,9 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   pbs_mat* m = L.m;
   long long nblk = (hi - lo + kThreads - 1) / kThreads;
   int grid;
+  ZmGeom zm;
+  size_t zm_smem = 0;
+  const CUtensorMap* zm_map = nullptr;
   if (!m->stencil && csr_engine_tpr()) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, nullptr};
     if (csr_engine_tpr() == 2) {
@@ -496,6 +598,20 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, false>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
                  cstages, chunk);
     if (L.err) return 0;
+  } else if (m->stencil &&
+             stencil_zm_geom(L.ctx, L.sms(), m, lo, hi,
+                             m->sv.npts == 27 ? (const void*)stencil_zm_kernel<Epi, 27>
+                                              : (const void*)stencil_zm_kernel<Epi, 7>,
+                             &zm_smem, &grid, &zm) &&
+             (zm_map = stencil_zm_map(m, x, zm)) != nullptr) {
+    grid = L.cap_grid(grid);
+    StencilView S = m->sv;
+    S.row_lo = lo;
+    S.row_hi = hi;
+    if (S.npts == 27)
+      launch_pdl(L, kPdlStencilZm, stencil_zm_kernel<Epi, 27>, grid, kZmCTA, zm_smem, S, *zm_map, epi, zm);
+    else
+      launch_pdl(L, kPdlStencilZm, stencil_zm_kernel<Epi, 7>, grid, kZmCTA, zm_smem, S, *zm_map, epi, zm);
   } else if (m->stencil && m->xwin.nwin && stencil_engine_pipe<Epi>(m->sv.npts)) {
     StencilView S = m->sv;
     S.row_lo = lo;

@@ -22,7 +22,10 @@ static void setup_pipelined(Launcher& L, Workspace* ws, const Mode& md) {
 // (Aw + l g s + the fused check of j+1)
 static void iter_steady(Launcher& L, Workspace* ws, const Mode& md) {
   auto& V = ws->V.v;
-  if (!md.plan && !k3_dots_split() && k12_dots() && (!L.m->stencil || k12_dots() == 2)) {
+  // the batch split between K12 and K3: CSR, and stencils on the z-marching
+  // engine (register room for the five accumulators)
+  const bool split = !L.m->stencil || k12_dots() == 2 || stencil_zm_ok(L.m, 0, ws->n);
+  if (!md.plan && !k3_dots_split() && k12_dots() && split) {
     const int fuse = L.trace_cfg || !fuse_check() ? 0 : 1;
     const int np12 = spmv_launch(L, ws->X.v[VS], epi_k12d(ws, md), 0, ws->n, KK1);
     const int grid = spmv_launch(L, ws->X.v[VW], epi_k3s(ws, md, fuse, np12), 0, ws->n, KK3);
