@@ -682,8 +682,12 @@ static void iter_steps(std::vector<Step>& st, long long j, bool replace) {
 // p o u, then w = A u + t z y x r
 static void ss_iter_steps(std::vector<Step>& st, long long j) {
   st.push_back([](Part& P) { push(P, VR); });
-  st.push_back([](Part& P) {
-    P.np = halo_spmv(P, VR, KK1, [&](int off) { return epi_dots_parts(P.ws, 1, off); });
+  st.push_back([j](Part& P) {
+    P.np = halo_spmv(P, VR, KK1, [&](int off) {
+      EpiDots e = epi_dots_parts(P.ws, 1, off);
+      e.stamp = stamp_at(P, j, kStK1);  // the spine product (A r) in the As slot
+      return e;
+    });
     P.np2 = 0;
   });
   st.push_back([j](Part& P) { publish(P, j); });

@@ -406,9 +406,14 @@ static inline bool stencil_zm_ok(const pbs_mat* m, long long lo, long long hi) {
     const char* e = getenv("PBS_STENCIL_ENGINE");
     forced = (e && (std::string(e) == "pipe" || std::string(e) == "direct")) ? 1 : 0;
   }
+  // 7-point stencils stay on the direct / staged engines by default: their
+  // rows read 3 planes of only 7 points, which the L1-cached direct engine
+  // (K12, K1) and the staged engine (K3) already stream near the copy peak
+  // (config 2 matrix-free: 8861 vs 8785 it/s); PBS_ZM7=1 moves them too
+  static int zm7 = env_int("PBS_ZM7", 0, 0, 1);
   if (!m->stencil) return false;
   const StencilView& S = m->sv;
-  if (forced || S.dim != 3 || (S.npts != 7 && S.npts != 27) || (S.k & 1) || S.k < 4) return false;
+  if (forced || S.dim != 3 || (S.npts != 27 && !(S.npts == 7 && zm7)) || (S.k & 1) || S.k < 4) return false;
   for (int p = 0; p < S.npts; ++p)  // the engine's compile-time neighbour table
     for (int a = 0; a < 3; ++a)
       if (S.off[p][a] != (S.npts == 27 ? zm_off<27>(p, a) : zm_off<7>(p, a))) return false;

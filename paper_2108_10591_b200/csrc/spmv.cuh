@@ -234,18 +234,28 @@ struct EpiDots {  // s = A r, then the batch partials over (s, y, r, r0s, t)
   int tag;
   int spine;
   DotSink sink;
+  unsigned long long* stamp;  // nullable: [~start, end] of the product (see EpiStore)
   const double* in[kIn];  // y r r0s t
   Dots9 d;
   __device__ bool active() const { return spine ? gate_spine(st) : gate_all(st); }
   __device__ void on_skip() const {}
-  __device__ void init() { d.zero(); }
+  __device__ void init() {
+    if (stamp && threadIdx.x == 0) atomicMax(stamp, ~gtime());
+    d.zero();
+  }
   __device__ void row(long long i, double v, const double* in4) {
     s[i] = v;
     if (!isfinite(v)) report_nonfinite(st, tag, i);
     if (sink.partials) d.add_row(v, in4[0], in4[1], in4[2], in4[3]);
   }
   template <int NT, bool NAMED>
-  __device__ void finish() { sink.finish<NT, NAMED>(d, st); }
+  __device__ void finish() {
+    if (stamp) {
+      block_bar<NT, NAMED>();
+      if (threadIdx.x == 0) atomicMax(stamp + 1, gtime());
+    }
+    sink.finish<NT, NAMED>(d, st);
+  }
 };
 
 // DOTS: also the partials of the s-independent dots of the next check (b e f

@@ -109,24 +109,30 @@ _KINDS = {0: REDUCE_START, 1: REDUCE_END, 2: SPMV_START, 3: SPMV_END, 4: COEFF_R
 _TAGS = {0: None, 1: "Ax", 2: "Ar", 3: "As", 4: "Aw", 5: "Ao", 6: "Au", 7: "At", 8: "Ay"}
 
 
-def stamps_to_records(stamps) -> list[tuple[int, int, int, float]]:
+def stamps_to_records(stamps, spine: str = "As") -> list[tuple[int, int, int, float]]:
     """Device-clock stamps of one partition ([iterations, 8]: As start/end, Aw
     start/end, publish start/end and finalize start/end of check i, ns; -1
     absent) -> schedule records (iter, kind, tag, t) in the reference's
     vocabulary: the reduction of check i starts when its record is published
     and ends (coefficients ready) when its finalize has run; the products are
     the As and Aw SpMVs of iteration i."""
+    spine_tag = {"As": 3, "Ar": 2}[spine]  # ssBiCGSafe2's spine product is s = A r
     recs = []
     for i, row in enumerate(np.asarray(stamps)):
         as0, as1, aw0, aw1, pub0, _pub1, _fin0, fin1 = (float(v) for v in row)
+        if as0 < 0:
+            # no spine product: the record after max_iters, which the reference
+            # takes with plan_dot outside the loop (solvers.py:736-739), not as a
+            # batch reduction -- its log has no events for it either
+            continue
         if pub0 >= 0:
             recs.append((i, 0, 0, pub0))
         if fin1 >= 0:
             recs.append((i, 1, 0, fin1))
             recs.append((i, 4, 0, fin1))
         if as0 >= 0 and as1 >= 0:
-            recs.append((i, 2, 3, as0))
-            recs.append((i, 3, 3, as1))
+            recs.append((i, 2, spine_tag, as0))
+            recs.append((i, 3, spine_tag, as1))
         if aw0 >= 0 and aw1 >= 0:
             recs.append((i, 2, 4, aw0))
             recs.append((i, 3, 4, aw1))

@@ -242,3 +242,48 @@ def test_overlap_evidence_device_clock(nparts):
         rep = overlap_report(stamps[p])
         steady = [r for i, r in rep.items() if i >= 1]
         assert sum(r["overlapped"] for r in steady) >= 0.9 * len(steady), rep
+
+
+def test_zmarch_engine_on_7point_bitwise():
+    """The z-marching engine is the default for 27-point stencils; 7-point
+    stencils take it with PBS_ZM7=1 (read once per process, hence the
+    subprocess): the plain SpMV and a partitioned solve stay bitwise / on the
+    near-exact run."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np
+from oracle import oracle as orc
+import paper_2108_10591_b200 as pb
+from paper_2108_10591_b200 import problems
+from paper_2108_10591_b200.operators import DeviceMatrix
+from paper_2108_10591_b200.distributed import LoopbackSystem
+spec = problems.convdiff_stencil(3, 40, (1.0, 0.5, 0.25))
+rp, ci, v = problems.stencil_csr(spec)
+x = np.random.default_rng(1).standard_normal(spec.n)
+ref = orc.spmv(rp, ci, v, x)
+import torch
+dm = DeviceMatrix.from_stencil(spec)
+xd = torch.from_numpy(x).cuda()
+yd = torch.empty_like(xd)
+assert dm.spmv_dev(xd.data_ptr(), yd.data_ptr()) == -1
+assert np.array_equal(yd.cpu().numpy(), ref)
+g = LoopbackSystem(3, spec=spec, operator="stencil")
+try:
+    assert np.array_equal(g.spmv(x), ref)
+    b = orc.spmv(rp, ci, v, np.ones(spec.n))
+    out = g.solve(b, config=pb.SolverConfig(tol=1e-10, max_iters=2000))
+finally:
+    g.close()
+ne = orc.solve(rp, ci, v, b, tol=1e-10, max_iters=2000, workers=-1)
+assert out.iterations == ne["iterations"], (out.iterations, ne["iterations"])
+one = pb.solve(dm, b, config=pb.SolverConfig(tol=1e-10, max_iters=2000))
+assert one.iterations == ne["iterations"]
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
+                       env={**os.environ, "PBS_ZM7": "1", "PYTHONPATH": root})
+    assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-3000:]
