@@ -596,10 +596,14 @@ static void run_steps(std::vector<Part>& parts, const std::vector<Step>& steps) 
 }
 
 static void k1_step(Part& P, long long j) {
-  P.L.sm_limit = eff_sms(P) - 1;  // one SM stays free for the comm stream's kernels
+  // room for the comm stream's 1-CTA publish / finalize beside K1: one SM
+  // for the persistent staged engines, one CTA slot per SM for the rest
+  P.L.sm_limit = eff_sms(P) - 1;
   if (P.L.sm_limit < 1) P.L.sm_limit = 1;
+  P.L.leave_room = true;
   halo_spmv(P, VS, KK1, [&](int) { return epi_store_st(P.ws, VAS, PBS_TAG_AS, 1, stamp_at(P, j, kStK1)); });
   P.L.sm_limit = eff_sms(P);
+  P.L.leave_room = false;
 }
 
 // setup (solvers.py:612-631): r0 = b - A x0, r0s = r0; the pipelined methods

@@ -223,6 +223,7 @@ struct Launcher {
   // grid (its partial records must fit the buffer after earlier pieces')
   int sm_limit = 0;
   long long grid_cap = 0;
+  bool leave_room = false;  // many-CTAs-per-SM engines keep one CTA slot per SM free
   int sms() const { return sm_limit > 0 ? sm_limit : ctx->sms; }
   int cap_grid(long long g) const {
     if (grid_cap > 0 && g > grid_cap) g = grid_cap;
@@ -558,6 +559,24 @@ static void launch_pdl(Launcher& L, int engine, void (*kernel)(KArgs...), int gr
   if (e != cudaSuccess) L.err = set_err(L.ctx, PBS_ERR_CUDA, std::string("PDL launch: ") + cudaGetErrorString(e));
 }
 
+// The plain products (no or one epilogue input: setup and replacement
+// SpMVs) of short-row CSR matrices run on the thread-per-row engine: with ~7
+// nonzeros per row the staged engine's consumers wait on their block
+// barriers (56% of warp samples) while each thread pays a block's
+// bookkeeping for one row; at full occupancy with x from L1/L2 the plain
+// SpMV of config 2 takes 41 instead of 50 us (0.84 vs 0.68 of the HBM peak).
+// Not for the multi-GPU schedule's K1 (leave_room): filling every SM it keeps
+// the reduction's 1-CTA kernels from running beside it, and the iteration
+// loses more than K1 gains (5195 vs 5465 it/s, partitioned config 2).  Rows
+// of 27 nonzeros stream better staged (config 4: 4.1 vs 8.7 ms).
+// PBS_PLAIN_TPR=0 keeps the staged engine.
+template <class Epi>
+static bool csr_plain_tpr(const pbs_mat* m) {
+  static int on = env_int("PBS_PLAIN_TPR", 1, 0, 1);
+  return on && (std::is_same<Epi, EpiStore>::value || std::is_same<Epi, EpiResid>::value) &&
+         m->nnz <= 8 * m->n_rows;
+}
+
 template <class Epi>
 static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long long hi, int kind) {
   pbs_mat* m = L.m;
@@ -566,13 +585,20 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   ZmGeom zm;
   size_t zm_smem = 0;
   const CUtensorMap* zm_map = nullptr;
-  if (!m->stencil && csr_engine_tpr()) {
+  if (!m->stencil && (csr_engine_tpr() || (csr_plain_tpr<Epi>(m) && !L.leave_room))) {
     CsrView A{m->rp, m->ci, m->v, lo, hi, m->n_cols, nullptr};
+    // leave_room: one CTA slot per SM stays free for the reduction's 1-CTA
+    // kernels (the multi-GPU K1 overlaps them)
+    auto tpr_grid = [&](const void* k) {
+      const int full = grid_for(L.ctx, k, 1LL << 40, 8, L.sms()) / L.sms();
+      const int per_sm = L.leave_room && full > 1 ? full - 1 : full;
+      return L.cap_grid(grid_for(L.ctx, k, nblk, per_sm, L.sms()));
+    };
     if (csr_engine_tpr() == 2) {
-      grid = L.cap_grid(grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, true>, nblk, 8, L.sms()));
+      grid = tpr_grid((const void*)csr_tpr_kernel<Epi, true>);
       csr_tpr_kernel<Epi, true><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     } else {
-      grid = L.cap_grid(grid_for(L.ctx, (const void*)csr_tpr_kernel<Epi, false>, nblk, 8, L.sms()));
+      grid = tpr_grid((const void*)csr_tpr_kernel<Epi, false>);
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
   } else if (!m->stencil) {
