@@ -327,13 +327,15 @@ def run_single(args):
     # e2e through the public API, pinned host buffers
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
     b_host = pin(b_dev.cpu().numpy())
+    eng_pin = pb.DeviceEngine(pinned_result=True)  # x into page-locked memory (opt-in)
     if rp is not None:
         A_host = pb.CsrMatrix(n, n, pin(rp), pin(ci), pin(v))
-        call, h2d = (lambda: pb.solve(A_host, b_host, config=cfgpb)), rp.nbytes + ci.nbytes + v.nbytes + b_host.nbytes
-        note = ("wall clock around solve(CsrMatrix, b): CSR (int64 col_idx) + b H2D, int64->int32 narrowing, "
-                "solve, x + history D2H")
+        call = lambda: pb.solve(A_host, b_host, config=cfgpb, engine=eng_pin)  # noqa: E731
+        h2d = rp.nbytes + ci.nbytes + v.nbytes + b_host.nbytes
+        note = ("wall clock around solve(CsrMatrix, b, engine=DeviceEngine(pinned_result=True)): CSR (int64 "
+                "col_idx) + b H2D, int64->int32 narrowing, solve, x (page-locked) + history D2H")
     else:
-        call, h2d = (lambda: pb.solve(dm, b_host, config=cfgpb)), b_host.nbytes
+        call, h2d = (lambda: pb.solve(dm, b_host, config=cfgpb, engine=eng_pin)), b_host.nbytes
         note = ("wall clock around solve(DeviceMatrix, b): b H2D, solve, x + history D2H; the operator is "
                 "generated on the device once (config 4's CSR has no host form here: 25 GB)")
     for _ in range(max(2, args.warmup)):
@@ -517,10 +519,12 @@ def run_partitioned(args):
             pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()  # noqa: E731
             slab_host = (pin(lrp), pin(lci.astype(np.int64)), pin(lv))
 
+        eng_pin = pb.DeviceEngine(pinned_result=True)
+
         def e2e_step():
             if slab_host is not None:
                 mats[0].update_csr(*slab_host)  # the rank's slab from the host, like solve(CsrMatrix, b)
-            return sysd.solve(b_host, config=cfgpb)
+            return sysd.solve(b_host, config=cfgpb, engine=eng_pin)
 
         e2e_step()
         barrier()

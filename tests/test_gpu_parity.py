@@ -614,11 +614,12 @@ def test_result_x_owned_across_solves(pb):
     solves (which reuse freed blocks) never overwrite an earlier x."""
     spec, A, b, x0, g = gc.load_case("cd3d16_pbicgsafe", orc.spmv)
     cfg = _cfg(pb, spec)
-    first = pb.solve(A, b, config=cfg)
+    eng = pb.DeviceEngine(pinned_result=True)
+    first = pb.solve(A, b, config=cfg, engine=eng)
     keep = first.x.copy()
-    second = pb.solve(A, 2.0 * b, config=cfg)
+    second = pb.solve(A, 2.0 * b, config=cfg, engine=eng)
     for _ in range(3):  # churn the allocator: freed blocks come back
-        pb.solve(A, 3.0 * b, config=cfg)
+        pb.solve(A, 3.0 * b, config=cfg, engine=eng)
     assert first.x.ctypes.data != second.x.ctypes.data
     assert np.array_equal(first.x, keep)
     assert first.x.flags.writeable and first.x.shape == (A.n_rows,)
