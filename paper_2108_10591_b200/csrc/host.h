@@ -111,7 +111,7 @@ struct pbs_mat {
   long long blk_nnz_max = 0;  // most nonzeros in one 256-row block (chunk sizing)
   Partition part;  // multi-GPU row partition (part.dist == nullptr: single GPU)
   Workspace* ws = nullptr;
-  std::map<const double*, ZmMap> zm_maps;  // z-marching engine: tensor map per input vector
+  std::map<std::pair<const double*, int>, ZmMap> zm_maps;  // z-marching engine: tensor map per input vector, rows per thread
 };
 
 static inline int set_err(pbs_ctx* ctx, int code, const std::string& msg) {
@@ -422,22 +422,24 @@ static inline bool stencil_zm_ok(const pbs_mat* m, long long lo, long long hi) {
   return !(lo % k2 || hi % k2 || S.g0 % k2 || (-S.xlo) % k2 || S.xhi % k2 || hi <= lo);
 }
 
-static inline bool stencil_zm_geom(pbs_ctx* ctx, int sms, const pbs_mat* m, long long lo, long long hi,
-                                   const void* kernel, size_t* smem, int* grid, ZmGeom* G) {
+template <class Epi>
+static bool stencil_zm_geom(pbs_ctx* ctx, int sms, const pbs_mat* m, long long lo, long long hi,
+                            const void* kernel, size_t* smem, int* grid, ZmGeom* G) {
+  using Sh = ZmShape<zm_rpt<Epi>()>;
   if (!stencil_zm_ok(m, lo, hi)) return false;
   const StencilView& S = m->sv;
   const long long k2 = S.k2;
   static int ring_env = env_int("PBS_ZM_RING", 8, 4, kZmMaxRing);
   static int waves_env = env_int("PBS_ZM_WAVES", 8, 1, 64);
   G->tiles_y = (int)((S.k + kZmTY - 1) / kZmTY);
-  G->tiles_x = (int)((S.k + kZmTX - 1) / kZmTX);
+  G->tiles_x = (int)((S.k + Sh::TX - 1) / Sh::TX);
   G->z_lo = (int)(lo / k2);
   G->z_hi = (int)(hi / k2);
   G->zx_lo = (int)(S.xlo / k2);
   G->zx_hi = (int)(S.xhi / k2);
   G->gz0 = S.g0 / k2;
   G->ring = ring_env;
-  *smem = 256 + sizeof(double) * (size_t)kZmStage * G->ring;
+  *smem = 256 + sizeof(double) * (size_t)Sh::Stage * G->ring;
   auto it = ctx->occ.find(kernel);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem) != cudaSuccess)
@@ -466,8 +468,9 @@ typedef CUresult (*PfnTensorMapEncodeTiled)(CUtensorMap*, CUtensorMapDataType, c
                                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                             CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                             CUtensorMapFloatOOBfill);
-static inline const CUtensorMap* stencil_zm_map(pbs_mat* m, const double* x, const ZmGeom& G) {
-  auto it = m->zm_maps.find(x);
+template <int RPT>
+static const CUtensorMap* stencil_zm_map(pbs_mat* m, const double* x, const ZmGeom& G) {
+  auto it = m->zm_maps.find({x, RPT});
   if (it != m->zm_maps.end()) return &it->second.map;
   if (m->zm_maps.size() >= 64) m->zm_maps.clear();  // callers' temporary x buffers
   static PfnTensorMapEncodeTiled encode = nullptr;
@@ -483,7 +486,7 @@ static inline const CUtensorMap* stencil_zm_map(pbs_mat* m, const double* x, con
   const StencilView& S = m->sv;
   const cuuint64_t dims[3] = {(cuuint64_t)S.k, (cuuint64_t)S.k, (cuuint64_t)(G.zx_hi - G.zx_lo)};
   const cuuint64_t strides[2] = {(cuuint64_t)S.k * sizeof(double), (cuuint64_t)S.k2 * sizeof(double)};
-  const cuuint32_t box[3] = {kZmRowW, kZmTY + 2, 1};
+  const cuuint32_t box[3] = {(cuuint32_t)ZmShape<RPT>::RowW, kZmTY + 2, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   ZmMap zm;
   void* base = (void*)(x + (long long)G.zx_lo * S.k2);
@@ -491,7 +494,7 @@ static inline const CUtensorMap* stencil_zm_map(pbs_mat* m, const double* x, con
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return nullptr;
-  return &m->zm_maps.emplace(x, zm).first->second.map;
+  return &m->zm_maps.emplace(std::make_pair(x, RPT), zm).first->second.map;
 }
 
 template <class Epi, int DIM, int NP>
@@ -630,11 +633,11 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
                  cstages, chunk);
     if (L.err) return 0;
   } else if (m->stencil &&
-             stencil_zm_geom(L.ctx, L.sms(), m, lo, hi,
-                             m->sv.npts == 27 ? (const void*)stencil_zm_kernel<Epi, 27>
-                                              : (const void*)stencil_zm_kernel<Epi, 7>,
-                             &zm_smem, &grid, &zm) &&
-             (zm_map = stencil_zm_map(m, x, zm)) != nullptr) {
+             stencil_zm_geom<Epi>(L.ctx, L.sms(), m, lo, hi,
+                                  m->sv.npts == 27 ? (const void*)stencil_zm_kernel<Epi, 27>
+                                                   : (const void*)stencil_zm_kernel<Epi, 7>,
+                                  &zm_smem, &grid, &zm) &&
+             (zm_map = stencil_zm_map<zm_rpt<Epi>()>(m, x, zm)) != nullptr) {
     grid = L.cap_grid(grid);
     StencilView S = m->sv;
     S.row_lo = lo;

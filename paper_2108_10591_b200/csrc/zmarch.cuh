@@ -30,14 +30,21 @@
 namespace pbs {
 
 constexpr int kZmTY = 15, kZmTX = 32;  // 15 rows: with the producer warp a CTA is 16 warps (register file split evenly)
-constexpr int kZmThreads = kZmTY * kZmTX;  // consumers: one thread per tile point
+constexpr int kZmThreads = kZmTY * kZmTX;  // consumers: one thread per tile column position
 constexpr int kZmWarps = kZmThreads / 32;
 constexpr int kZmCTA = kZmThreads + 32;     // + one producer warp
-constexpr int kZmRowW = kZmTX + 4;         // staged doubles per tile row: x in [x0 - 2, x0 + TX + 2)
-constexpr int kZmPlane = (kZmTY + 2) * kZmRowW;  // doubles of one staged plane tile (the TMA box)
-constexpr uint32_t kZmPlaneBytes = kZmPlane * sizeof(double);
-constexpr int kZmStage = (kZmPlane * 8 + 127) / 128 * 128 / 8;  // stage stride in doubles (128-byte aligned)
 constexpr int kZmMaxRing = 16;
+// RPT rows per consumer thread along x (2 for the light epilogues: the
+// neighbours of the pair come from 4 staged values per line instead of 6, and
+// the two row sums are independent chains)
+template <int RPT>
+struct ZmShape {
+  static constexpr int TX = kZmTX * RPT;                   // tile width
+  static constexpr int RowW = TX + 4;                      // staged doubles per tile row: x in [x0-2, x0+TX+2)
+  static constexpr int Plane = (kZmTY + 2) * RowW;         // doubles of one staged plane tile (the TMA box)
+  static constexpr uint32_t PlaneBytes = Plane * sizeof(double);
+  static constexpr int Stage = (Plane * 8 + 127) / 128 * 128 / 8;  // stage stride in doubles (128-byte aligned)
+};
 
 // 3-D tiled TMA load of one plane tile: box (TX+4, TY+2, 1) at (x, y, z) of
 // the tensor map; out-of-range elements arrive as zeros (never read: their
@@ -63,11 +70,22 @@ struct ZmGeom {
 // epilogues without dot accumulators run two 512-thread CTAs per SM (64
 // registers), the rest one
 template <class Epi>
-constexpr int zm_minb() {
+__host__ __device__ constexpr int zm_minb() {
   return (std::is_same<Epi, EpiStore>::value || std::is_same<Epi, EpiResid>::value ||
           std::is_same<Epi, EpiK3n>::value)
              ? 2
              : 1;
+}
+
+// rows per consumer thread (the engine supports 2: a pair's neighbours come
+// from 4 staged values per line instead of 6, two independent row chains).
+// One everywhere: the plain 27-point product is bound by the FP64 pipe (the
+// bitwise row sum is 27 DMUL + 27 DADD per row, ~9e12 DP instructions/s on
+// B200, 340 us for config 4), and two rows per thread measured no faster
+// (573 vs 531 us, the partitioned schedule's K1).
+template <class Epi>
+__host__ __device__ constexpr int zm_rpt() {
+  return 1;
 }
 
 // neighbour p of the 7- and 27-point stencils in ascending flattened offset
@@ -82,14 +100,18 @@ __host__ __device__ constexpr int zm_off(int p, int axis) {
 
 // register cap: the whole register file split between the resident CTAs
 template <class Epi>
-constexpr int zm_maxreg() {
+__host__ __device__ constexpr int zm_maxreg() {
   return zm_minb<Epi>() == 2 ? 64 : 128;
 }
 
 template <class Epi, int NP>
-__global__ void __launch_bounds__(kZmCTA) __maxnreg__(zm_maxreg<Epi>()) stencil_zm_kernel(const __grid_constant__ StencilView S,
-                                                                           const __grid_constant__ CUtensorMap xmap,
-                                                                           Epi epi, ZmGeom G) {
+__global__ void __launch_bounds__(kZmCTA) __maxnreg__(zm_maxreg<Epi>())
+    stencil_zm_kernel(const __grid_constant__ StencilView S, const __grid_constant__ CUtensorMap xmap, Epi epi,
+                      ZmGeom G) {
+  constexpr int RPT = zm_rpt<Epi>();
+  using Sh = ZmShape<RPT>;
+  constexpr int kZmRowW = Sh::RowW, kZmStage = Sh::Stage, TXE = Sh::TX;
+  constexpr uint32_t kZmPlaneBytes = Sh::PlaneBytes;
   __shared__ int go;
   griddep_wait();  // PDL: everything here reads the previous kernel's output
   if (threadIdx.x == 0) {
@@ -127,7 +149,7 @@ __global__ void __launch_bounds__(kZmCTA) __maxnreg__(zm_maxreg<Epi>()) stencil_
       uint32_t ph = 0;
       for (int it = blockIdx.x; it < items; it += gridDim.x) {
         const int tile = it % ntiles, chunk = it / ntiles;
-        const int y0 = (tile / G.tiles_x) * kZmTY, x0 = (tile % G.tiles_x) * kZmTX;
+        const int y0 = (tile / G.tiles_x) * kZmTY, x0 = (tile % G.tiles_x) * TXE;
         const int za = G.z_lo + chunk * G.zchunk, zb = min(G.z_hi, za + G.zchunk);
         for (int zl = za - 1; zl <= zb; ++zl) {
           mbar_wait(&empty[s], ph ^ 1);
@@ -149,25 +171,31 @@ __global__ void __launch_bounds__(kZmCTA) __maxnreg__(zm_maxreg<Epi>()) stencil_
   int s = 0;
   uint32_t ph = 0;
   constexpr unsigned kAll = (1u << NP) - 1u;
-  const int ctr = (ty + 1) * kZmRowW + tx + 2;
+  const int ctr = (ty + 1) * kZmRowW + RPT * tx + 2;
   for (int it = blockIdx.x; it < items; it += gridDim.x) {
     const int tile = it % ntiles, chunk = it / ntiles;
-    const int y0 = (tile / G.tiles_x) * kZmTY, x0 = (tile % G.tiles_x) * kZmTX;
+    const int y0 = (tile / G.tiles_x) * kZmTY, x0 = (tile % G.tiles_x) * TXE;
     const int za = G.z_lo + chunk * G.zchunk, zb = min(G.z_hi, za + G.zchunk);
-    const int y = y0 + ty, xx = x0 + tx;
-    const bool live = y < ki && xx < ki;
-    const long long rowoff = (long long)y * k + xx;
-    // in-grid neighbours as far as y and x decide (z per plane below)
-    unsigned vm_yx = kAll;
-    if (y == 0) vm_yx &= S.nlo[1];
-    if (y == ki - 1) vm_yx &= S.nhi[1];
-    if (xx == 0) vm_yx &= S.nlo[2];
-    if (xx == ki - 1) vm_yx &= S.nhi[2];
-    double nin[Epi::kIn > 0 ? Epi::kIn : 1];
-    if (live) {
+    const int y = y0 + ty, xx = x0 + RPT * tx;  // this thread's rows: x = xx .. xx + RPT - 1
+    bool live[RPT];
+    unsigned vm_yx[RPT];  // in-grid neighbours as far as y and x decide (z per plane below)
 #pragma unroll
-      for (int j = 0; j < Epi::kIn; ++j) nin[j] = __ldg(e.in[j] + (long long)za * k2 + rowoff);
+    for (int r = 0; r < RPT; ++r) {
+      live[r] = y < ki && xx + r < ki;
+      vm_yx[r] = kAll;
+      if (y == 0) vm_yx[r] &= S.nlo[1];
+      if (y == ki - 1) vm_yx[r] &= S.nhi[1];
+      if (xx + r == 0) vm_yx[r] &= S.nlo[2];
+      if (xx + r == ki - 1) vm_yx[r] &= S.nhi[2];
     }
+    const long long rowoff = (long long)y * k + xx;
+    double nin[RPT][Epi::kIn > 0 ? Epi::kIn : 1];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+      if (live[r]) {
+#pragma unroll
+        for (int j = 0; j < Epi::kIn; ++j) nin[r][j] = __ldg(e.in[j] + (long long)za * k2 + rowoff + r);
+      }
     // stages of the planes below / at / above the centre, and their phases
     int s0 = s, s1 = s + 1, s2 = s + 2;
     uint32_t p0 = ph, p1 = ph, p2 = ph;
@@ -176,38 +204,66 @@ __global__ void __launch_bounds__(kZmCTA) __maxnreg__(zm_maxreg<Epi>()) stencil_
     mbar_wait(&full[s0], p0);
     mbar_wait(&full[s1], p1);
     for (int z = za; z < zb; ++z) {
-      double inr[Epi::kIn > 0 ? Epi::kIn : 1];
+      double inr[RPT][Epi::kIn > 0 ? Epi::kIn : 1];
 #pragma unroll
-      for (int j = 0; j < Epi::kIn; ++j) inr[j] = nin[j];
-      if (live && z + 1 < zb) {  // the next plane's epilogue inputs, in flight during this one
+      for (int r = 0; r < RPT; ++r) {
 #pragma unroll
-        for (int j = 0; j < Epi::kIn; ++j) nin[j] = __ldg(e.in[j] + (long long)(z + 1) * k2 + rowoff);
+        for (int j = 0; j < Epi::kIn; ++j) inr[r][j] = nin[r][j];
+        if (live[r] && z + 1 < zb) {  // the next plane's epilogue inputs, in flight during this one
+#pragma unroll
+          for (int j = 0; j < Epi::kIn; ++j) nin[r][j] = __ldg(e.in[j] + (long long)(z + 1) * k2 + rowoff + r);
+        }
       }
       mbar_wait(&full[s2], p2);
-      if (live) {
-        const long long gz = z + G.gz0;
-        unsigned vm = vm_yx;
-        if (gz == 0) vm &= S.nlo[0];
-        if (gz == k - 1) vm &= S.nhi[0];
-        const double* pl0 = ring + (size_t)s0 * kZmStage + ctr;
-        const double* pl1 = ring + (size_t)s1 * kZmStage + ctr;
-        const double* pl2 = ring + (size_t)s2 * kZmStage + ctr;
-        double acc = 0.0;
-        if (vm == kAll) {  // interior row: every neighbour, no predicates
+      const long long gz = z + G.gz0;
+      unsigned vm[RPT];
+      bool interior = true;
 #pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            const int dz = zm_off<NP>(p, 0), o = zm_off<NP>(p, 1) * kZmRowW + zm_off<NP>(p, 2);
-            acc = add(acc, mul(S.coef[p], (dz < 0 ? pl0 : (dz == 0 ? pl1 : pl2))[o]));
-          }
-        } else {
-#pragma unroll
-          for (int p = 0; p < NP; ++p) {
-            const int dz = zm_off<NP>(p, 0), o = zm_off<NP>(p, 1) * kZmRowW + zm_off<NP>(p, 2);
-            if ((vm >> p) & 1u) acc = add(acc, mul(S.coef[p], (dz < 0 ? pl0 : (dz == 0 ? pl1 : pl2))[o]));
-          }
-        }
-        e.row((long long)z * k2 + rowoff, acc, inr);
+      for (int r = 0; r < RPT; ++r) {
+        vm[r] = vm_yx[r];
+        if (gz == 0) vm[r] &= S.nlo[0];
+        if (gz == k - 1) vm[r] &= S.nhi[0];
+        interior = interior && vm[r] == kAll && live[r];
       }
+      const double* pl0 = ring + (size_t)s0 * kZmStage + ctr;
+      const double* pl1 = ring + (size_t)s1 * kZmStage + ctr;
+      const double* pl2 = ring + (size_t)s2 * kZmStage + ctr;
+      double acc[RPT];
+#pragma unroll
+      for (int r = 0; r < RPT; ++r) acc[r] = 0.0;
+      // each row's neighbours in ascending flattened offset; the points come
+      // grouped by (dz, dy) line, and a line's staged values are loaded once
+      // for all the thread's rows
+      double w[RPT + 2];
+      if (interior) {  // no predicates
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const int dz = zm_off<NP>(p, 0), dy = zm_off<NP>(p, 1), dx = zm_off<NP>(p, 2);
+          if (p == 0 || dz != zm_off<NP>(p - 1, 0) || dy != zm_off<NP>(p - 1, 1)) {
+            const double* ln = (dz < 0 ? pl0 : (dz == 0 ? pl1 : pl2)) + dy * kZmRowW;
+#pragma unroll
+            for (int q = 0; q < RPT + 2; ++q) w[q] = ln[q - 1];
+          }
+#pragma unroll
+          for (int r = 0; r < RPT; ++r) acc[r] = add(acc[r], mul(S.coef[p], w[dx + 1 + r]));
+        }
+      } else {
+#pragma unroll
+        for (int p = 0; p < NP; ++p) {
+          const int dz = zm_off<NP>(p, 0), dy = zm_off<NP>(p, 1), dx = zm_off<NP>(p, 2);
+          if (p == 0 || dz != zm_off<NP>(p - 1, 0) || dy != zm_off<NP>(p - 1, 1)) {
+            const double* ln = (dz < 0 ? pl0 : (dz == 0 ? pl1 : pl2)) + dy * kZmRowW;
+#pragma unroll
+            for (int q = 0; q < RPT + 2; ++q) w[q] = ln[q - 1];
+          }
+#pragma unroll
+          for (int r = 0; r < RPT; ++r)
+            if ((vm[r] >> p) & 1u) acc[r] = add(acc[r], mul(S.coef[p], w[dx + 1 + r]));
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < RPT; ++r)
+        if (live[r]) e.row((long long)z * k2 + rowoff + r, acc[r], inr[r]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s0]);  // this warp is done with the plane below
       s0 = s1, p0 = p1;
