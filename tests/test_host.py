@@ -232,3 +232,32 @@ def test_bench_reference_arm_contract():
     assert d["cpu_baseline"]["kind"] in ("port", "reference") and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
     assert d["config"]["workload"].startswith("BASELINE config 2")
+
+
+def test_sass_census_blackwell_async_copies():
+    """The hot engines are Blackwell-native in SASS, not just built for sm_100a:
+    every staged CSR / stencil SpMV instantiation issues 1-D bulk async copies
+    (UBLKCP) and waits on mbarrier phases (SYNCS.PHASECHK), and the z-marching
+    engine issues 3-D TMA tensor loads (UTMALDG)."""
+    import subprocess
+
+    obj = os.path.join(ROOT, "build", "pbsafe", "solve.cu.o")  # the single-GPU schedules' TU
+    target = obj if os.path.exists(obj) else build.build()
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", target], capture_output=True, text=True,
+                          timeout=600).stdout
+    funcs = {}
+    for chunk in re.split(r"\n\s*Function : ", sass)[1:]:
+        name, body = chunk.split("\n", 1)
+        funcs[name.strip()] = body
+    pipe = {n: b for n, b in funcs.items() if "csr_pipe_kernel" in n or "stencil_pipe_kernel" in n}
+    zm = {n: b for n, b in funcs.items() if "stencil_zm_kernel" in n}
+    assert len(pipe) >= 20 and len(zm) >= 8, (len(pipe), len(zm))
+    for n, b in pipe.items():
+        assert "UBLKCP" in b and "SYNCS.PHASECHK" in b, n
+    for n, b in zm.items():
+        assert "UTMALDG" in b and "SYNCS.PHASECHK" in b, n
+    # the two kernels of the config-2 iteration and the config-4 matrix-free K12
+    hot = ("csr_pipe_kernelINS_7EpiK12TILb1EEE", "csr_pipe_kernelINS_6EpiK3TILj77EEE",
+           "stencil_zm_kernelINS_7EpiK12TILb1EEELi27E")
+    for h in hot:
+        assert any(h in n for n in funcs), h
