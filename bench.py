@@ -655,6 +655,8 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=600)  # ~10 s on a 16-core host
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-comparators", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="resolve the launch (ranks, workload, schedule) and print it; no GPU work")
     args = ap.parse_args()
     os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")  # compute, halo and comm streams on separate queues
     rank, world, _ = dist_env()
@@ -662,6 +664,19 @@ def main():
         return self_launch(args)
     if "WORLD_SIZE" in os.environ and world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        if world > 1:  # every rank reaches the rendezvous, like the real run
+            import torch.distributed as dist
+
+            dist.init_process_group("gloo")
+            dist.barrier()
+            dist.destroy_process_group()
+        if rank == 0:
+            emit({"dry_run": True, "impl": args.impl, "n_gpus": world, "config": args.config,
+                  "operator": args.operator,
+                  "schedule": ("partitioned" if world > 1 or args.loopback > 1 or args.partitioned else "fused"),
+                  "loopback": args.loopback})
+        return 0
     if args.impl == "reference":
         return run_reference(args)
     if world > 1 or args.loopback > 1 or args.partitioned:

@@ -1,0 +1,81 @@
+"""Full-size parity of the stability and scaling configs against recorded
+oracle runs.
+
+tests/golden/fullsize_counts.json was written by tools/full_size_oracle.py:
+the oracle (the C restatement of the reference, bitwise equal to it on the
+fixtures) run once on config 5 at full size (256^3, Péclet 100,
+p-BiCGSafe-rr m = 100 to 1e-12) and on config 4's operator at k = 128
+(27-point, 2.1M rows) to 1e-10, under the reference's default reduction order
+(W = 1), other PartitionPlan orders and near-exact dots.  These sizes take
+minutes on the host, so the runs are recorded, not repeated here.  The device
+solve must converge like them: iteration count inside their ensemble +-2%,
+the first records on the near-exact run, and a true residual as good.
+"""
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "fullsize_counts.json")
+
+
+def _case(name):
+    if not os.path.exists(GOLDEN):
+        pytest.skip("no recorded full-size oracle runs")
+    data = json.load(open(GOLDEN))
+    if name not in data:
+        pytest.skip(f"{name} not recorded")
+    return data[name]
+
+
+def _solve(spec, operator, method, tol, max_iters):
+    import torch
+
+    import paper_2108_10591_b200 as pb
+    from paper_2108_10591_b200.operators import DeviceMatrix
+
+    dm = DeviceMatrix.from_stencil(spec)
+    if operator == "csr":
+        st, dm = dm, dm.to_csr()
+        st.free()
+    ones = torch.ones(spec.n, dtype=torch.float64, device="cuda")
+    bd = torch.empty_like(ones)
+    dm.spmv_dev(ones.data_ptr(), bd.data_ptr())
+    b = bd.cpu().numpy()
+    out = pb.solve(dm, b, method=method, config=pb.SolverConfig(tol=tol, max_iters=max_iters))
+    # true residual on the device: || b - A x || / r0_norm
+    xd = torch.from_numpy(np.ascontiguousarray(out.x)).cuda()
+    ax = torch.empty_like(xd)
+    dm.spmv_dev(xd.data_ptr(), ax.data_ptr())
+    true = float(torch.linalg.norm(bd - ax).item()) / out.r0_norm
+    dm.free()
+    return out, true
+
+
+@pytest.mark.parametrize("name,cfg,k,operator", [("c5_full_rr", "c5", None, "stencil"),
+                                                  ("c5_full_rr", "c5", None, "csr"),
+                                                  ("c4_k128", "c4", 128, "csr"),
+                                                  ("c4_k128", "c4", 128, "stencil")])
+def test_full_size_count_in_oracle_ensemble(name, cfg, k, operator):
+    from paper_2108_10591_b200 import problems
+
+    rec = _case(name)
+    spec = problems.config_stencil(cfg, k=k)
+    assert spec.n == rec["n"]
+    out, true = _solve(spec, operator, rec["method"], rec["tol"], rec["max_iters"])
+    runs = rec["runs"]
+    assert all(r["status"] == "converged" for r in runs.values()), runs
+    assert out.converged, out.status
+    counts = [r["iterations"] for r in runs.values()]
+    lo, hi = min(counts), max(counts)
+    assert math.floor(0.98 * lo) - 1 <= out.iterations <= math.ceil(1.02 * hi) + 1, (out.iterations, counts)
+    ne = runs["-1"]
+    m = min(len(ne["rel_first"]), len(out.history))
+    np.testing.assert_allclose([r.rel_res_recur for r in out.history[:m]], ne["rel_first"][:m], rtol=1e-9)
+    ref_true = max(r["true_rel"] for r in runs.values())
+    assert true <= max(100 * rec["tol"], 10 * ref_true), (true, ref_true)

@@ -261,3 +261,31 @@ def test_sass_census_blackwell_async_copies():
            "stencil_zm_kernelINS_7EpiK12TILb1EEELi27E")
     for h in hot:
         assert any(h in n for n in funcs), h
+
+
+def test_bench_gpus_n_self_launches_n_ranks():
+    """bench.py --gpus N without torchrun's environment re-launches itself
+    under torch.distributed.run with N processes; every rank reaches the
+    rendezvous and rank 0's line reports n_gpus = N (dry run: no GPU work)."""
+    import json
+    import subprocess
+    import sys
+
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--config", "c4", "--dry-run"], cwd=ROOT,
+                       capture_output=True, text=True, timeout=300,
+                       env={k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")})
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["schedule"] == "partitioned" and d["config"] == "c4"
+
+
+def test_bench_rejects_world_size_mismatch():
+    import subprocess
+    import sys
+
+    env = {**os.environ, "WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"}
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "4", "--dry-run"], cwd=ROOT, capture_output=True,
+                       text=True, timeout=120, env=env)
+    assert p.returncode != 0 and "WORLD_SIZE=2" in (p.stderr + p.stdout)
