@@ -100,6 +100,10 @@ struct SolverState {
   int remote_err;
   int err_tag;
   long long err_row;
+  // multi-GPU: the finalize of check j publishes its coefficients by setting
+  // this to j + 1 (release, after the state is stored); K1's opportunistic
+  // epilogue reads it (acquire)
+  unsigned long long coef_epoch;
   unsigned int done_ctas;  // last-CTA ticket of the fused finalize (reset by the last CTA)
   // history (device arrays, max_iters+1 slots)
   double* hist_rel;

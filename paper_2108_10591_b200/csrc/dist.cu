@@ -224,6 +224,51 @@ static __global__ void __launch_bounds__(kThreads) k2_dots_kernel(VecPtrs V, lon
   block_reduce9<kThreads, false, kDotsK12>(d.acc, parts + blockIdx.x);
 }
 
+// K2 for the row blocks K1 left (EpiK1opp: streamed before the coefficients
+// of check j were published): block 1 of the iteration and the b e f h r
+// partials of check j+1 over those rows only.  Always launched: its gate
+// closes the spine once a check has stopped the solve.
+static __global__ void __launch_bounds__(kThreads) k2_deferred_kernel(VecPtrs V, long long n, SolverState* st,
+                                                                      const int* rows, const unsigned* count,
+                                                                      double* parts) {
+  if (!gate_after_spine(st)) return;
+  const double alpha = st->alpha, beta = st->beta, zeta = st->zeta, eta = st->eta;
+  double *__restrict__ x = V.v[VX], *__restrict__ r = V.v[VR], *__restrict__ p = V.v[VP],
+         *__restrict__ u = V.v[VU], *__restrict__ t = V.v[VT], *__restrict__ w = V.v[VW],
+         *__restrict__ y = V.v[VY], *__restrict__ z = V.v[VZ];
+  const double *__restrict__ s = V.v[VS], *__restrict__ as = V.v[VAS], *__restrict__ l = V.v[VL],
+               *__restrict__ g = V.v[VG], *__restrict__ r0s = V.v[VR0S];
+  DotsT<kDotsK12> d;
+  d.zero();
+  const unsigned nb = *count;
+  for (unsigned b = blockIdx.x; b < nb; b += gridDim.x) {
+    const long long i = (long long)rows[b] + threadIdx.x;
+    if (i >= n) continue;
+    const double rv = r[i], pv = p[i], uv = u[i], sv = s[i], tv = t[i], yv = y[i];
+    const double asv = __ldcs(as + i), lv = l[i], gv = g[i], wv = w[i], zv = z[i], xv = x[i];
+    const double pn = asd(rv, beta, pv, uv);
+    const double o = lc2(1.0, sv, beta, tv);
+    const double un = lcn(zeta, o, eta, yv, beta, uv);
+    const double q = lc2(1.0, asv, beta, lv);
+    const double wn = lcn(zeta, q, eta, gv, beta, wv);
+    const double tn = lc2(1.0, o, -1.0, wn);
+    const double zn = lc3(zeta, rv, eta, zv, -alpha, un);
+    const double yn = lc3(zeta, sv, eta, yv, -alpha, wn);
+    const double xn = lc3(1.0, xv, alpha, pn, 1.0, zn);
+    const double rn = lc3(1.0, rv, -alpha, o, -1.0, yn);
+    p[i] = pn;
+    u[i] = un;
+    w[i] = wn;
+    t[i] = tn;
+    z[i] = zn;
+    y[i] = yn;
+    x[i] = xn;
+    r[i] = rn;
+    d.add_row(0.0, yn, rn, __ldcs(r0s + i), tn);
+  }
+  block_reduce9<kThreads, false, kDotsK12>(d.acc, parts + blockIdx.x);
+}
+
 // Where a publish stores this partition's record: one slot and one flag per
 // partition of the group (peer mappings; its own mailbox included).
 struct PubTargets {
@@ -335,6 +380,10 @@ static __global__ void __launch_bounds__(288) dist_finalize_kernel(SolverState* 
     check_and_publish<288, false>(st, &ss, dots, replaced);
   }
   if (threadIdx.x != 0) return;
+  // the coefficients of this check are in the state: let K1's opportunistic
+  // epilogue use them
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(&st->coef_epoch), "l"((unsigned long long)ss.iter)
+               : "memory");
   if (mirror) {
     mirror->stop_check = ss.stop_check;
     mirror->run_all = ss.run_all;
@@ -385,6 +434,13 @@ struct Part {
   std::vector<int> send_peers, recv_peers;  // distinct peers
   int np = 0, np2 = 0;                      // records of the next publish
   int seq = 0;                              // SpMV launch sequence (identical on every partition)
+  int* defer_rows = nullptr;                // EpiK1opp: blocks left to k2_deferred_kernel, and their count
+  unsigned* defer_count = nullptr;
+  // records of the dots b e f h r, by iteration parity: K1 of iteration j+1
+  // (EpiK1opp) writes its records while the publish of check j+1 still
+  // reads those of iteration j
+  double* p12buf[2] = {nullptr, nullptr};
+  double* p12 = nullptr;
   unsigned long long* stamps = nullptr;     // device [cap][kStampWords]
   long long stamps_cap = 0;
   Part() = default;
@@ -525,7 +581,7 @@ static void publish(Part& P, long long i) {
   cudaStreamWaitEvent(D->comm, D->ev_k3, 0);
   const unsigned mask2 = P.np2 ? kDotsK12 : 0u;
   if (D->transport == PBS_TRANSPORT_NCCL) {
-    pack_record_kernel<<<1, 288, 0, D->comm>>>(P.ws->partials, P.np, P.ws->partials12, P.np2, mask2, P.ws->st,
+    pack_record_kernel<<<1, 288, 0, D->comm>>>(P.ws->partials, P.np, P.p12, P.np2, mask2, P.ws->st,
                                                P.m->part.row_lo, D->sendbuf, stamp_at(P, i, kStPub));
   } else {
     PubTargets T;
@@ -534,7 +590,7 @@ static void publish(Part& P, long long i) {
       T.slot[q] = &D->peers[q].mbox->slots[D->parity][D->rank][0];
       T.flag[q] = &D->peers[q].mbox->red[D->parity][D->rank];
     }
-    publish_kernel<<<1, 288, 0, D->comm>>>(P.ws->partials, P.np, P.ws->partials12, P.np2, mask2, P.ws->st,
+    publish_kernel<<<1, 288, 0, D->comm>>>(P.ws->partials, P.np, P.p12, P.np2, mask2, P.ws->st,
                                            P.m->part.row_lo, T, stamp_at(P, i, kStPub));
   }
   P.L.done(KD);
@@ -595,13 +651,43 @@ static void run_steps(std::vector<Part>& parts, const std::vector<Step>& steps) 
     }
 }
 
-static void k1_step(Part& P, long long j) {
+// K1 fuses block 1 opportunistically (EpiK1opp) on large CSR slabs: the
+// reduction (~25 us) then covers a small share of K1 and the K2 pass mostly
+// disappears (config 4 partitioned, N = 1: 98.6 -> 102.7 it/s).  On small
+// slabs a third of the blocks stream before the coefficients exist and the
+// fused epilogue's register pressure costs more than the K2 pass it saves
+// (config 2, N = 1: 5434 -> 4870 it/s), so they keep the plain product.
+// Stencil operators keep it too.  PBS_K1_OPP=0|1 forces either.
+static bool k1_opp(const Part& P) {
+  static int forced = env_int("PBS_K1_OPP", -1, -1, 1);
+  if (P.m->stencil || csr_engine_tpr() || forced == 0) return false;
+  return forced == 1 || P.m->nnz >= (64LL << 20);
+}
+
+static void k1_step(Part& P, long long j, bool fuse) {
   // room for the comm stream's 1-CTA publish / finalize beside K1: one SM
   // for the persistent staged engines, one CTA slot per SM for the rest
   P.L.sm_limit = eff_sms(P) - 1;
   if (P.L.sm_limit < 1) P.L.sm_limit = 1;
   P.L.leave_room = true;
-  halo_spmv(P, VS, KK1, [&](int) { return epi_store_st(P.ws, VAS, PBS_TAG_AS, 1, stamp_at(P, j, kStK1)); });
+  P.p12 = P.p12buf[j & 1];
+  if (fuse && k1_opp(P)) {
+    if (cudaMemsetAsync(P.defer_count, 0, sizeof(unsigned), P.D->s) != cudaSuccess)
+      P.L.err = set_err(P.D->ctx, PBS_ERR_CUDA, "defer list reset failed");
+    Mode md;
+    P.np2 = halo_spmv(P, VS, KK1, [&](int off) {
+      EpiK1opp e = epi_k12_fill<EpiK1opp>(P.ws, md);
+      e.parts = P.p12 + off;
+      e.stamp = stamp_at(P, j, kStK1);
+      e.want = (unsigned long long)(j + 1);  // check j's coefficients
+      e.defer_rows = P.defer_rows;
+      e.defer_count = P.defer_count;
+      e.tag = PBS_TAG_AS;
+      return e;
+    });
+  } else {
+    halo_spmv(P, VS, KK1, [&](int) { return epi_store_st(P.ws, VAS, PBS_TAG_AS, 1, stamp_at(P, j, kStK1)); });
+  }
   P.L.sm_limit = eff_sms(P);
   P.L.leave_room = false;
 }
@@ -624,14 +710,27 @@ static void setup_steps(std::vector<Step>& st, bool pipelined) {
 // one p-BiCGSafe(-rr) iteration j (solvers.py:639-734); its batch is check j+1
 static void iter_steps(std::vector<Step>& st, long long j, bool replace) {
   st.push_back([](Part& P) { push(P, VS); });
-  st.push_back([j](Part& P) { k1_step(P, j); });
+  st.push_back([j, replace](Part& P) { k1_step(P, j, !replace); });
   if (!replace) {
     st.push_back([](Part& P) {
       cudaStreamWaitEvent(P.D->s, P.D->ev_coef, 0);  // coefficients of check j
       Launcher& L = P.L;
       const long long nblk = (P.ws->n + kThreads - 1) / kThreads;
-      P.np2 = L.cap_grid(grid_for(L.ctx, (const void*)k2_dots_kernel, nblk, 8, L.sms()));
-      k2_dots_kernel<<<P.np2, kThreads, 0, L.s>>>(P.ws->V, P.ws->n, P.ws->st, P.ws->partials12);
+      if (k1_opp(P)) {  // only the blocks K1 left
+        if (P.np2 >= kMaxParts) {
+          L.err = set_err(P.D->ctx, PBS_ERR_INVALID, "K1 records fill the partial-record buffer");
+          return;
+        }
+        L.grid_cap = kMaxParts - P.np2;
+        const int g = L.cap_grid(grid_for(L.ctx, (const void*)k2_deferred_kernel, nblk, 2, L.sms()));
+        L.grid_cap = 0;
+        k2_deferred_kernel<<<g, kThreads, 0, L.s>>>(P.ws->V, P.ws->n, P.ws->st, P.defer_rows, P.defer_count,
+                                                    P.p12 + P.np2);
+        P.np2 += g;
+      } else {
+        P.np2 = L.cap_grid(grid_for(L.ctx, (const void*)k2_dots_kernel, nblk, 8, L.sms()));
+        k2_dots_kernel<<<P.np2, kThreads, 0, L.s>>>(P.ws->V, P.ws->n, P.ws->st, P.p12);
+      }
       L.done(KK2);
     });
     st.push_back([](Part& P) { push(P, VW); });
@@ -774,6 +873,13 @@ static int init_part(Part& P, pbs_mat* m, const pbs_config* cfg, int method) {
     CK(pool_alloc(ctx, &P.stamps, sizeof(unsigned long long) * kStampWords * P.stamps_cap));
     CK(cudaMemsetAsync(P.stamps, 0, sizeof(unsigned long long) * kStampWords * P.stamps_cap, s));
   }
+  const long long nblk = (ws->n + kPipeRows - 1) / kPipeRows;
+  CK(pool_alloc(ctx, &P.defer_rows, sizeof(int) * (nblk > 0 ? nblk : 1)));
+  CK(pool_alloc(ctx, &P.defer_count, sizeof(unsigned)));
+  CK(cudaMemsetAsync(P.defer_count, 0, sizeof(unsigned), s));
+  P.p12buf[0] = ws->partials12;
+  CK(pool_alloc(ctx, &P.p12buf[1], sizeof(double) * kMaxParts * kPartStride));
+  P.p12 = P.p12buf[0];
   // the comm / halo streams start after the state is in place
   CK(cudaEventRecord(D->ev_coef, s));
   CK(cudaStreamWaitEvent(D->comm, D->ev_coef, 0));
@@ -885,8 +991,12 @@ static int group_solve(std::vector<pbs_mat*>& mats, int method, const pbs_config
     }
     if (cfg->stamps_count) *cfg->stamps_count = cap;
   }
-  for (Part& P : parts)
+  for (Part& P : parts) {
     if (P.stamps) pool_free(ctx, P.stamps);
+    pool_free(ctx, P.defer_rows);
+    pool_free(ctx, P.defer_count);
+    pool_free(ctx, P.p12buf[1]);
+  }
   // results: every partition's state is identical; a non-finite SpMV
   // output anywhere reached every partition through the next check's records
   // (NonFiniteVectorError with the group's first failure: tag, global row)

@@ -120,6 +120,20 @@ struct StencilView {
 };
 
 // ---------------------------------------------------------------- epilogues
+//
+// Opportunistic epilogues (Epi::kOpp, csr_pipe_kernel only): the producer
+// decides per row block whether the epilogue can run now (Epi::ready(): the
+// coefficients it needs exist yet), stages the block's epilogue inputs only
+// then, and tells the consumers through the block header; the consumers run
+// the full epilogue for such blocks and hand the others to Epi::defer().
+template <class Epi, class = void>
+struct EpiOpp {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiOpp<Epi, decltype((void)Epi::kOpp)> {
+  static constexpr bool value = Epi::kOpp;
+};
 
 template <unsigned M>
 struct DotsT {
@@ -324,6 +338,100 @@ struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-loca
 };
 using EpiK12 = EpiK12T<false>;
 using EpiK12d = EpiK12T<true>;
+
+// K1 of the multi-GPU schedule (As = A s, overlapping the reduction of check
+// j) with block 1 of the iteration fused in opportunistically: the row blocks
+// whose producer finds the coefficients of check j already published (the
+// finalize has advanced coef_epoch to want) run EpiK12d's epilogue — p u w t
+// z y x r and the dots b e f h r of check j+1 — in the same pass; the blocks
+// streamed before that only store As and are listed for k2_deferred_kernel.
+// On a large slab the reduction (~30 us) covers a few percent of K1, so the
+// partitioned iteration streams like the fused single-GPU one.
+struct EpiK1opp {
+  static constexpr bool kOpp = true;
+  static constexpr int kIn = 12;
+  static constexpr int kInStaged = 11;  // r0s is loaded by the consumer thread
+  static constexpr int kWcBatch = PBS_WCB_K12D;
+  static constexpr int kMinBlocks = PBS_K12D_MINB;
+  static constexpr bool kStencilPipe = false;
+  static constexpr int kGatherBatch = 4;
+  double* as;
+  double *p, *u, *w, *t, *z, *y, *x, *r;
+  double *o_out, *q_out;  // unused (epi_k12_fill sets them)
+  double* parts;  // records of this launch's b e f h r partials (kDotsK12)
+  SolverState* st;
+  const double* in[kIn];  // r p u s t y l g w z x r0s
+  unsigned long long* stamp;
+  unsigned long long want;  // the coefficients exist once st->coef_epoch >= want
+  int* defer_rows;          // first rows of the blocks left to k2_deferred_kernel
+  unsigned* defer_count;
+  int tag;
+  int have, full;
+  double alpha, beta, zeta, eta;
+  DotsT<kDotsK12> d;
+  __device__ bool active() const { return gate_spine(st); }
+  __device__ void on_skip() const {}
+  __device__ void init() {
+    if (stamp && threadIdx.x == 0) atomicMax(stamp, ~gtime());
+    d.zero();
+    have = 0;
+    full = 0;
+  }
+  __device__ bool ready() const {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(&st->coef_epoch) : "memory");
+    return v >= want;
+  }
+  __device__ void row_opp(long long i, double asv, const double* v, bool fused) {
+    as[i] = asv;
+    if (!isfinite(asv)) report_nonfinite(st, tag, i);
+    if (!fused) return;
+    if (!have) {  // the producer saw the coefficients published: read them once
+      have = 1;
+      full = !dev_err(st) && __ldcg(&st->run_all);
+      alpha = __ldcg(&st->alpha);
+      beta = __ldcg(&st->beta);
+      zeta = __ldcg(&st->zeta);
+      eta = __ldcg(&st->eta);
+    }
+    if (!full) return;
+    const double rv = v[0], pv = v[1], uv = v[2], sv = v[3], tv = v[4], yv = v[5];
+    const double lv = v[6], gv = v[7], wv = v[8], zv = v[9], xv = v[10];
+    const double pn = asd(rv, beta, pv, uv);              // p = r + beta*(p - u)
+    const double o = lc2(1.0, sv, beta, tv);              // o = s + beta*t
+    const double un = lcn(zeta, o, eta, yv, beta, uv);    // u = zeta*o + eta*(y + beta*u)
+    const double q = lc2(1.0, asv, beta, lv);             // q = As + beta*l
+    const double wn = lcn(zeta, q, eta, gv, beta, wv);    // w = zeta*q + eta*(g + beta*w)
+    const double tn = lc2(1.0, o, -1.0, wn);              // t = o - w
+    const double zn = lc3(zeta, rv, eta, zv, -alpha, un); // z = zeta*r + eta*z - alpha*u
+    const double yn = lc3(zeta, sv, eta, yv, -alpha, wn); // y = zeta*s + eta*y - alpha*w
+    const double xn = lc3(1.0, xv, alpha, pn, 1.0, zn);   // x = x + alpha*p + z
+    const double rn = lc3(1.0, rv, -alpha, o, -1.0, yn);  // r = r - alpha*o - y
+    p[i] = pn;
+    u[i] = un;
+    w[i] = wn;
+    t[i] = tn;
+    z[i] = zn;
+    y[i] = yn;
+    x[i] = xn;
+    r[i] = rn;
+    d.add_row(0.0, yn, rn, v[kIn - 1], tn);  // next check's b e f h r
+  }
+  // engines without the producer's per-block decision defer every row
+  __device__ void row(long long i, double asv, const double* v) { row_opp(i, asv, v, false); }
+  __device__ void defer(long long r0) {
+    const unsigned k = atomicAdd(defer_count, 1u);
+    defer_rows[k] = (int)r0;
+  }
+  template <int NT, bool NAMED>
+  __device__ void finish() {
+    if (stamp) {
+      block_bar<NT, NAMED>();
+      if (threadIdx.x == 0) atomicMax(stamp + 1, gtime());
+    }
+    block_reduce9<NT, NAMED, kDotsK12>(d.acc, parts + blockIdx.x);
+  }
+};
 
 // block 2 of the pipelined iteration with the dot partials in M of the next
 // check's batch: all 9 (kAllDots), the 4 that need the new s (kDotsK3; K12
@@ -756,6 +864,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
       return false;
     };
     long long xhi = 0;  // band mode: x staged up to here (exclusive)
+    bool opp_ready = false;
     if (nblk <= first_blk && !gate()) return;
     for (long long blk = first_blk, q = 0; blk < nblk; blk += bstep, ++q) {
       const int slot = (int)(q & 31);
@@ -817,10 +926,17 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
         issued = (int)cfirst;
         if (!gate()) return;
       }
+      // an opportunistic epilogue runs (and its inputs are staged) only for
+      // blocks whose coefficients already exist (see EpiOpp)
+      bool fuse_in = true;
+      if constexpr (EpiOpp<Epi>::value) {  // polled until seen once (it never goes back)
+        if (!opp_ready) opp_ready = __shfl_sync(0xffffffffu, lane == 0 ? epi.ready() : false, 0);
+        fuse_in = opp_ready;
+      }
       // x windows of this block (every lane computes them; lane 1+c copies window c)
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = brp + (stage_in ? Epi::kInStaged * bin : 0u);
+      uint32_t total = brp + (stage_in && fuse_in ? Epi::kInStaged * bin : 0u);
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0x7fffffff;
@@ -873,6 +989,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
         bh->nr = nr;
         bh->dr = dr;
         bh->nch = (int)nch;
+        bh->pad = fuse_in ? 1 : 0;
 #pragma unroll
         for (int c = 0; c < kMaxWin; ++c) bh->ws[c] = wlo[c];
         mbar_arrive_expect_tx(&bfull[bs], total);
@@ -895,7 +1012,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
             bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
           soff += cc < W.nwin ? W.cap[cc] : 0;
         }
-      } else if (stage_in && lane >= 8 && lane < 8 + Epi::kInStaged) {
+      } else if (stage_in && fuse_in && lane >= 8 && lane < 8 + Epi::kInStaged) {
         const int e = lane - 8;
         bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
       }
@@ -927,6 +1044,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
     const BlockHdr* bhp = reinterpret_cast<const BlockHdr*>(bst);
     const int nr = bhp->nr, dr = bhp->dr;
     const long long r0 = bhp->r0;
+    const bool fused = !EpiOpp<Epi>::value || bhp->pad;  // the producer's decision for this block
     long long my_s = 0, my_e = 0;
     double inr[Epi::kIn > 0 ? Epi::kIn : 1];
     if (t < nr) {
@@ -934,9 +1052,11 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
       my_s = rps[t + dr];
       my_e = rps[t + dr + 1];
       // inputs the producer does not stage: in flight during the row's products
+      if (fused) {
 #pragma unroll
-      for (int k = 0; k < Epi::kIn; ++k)
-        if (k >= Epi::kInStaged || !stage_in) inr[k] = __ldg(e.in[k] + r0 + t);
+        for (int k = 0; k < Epi::kIn; ++k)
+          if (k >= Epi::kInStaged || !stage_in) inr[k] = __ldg(e.in[k] + r0 + t);
+      }
     }
     // staged x windows (or the band buffer), addressed by the window-local
     // column stream
@@ -994,11 +1114,16 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) csr_pipe_kernel(CsrView A,
     }
     if (t < nr) {
       const double* ein = reinterpret_cast<const double*>(bst + BL.ein);
-      if (stage_in) {
+      if (stage_in && fused) {
 #pragma unroll
         for (int k = 0; k < Epi::kInStaged; ++k) inr[k] = ein[k * (kPipeRows + 2) + t + dr];
       }
-      e.row(r0 + t, acc, inr);
+      if constexpr (EpiOpp<Epi>::value) {
+        e.row_opp(r0 + t, acc, inr, fused);
+        if (!fused && t == 0) e.defer(r0);
+      } else {
+        e.row(r0 + t, acc, inr);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&bempty[bs]);

@@ -46,8 +46,11 @@ def _system(name, nparts, operator):
     from paper_2108_10591_b200 import problems
     from paper_2108_10591_b200.distributed import LoopbackSystem
 
-    if name == "rand":
-        rp, ci, v, _ = problems.random_banded_csr(30000, seed=5, half_window=2000)
+    if name in ("rand", "randwide"):
+        # randwide: the band spans several slabs, so a halo comes from up to
+        # three peers on each side (multi-segment halo plans)
+        n0, w = (30000, 2000) if name == "rand" else (6000, 2000)
+        rp, ci, v, _ = problems.random_banded_csr(n0, seed=5, half_window=w)
         n = len(rp) - 1
         return LoopbackSystem(nparts, rp, ci, v, n), rp, ci, v
     spec = _spec(name)
@@ -59,10 +62,10 @@ def _system(name, nparts, operator):
     return sysd, rp, ci, v
 
 
-@pytest.mark.parametrize("nparts", [2, 3, 4])
+@pytest.mark.parametrize("nparts", [2, 3, 4, 8])
 @pytest.mark.parametrize("name,operator", [("cd3d32", "host"), ("cd3d32", "csr"), ("cd3d32", "stencil"),
                                            ("cd27_20", "csr"), ("cd27_20", "stencil"), ("cd2d40", "stencil"),
-                                           ("rand", "host")])
+                                           ("rand", "host"), ("randwide", "host")])
 def test_loopback_spmv_bitwise(name, operator, nparts):
     sysd, rp, ci, v = _system(name, nparts, operator)
     try:
@@ -88,6 +91,21 @@ def _near_exact(rp, ci, v, b, method, tol, max_iters, rr_epoch=100):
     ("rand", "host", "pbicgsafe", 1e-10, 100),
 ])
 def test_loopback_solve_matches_oracle(name, operator, method, tol, rr_epoch, nparts):
+    _loopback_solve_case(name, operator, method, tol, rr_epoch, nparts)
+
+
+@pytest.mark.parametrize("name,operator,method,tol,rr_epoch", [
+    ("randwide", "host", "pbicgsafe-rr", 1e-10, 20),
+    ("cd27_20", "csr", "pbicgsafe", 1e-10, 100),
+    ("cd3d32", "stencil", "ssbicgsafe2", 1e-10, 100),
+])
+def test_loopback_solve_matches_oracle_8_partitions(name, operator, method, tol, rr_epoch):
+    """8 partitions (the north star's GPU count) on one device, including a
+    band wide enough that every halo spans three peers per side."""
+    _loopback_solve_case(name, operator, method, tol, rr_epoch, 8)
+
+
+def _loopback_solve_case(name, operator, method, tol, rr_epoch, nparts):
     import paper_2108_10591_b200 as pb
 
     sysd, rp, ci, v = _system(name, nparts, operator)
@@ -286,4 +304,47 @@ print("ok")
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=300,
                        env={**os.environ, "PBS_ZM7": "1", "PYTHONPATH": root})
+    assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-3000:]
+
+
+def test_opportunistic_k1_matches_oracle_and_is_race_free():
+    """K1 with block 1 fused opportunistically (EpiK1opp; on by default for
+    slabs of >= 64M nonzeros, forced here with PBS_K1_OPP=1 in a subprocess):
+    solves on 2 and 4 partitions follow the oracle's near-exact run, including
+    a replacement run, and 40 repeated solves give bitwise the same history
+    (a record-buffer race once showed up here as a different count in ~5% of
+    solves)."""
+    import os
+    import subprocess
+    import sys
+
+    code = r'''
+import numpy as np
+from oracle import oracle as orc
+import paper_2108_10591_b200 as pb
+from paper_2108_10591_b200 import problems
+from paper_2108_10591_b200.distributed import LoopbackSystem
+spec = problems.convdiff_stencil(3, 32, (1.0, 0.5, 0.25))
+rp, ci, v = problems.stencil_csr(spec)
+b = orc.spmv(rp, ci, v, np.ones(spec.n))
+for method, m in (("pbicgsafe", 100), ("pbicgsafe-rr", 20)):
+    cfg = pb.SolverConfig(tol=1e-10, max_iters=2000, rr_epoch=m)
+    ne = orc.solve(rp, ci, v, b, method=method, tol=1e-10, max_iters=2000, rr_epoch=m, workers=-1)
+    for nparts in (2, 4):
+        g = LoopbackSystem(nparts, spec=spec, operator="csr")
+        try:
+            hists = set()
+            for rep in range(20 if method == "pbicgsafe" else 3):
+                out = g.solve(b, method=method, config=cfg)
+                hists.add(tuple(r.rel_res_recur for r in out.history))
+        finally:
+            g.close()
+        assert len(hists) == 1, (method, nparts, len(hists))
+        assert out.iterations == ne["iterations"], (method, nparts, out.iterations, ne["iterations"])
+        np.testing.assert_allclose([r.rel_res_recur for r in out.history[:60]], ne["rel"][:60], rtol=1e-12)
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                       env={**os.environ, "PBS_K1_OPP": "1", "PYTHONPATH": root})
     assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-3000:]

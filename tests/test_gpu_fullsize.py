@@ -33,7 +33,7 @@ def _case(name):
     return data[name]
 
 
-def _solve(spec, operator, method, tol, max_iters):
+def _solve(spec, operator, method, tol, max_iters, engine=None):
     import torch
 
     import paper_2108_10591_b200 as pb
@@ -47,7 +47,7 @@ def _solve(spec, operator, method, tol, max_iters):
     bd = torch.empty_like(ones)
     dm.spmv_dev(ones.data_ptr(), bd.data_ptr())
     b = bd.cpu().numpy()
-    out = pb.solve(dm, b, method=method, config=pb.SolverConfig(tol=tol, max_iters=max_iters))
+    out = pb.solve(dm, b, method=method, config=pb.SolverConfig(tol=tol, max_iters=max_iters), engine=engine)
     # true residual on the device: || b - A x || / r0_norm
     xd = torch.from_numpy(np.ascontiguousarray(out.x)).cuda()
     ax = torch.empty_like(xd)
@@ -79,3 +79,23 @@ def test_full_size_count_in_oracle_ensemble(name, cfg, k, operator):
     np.testing.assert_allclose([r.rel_res_recur for r in out.history[:m]], ne["rel_first"][:m], rtol=1e-9)
     ref_true = max(r["true_rel"] for r in runs.values())
     assert true <= max(100 * rec["tol"], 10 * ref_true), (true, ref_true)
+
+
+@pytest.mark.parametrize("name,cfg,k", [("c5_full_rr", "c5", None), ("c4_k128", "c4", 128)])
+def test_full_size_plan_order_equals_oracle_run(name, cfg, k):
+    """Bitwise at full size: the device in the reference's PartitionPlan order
+    (W = 8 chains, left-to-right combine) repeats the oracle's W = 8 run record
+    for record and stops at the same iteration (config 5: 1001 iterations of
+    a Péclet-100 system, where any last-bit difference in a dot changes the
+    count)."""
+    import paper_2108_10591_b200 as pb
+    from paper_2108_10591_b200 import problems
+
+    rec = _case(name)
+    ref = rec["runs"]["8"]
+    spec = problems.config_stencil(cfg, k=k)
+    out, true = _solve(spec, "stencil", rec["method"], rec["tol"], rec["max_iters"],
+                       engine=pb.DeviceEngine(reduce="plan", workers=8))
+    assert out.iterations == ref["iterations"]
+    m = len(ref["rel_first"])
+    assert [r.rel_res_recur for r in out.history[:m]] == ref["rel_first"]

@@ -30,7 +30,7 @@ args = ap.parse_args()
 out_path = os.path.join(ROOT, "tests", "golden", "fullsize_counts.json")
 res = json.load(open(out_path)) if os.path.exists(out_path) else {}
 cases = [
-    ("c5_full_rr", problems.config_stencil("c5"), "pbicgsafe-rr", 1e-12, 4000, (1, 8, -1)),
+    ("c5_full_rr", problems.config_stencil("c5"), "pbicgsafe-rr", 1e-12, 4000, (1, 8, -1, 2, 3, 16, 64, 512, 4096)),
     ("c4_k128", problems.config_stencil("c4", k=128), "pbicgsafe", 1e-10, 4000, (1, 8, 64, -1)),
 ]
 for name, spec, method, tol, max_iters, orders in cases:
