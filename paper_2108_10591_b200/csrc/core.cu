@@ -47,6 +47,10 @@ MatSig mat_sig(const pbs_mat* m) {
   g.ci = m->ci;
   g.v = m->v;
   g.wc = m->wc;
+  g.sell_v = m->sell_v;
+  g.sell_c = m->sell_c;
+  g.sell_off = m->sell_off;
+  g.sell_lmax = m->sell_lmax;
   memcpy(&g.xwin, &m->xwin, sizeof(XWin));
   memcpy(&g.sv, &m->sv, sizeof(StencilView));
   memcpy(&g.swin, &m->swin, sizeof(StencilWin));
@@ -472,7 +476,108 @@ __global__ void window_cols_kernel(const long long* rp, const int* ci, long long
   }
 }
 
+// ---- sliced-ELL copy of a window-mode operator (sell.cuh)
+
+// levels (longest row) of each 256-row block, as entries: out[b + 1] = 256 * L_b
+__global__ void sell_levels_kernel(const long long* rp, long long n_rows, long long nblk, long long* out, int* lmax) {
+  __shared__ int wmax[8];
+  for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const long long r = b * kPipeRows + threadIdx.x;
+    int len = r < n_rows ? (int)(rp[r + 1] - rp[r]) : 0;
+    len = __reduce_max_sync(0xffffffffu, len);
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = len;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int L = 0;
+      for (int w = 0; w < 8; ++w) L = max(L, wmax[w]);
+      out[b + 1] = (long long)L * kPipeRows;
+      atomicMax(lmax, L);
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
+}
+
+// entry (k, t) of block b: the k-th nonzero of row 256 b + t, or padding
+__global__ void sell_fill_kernel(const long long* rp, const double* v, const unsigned short* wc, long long n_rows,
+                                 long long nblk, const long long* soff, double* sv, unsigned short* sc) {
+  for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const long long r = b * kPipeRows + threadIdx.x;
+    long long s = 0;
+    int len = 0;
+    if (r < n_rows) {
+      s = rp[r];
+      len = (int)(rp[r + 1] - s);
+    }
+    const long long off = soff[b];
+    const int L = (int)((soff[b + 1] - off) / kPipeRows);
+    for (int k = 0; k < L; ++k) {
+      const long long e = off + (long long)k * kPipeRows + threadIdx.x;
+      sv[e] = k < len ? v[s + k] : 0.0;
+      sc[e] = k < len ? wc[s + k] : (unsigned short)kSellPad;
+    }
+  }
+}
+
+static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
+  pool_free(ctx, m->sell_v);
+  pool_free(ctx, m->sell_c);
+  pool_free(ctx, m->sell_off);
+  m->sell_v = nullptr;
+  m->sell_c = nullptr;
+  m->sell_off = nullptr;
+  m->sell_lmax = 0;
+  m->sell_entries = 0;
+}
+
+// Built when the padding stays small (PBS_SELL_PAD percent over nnz, default
+// 12; PBS_SELL=0 keeps CSR order only): stencil-like row lengths.
+static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
+  free_sell(ctx, m);
+  if (!m->wc || !m->xwin.nwin || m->xwin.band_s || !env_int("PBS_SELL", 1, 0, 1)) return PBS_OK;
+  cudaStream_t s = ctx->stream;
+  const long long nblk = (m->n_rows + kPipeRows - 1) / kPipeRows;
+  int* lmax = nullptr;
+  CK(pool_alloc(ctx, &m->sell_off, sizeof(long long) * (nblk + 1)));
+  CK(pool_alloc(ctx, &lmax, sizeof(int)));
+  CK(cudaMemsetAsync(lmax, 0, sizeof(int), s));
+  sell_levels_kernel<<<(int)std::min<long long>(nblk, ctx->sms * 8), kPipeRows, 0, s>>>(m->rp, m->n_rows, nblk, m->sell_off,
+                                                                                       lmax);
+  size_t tmp_bytes = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, m->sell_off, m->sell_off, nblk + 1, s);
+  void* tmp = nullptr;
+  CK(pool_alloc(ctx, &tmp, tmp_bytes));
+  cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, m->sell_off, m->sell_off, nblk + 1, s);
+  pool_free(ctx, tmp);
+  long long entries = 0;
+  int hl = 0;
+  CK(cudaMemcpyAsync(&entries, m->sell_off + nblk, sizeof(entries), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&hl, lmax, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  pool_free(ctx, lmax);
+  const long long pad_pct = env_int("PBS_SELL_PAD", 12, 0, 1000);
+  if (entries <= 0 || entries > m->nnz + m->nnz * pad_pct / 100 + 64 * kPipeRows) {
+    free_sell(ctx, m);
+    return PBS_OK;
+  }
+  CK(pool_alloc(ctx, &m->sell_v, sizeof(double) * entries));
+  CK(pool_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
+  sell_fill_kernel<<<(int)std::min<long long>(nblk, ctx->sms * 8), kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk,
+                                                                                     m->sell_off, m->sell_v, m->sell_c);
+  CK(cudaGetLastError());
+  m->sell_lmax = hl;
+  m->sell_entries = entries;
+  return PBS_OK;
+}
+
+static int build_window_cols_only(pbs_ctx* ctx, pbs_mat* m);
 static int build_window_cols(pbs_ctx* ctx, pbs_mat* m) {
+  int rc = build_window_cols_only(ctx, m);
+  if (rc) return rc;
+  return build_sell(ctx, m);
+}
+
+static int build_window_cols_only(pbs_ctx* ctx, pbs_mat* m) {
   if (m->wc) {
     pool_free(ctx, m->wc);
     m->wc = nullptr;
@@ -500,6 +605,11 @@ static int build_window_cols(pbs_ctx* ctx, pbs_mat* m) {
 // clusters of row offsets -> x windows (<= kMaxWin, <= kMaxWinElems staged)
 int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   m->xwin = XWin{};
+  if (!m->stencil) {  // rebuilt below when the new pattern windows
+    pool_free(ctx, m->wc);
+    m->wc = nullptr;
+    free_sell(ctx, m);
+  }
   if (m->n_rows == 0 || m->nnz == 0 || m->n_cols > 0x7fffffffLL) return PBS_OK;
   cudaStream_t s = ctx->stream;
   int *bmin = nullptr, *bmax = nullptr, *wide = nullptr;
@@ -971,6 +1081,9 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   pool_free(m->ctx, m->ci);
   pool_free(m->ctx, m->v);
   pool_free(m->ctx, m->wc);
+  pool_free(m->ctx, m->sell_v);
+  pool_free(m->ctx, m->sell_c);
+  pool_free(m->ctx, m->sell_off);
   delete m;
   return PBS_OK;
 }

@@ -16,6 +16,7 @@
 #include "spmv.cuh"
 #include "vec.cuh"
 #include "zmarch.cuh"
+#include "sell.cuh"
 
 using namespace pbs;
 
@@ -74,6 +75,8 @@ struct MatSig {
   long long n_rows, n_cols, nnz, blk_nnz_max;
   long long stencil;
   const void *rp, *ci, *v, *wc;
+  const void *sell_v, *sell_c, *sell_off;
+  long long sell_lmax;
   XWin xwin;
   StencilView sv;
   StencilWin swin;
@@ -105,6 +108,12 @@ struct pbs_mat {
   int* ci = nullptr;
   double* v = nullptr;
   unsigned short* wc = nullptr;  // window-local column per nonzero (staged engine; null: col_idx)
+  // sliced-ELL copy of the nonzeros for sell_pipe_kernel (sell.cuh; null: CSR order only)
+  double* sell_v = nullptr;
+  unsigned short* sell_c = nullptr;
+  long long* sell_off = nullptr;  // entry offset per 256-row block, nblk + 1
+  int sell_lmax = 0;          // most levels (longest row) in one block
+  long long sell_entries = 0;
   StencilView sv{};
   XWin xwin{};  // x windows of the pipelined engines (nwin = 0: gather x)
   StencilWin swin{};  // stencil point -> window
@@ -298,6 +307,10 @@ static inline int pipe_slots_cap() {
   static int v = env_int("PBS_PIPE_SLOTS", 2, 2, kMaxStages);
   return v;
 }
+static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
+  static int v = env_int("PBS_SELL_SLOTS", 2, 2, kMaxStages);
+  return v;
+}
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
   static int v = env_int("PBS_PIPE_XCHUNK", 0, 0, 4);
   return v;
@@ -371,6 +384,60 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   *smem = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double) + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
   const void* k = si ? (c == 1 ? (const void*)csr_pipe_kernel<Epi, true, 1> : (const void*)csr_pipe_kernel<Epi, true>)
                      : (const void*)csr_pipe_kernel<Epi, false>;
+  auto it = ctx->occ.find(k);
+  if (it == ctx->occ.end() || (size_t)it->second < *smem) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
+    if (e != cudaSuccess) return set_err(ctx, PBS_ERR_CUDA, std::string("smem attribute: ") + cudaGetErrorString(e));
+    ctx->occ[k] = (int)*smem;
+  }
+  return PBS_OK;
+}
+
+// Ring sizing of the sliced-ELL engine (sell.cuh), by the same rule: block
+// slots hold the x windows and epilogue inputs (no row_ptr slice), chunk
+// stages klev levels of the block (one chunk per block when its longest row
+// has at most kSellLevMax nonzeros: 7-point stencils).
+template <class Epi>
+static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, int* bslots, int* cstages, size_t* smem, int* ctas,
+                       int* klev) {
+  static int lev_cap = env_int("PBS_SELL_LEV", kSellLevMax, 1, kSellLevMax);
+  int kl = lmax < lev_cap ? lmax : lev_cap;
+  if (kl < 1) kl = 1;
+  const SellChunkLayout CL(kl);
+  const SellBlockLayout BL(W.total, Epi::kInStaged);
+  int per_sm = 0, optin = 0;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
+  const char* xenv = getenv("PBS_PIPE_XCHUNK");
+  const int xcap = xenv ? pipe_extra_chunks() : (lmax > kl ? kMaxStages : 0);
+  int n = 0, c = 0, xc = 0;
+  size_t best = 0;
+  for (int cc = pipe_ctas_per_sm(); cc >= 1; --cc) {
+    size_t budget = (size_t)per_sm / cc - 1024 - 2048;
+    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
+    if (budget <= kPipeBarrierBytes) continue;
+    budget -= kPipeBarrierBytes;
+    int nn = (int)(budget / (BL.bytes + CL.bytes));
+    if (nn > sell_slots_cap()) nn = sell_slots_cap();
+    if (nn < 2) continue;
+    int xx = (int)((budget - (size_t)nn * (BL.bytes + CL.bytes)) / CL.bytes);
+    if (xx > xcap) xx = xcap;
+    if (nn + xx > kMaxStages) xx = kMaxStages - nn;
+    const size_t bytes = (size_t)cc * ((size_t)nn * BL.bytes + (size_t)(nn + xx) * CL.bytes);
+    if (bytes * 20 > best * 21) {
+      best = bytes;
+      n = nn;
+      c = cc;
+      xc = xx;
+    }
+  }
+  if (n < 2) return set_err(ctx, PBS_ERR_UNSUPPORTED, "not enough shared memory for the SpMV pipeline");
+  *ctas = c;
+  *bslots = n;
+  *cstages = n + xc;
+  *klev = kl;
+  *smem = kPipeBarrierBytes + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
+  const void* k = c == 1 ? (const void*)sell_pipe_kernel<Epi, 1> : (const void*)sell_pipe_kernel<Epi, 2>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -604,6 +671,27 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       grid = tpr_grid((const void*)csr_tpr_kernel<Epi, false>);
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
+  } else if (!m->stencil && m->sell_v && (lo % kPipeRows) == 0) {
+    // sliced-ELL form (sell.cuh): row blocks counted from row 0, like the
+    // window-local columns
+    SellView A{m->sell_v, m->sell_c, m->sell_off, lo, hi, m->n_cols};
+    int bslots, cstages, ctas, klev;
+    size_t smem;
+    int rc = sell_config<Epi>(L.ctx, m->xwin, m->sell_lmax, &bslots, &cstages, &smem, &ctas, &klev);
+    if (rc) {
+      L.err = rc;
+      return 0;
+    }
+    const long long nb = (hi - lo + kPipeRows - 1) / kPipeRows;
+    const long long cap = (long long)L.sms() * ctas;
+    grid = L.cap_grid(nb < cap ? nb : cap);
+    if (ctas == 1)
+      launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, 1>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots,
+                 cstages, klev);
+    else
+      launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, 2>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots,
+                 cstages, klev);
+    if (L.err) return 0;
   } else if (!m->stencil) {
     // window-local columns describe the 256-row blocks counted from row 0, so
     // any launch starting on a block boundary can use them
