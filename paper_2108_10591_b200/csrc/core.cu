@@ -50,6 +50,9 @@ MatSig mat_sig(const pbs_mat* m) {
   g.sell_v = m->sell_v;
   g.sell_c = m->sell_c;
   g.sell_off = m->sell_off;
+  g.sell_len = m->sell_len;
+  g.sell_vi = m->sell_vi;
+  g.sell_dict = m->sell_dict;
   g.sell_lmax = m->sell_lmax;
   memcpy(&g.xwin, &m->xwin, sizeof(XWin));
   memcpy(&g.sv, &m->sv, sizeof(StencilView));
@@ -498,9 +501,76 @@ __global__ void sell_levels_kernel(const long long* rp, long long n_rows, long l
   if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
 }
 
-// entry (k, t) of block b: the k-th nonzero of row 256 b + t, or padding
+// ---- value dictionary: the distinct f64 bit patterns of the operator, when
+// there are at most kSellDict.  An open-addressing table of kDictSlots keys;
+// kDictEmpty (a NaN payload) marks a free slot and is itself refused as a value.
+constexpr int kDictSlots = 1024;
+constexpr unsigned long long kDictEmpty = 0x7ff8dead00000001ULL;
+
+__device__ __forceinline__ unsigned dict_hash(unsigned long long b) {
+  b ^= b >> 33;
+  b *= 0xff51afd7ed558ccdULL;
+  b ^= b >> 33;
+  return (unsigned)b & (kDictSlots - 1);
+}
+
+// ctl[0]: distinct values seen, ctl[1]: gave up (too many, or the reserved pattern)
+__global__ void dict_insert_kernel(const double* v, long long nnz, unsigned long long* table, int* ctl) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  unsigned long long last = kDictEmpty;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
+    if (b == last) continue;
+    last = b;
+    if (*(volatile int*)(ctl + 1)) return;
+    if (b == kDictEmpty) {
+      ctl[1] = 1;
+      return;
+    }
+    unsigned h = dict_hash(b);
+    for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+      unsigned long long cur = *(volatile unsigned long long*)(table + h);
+      if (cur == b) break;
+      if (cur == kDictEmpty) {
+        cur = atomicCAS(table + h, kDictEmpty, b);
+        if (cur == kDictEmpty) {
+          if (atomicAdd(ctl, 1) >= kSellDict) ctl[1] = 1;
+          break;
+        }
+        if (cur == b) break;
+      }
+    }
+  }
+}
+
+// occupied slots -> dictionary entries, in slot order (one thread: 1024 slots)
+__global__ void dict_compact_kernel(const unsigned long long* table, double* dict, unsigned char* slot_idx) {
+  int n = 0;
+  for (int h = 0; h < kDictSlots; ++h) {
+    const unsigned long long b = table[h];
+    if (b != kDictEmpty && n < kSellDict) {
+      dict[n] = __longlong_as_double((long long)b);
+      slot_idx[h] = (unsigned char)n++;
+    }
+  }
+  for (; n < kSellDict; ++n) dict[n] = 0.0;
+}
+
+__device__ __forceinline__ unsigned char dict_lookup(const unsigned long long* table, const unsigned char* slot_idx,
+                                                     double val) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(val);
+  unsigned h = dict_hash(b);
+  for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1))
+    if (__ldg(table + h) == b) return __ldg(slot_idx + h);
+  return 0;  // unreachable: every value was inserted
+}
+
+// entry (k, t) of block b: the k-th nonzero of row 256 b + t, or padding.
+// table != null: the value's dictionary index goes to svi instead of sv.
 __global__ void sell_fill_kernel(const long long* rp, const double* v, const unsigned short* wc, long long n_rows,
-                                 long long nblk, const long long* soff, double* sv, unsigned short* sc) {
+                                 long long nblk, const long long* soff, double* sv, unsigned short* sc,
+                                 unsigned char* slen, const unsigned long long* table,
+                                 const unsigned char* slot_idx, unsigned char* svi) {
   for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
     const long long r = b * kPipeRows + threadIdx.x;
     long long s = 0;
@@ -513,9 +583,13 @@ __global__ void sell_fill_kernel(const long long* rp, const double* v, const uns
     const int L = (int)((soff[b + 1] - off) / kPipeRows);
     for (int k = 0; k < L; ++k) {
       const long long e = off + (long long)k * kPipeRows + threadIdx.x;
-      sv[e] = k < len ? v[s + k] : 0.0;
-      sc[e] = k < len ? wc[s + k] : (unsigned short)kSellPad;
+      if (table)
+        svi[e] = k < len ? dict_lookup(table, slot_idx, v[s + k]) : (unsigned char)0;
+      else
+        sv[e] = k < len ? v[s + k] : 0.0;
+      sc[e] = k < len ? wc[s + k] : (unsigned short)0;
     }
+    slen[b * kPipeRows + threadIdx.x] = (unsigned char)len;
   }
 }
 
@@ -523,6 +597,13 @@ static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
   pool_free(ctx, m->sell_v);
   pool_free(ctx, m->sell_c);
   pool_free(ctx, m->sell_off);
+  pool_free(ctx, m->sell_len);
+  pool_free(ctx, m->sell_vi);
+  pool_free(ctx, m->sell_dict);
+  m->sell_len = nullptr;
+  m->sell_vi = nullptr;
+  m->sell_dict = nullptr;
+  m->sell_ndict = 0;
   m->sell_v = nullptr;
   m->sell_c = nullptr;
   m->sell_off = nullptr;
@@ -556,15 +637,45 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
   CK(cudaStreamSynchronize(s));
   pool_free(ctx, lmax);
   const long long pad_pct = env_int("PBS_SELL_PAD", 12, 0, 1000);
-  if (entries <= 0 || entries > m->nnz + m->nnz * pad_pct / 100 + 64 * kPipeRows) {
+  if (entries <= 0 || hl > kSellMaxLen || entries > m->nnz + m->nnz * pad_pct / 100 + 64 * kPipeRows) {
     free_sell(ctx, m);
     return PBS_OK;
   }
-  CK(pool_alloc(ctx, &m->sell_v, sizeof(double) * entries));
+  // value dictionary (PBS_SELL_DICT=0: keep the f64 value stream)
+  unsigned long long* table = nullptr;
+  unsigned char* slot_idx = nullptr;
+  int hctl[2] = {0, 1};
+  if (env_int("PBS_SELL_DICT", 1, 0, 1)) {
+    int* ctl = nullptr;
+    CK(pool_alloc(ctx, &table, sizeof(unsigned long long) * kDictSlots));
+    CK(pool_alloc(ctx, &slot_idx, kDictSlots));
+    CK(pool_alloc(ctx, &ctl, sizeof(int) * 2));
+    std::vector<unsigned long long> empty(kDictSlots, kDictEmpty);
+    CK(cudaMemcpyAsync(table, empty.data(), sizeof(unsigned long long) * kDictSlots, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(slot_idx, 0, kDictSlots, s));
+    CK(cudaMemsetAsync(ctl, 0, sizeof(int) * 2, s));
+    dict_insert_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->v, m->nnz, table, ctl);
+    CK(cudaMemcpyAsync(hctl, ctl, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // (also keeps `empty` alive until its copy has run)
+    pool_free(ctx, ctl);
+  }
+  const bool dict = hctl[1] == 0 && hctl[0] <= kSellDict;
+  if (dict) {
+    CK(pool_alloc(ctx, &m->sell_dict, sizeof(double) * kSellDict));
+    CK(pool_alloc(ctx, &m->sell_vi, (size_t)entries));
+    dict_compact_kernel<<<1, 1, 0, s>>>(table, m->sell_dict, slot_idx);
+    m->sell_ndict = hctl[0];
+  } else {
+    CK(pool_alloc(ctx, &m->sell_v, sizeof(double) * entries));
+  }
   CK(pool_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
+  CK(pool_alloc(ctx, &m->sell_len, (size_t)nblk * kPipeRows));
   sell_fill_kernel<<<(int)std::min<long long>(nblk, ctx->sms * 8), kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk,
-                                                                                     m->sell_off, m->sell_v, m->sell_c);
+                                                                                     m->sell_off, m->sell_v, m->sell_c, m->sell_len,
+                                                                                     dict ? table : nullptr, slot_idx, m->sell_vi);
   CK(cudaGetLastError());
+  pool_free(ctx, table);
+  pool_free(ctx, slot_idx);
   m->sell_lmax = hl;
   m->sell_entries = entries;
   return PBS_OK;
@@ -1084,6 +1195,9 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   pool_free(m->ctx, m->sell_v);
   pool_free(m->ctx, m->sell_c);
   pool_free(m->ctx, m->sell_off);
+  pool_free(m->ctx, m->sell_len);
+  pool_free(m->ctx, m->sell_vi);
+  pool_free(m->ctx, m->sell_dict);
   delete m;
   return PBS_OK;
 }

@@ -75,7 +75,7 @@ struct MatSig {
   long long n_rows, n_cols, nnz, blk_nnz_max;
   long long stencil;
   const void *rp, *ci, *v, *wc;
-  const void *sell_v, *sell_c, *sell_off;
+  const void *sell_v, *sell_c, *sell_off, *sell_len, *sell_vi, *sell_dict;
   long long sell_lmax;
   XWin xwin;
   StencilView sv;
@@ -111,7 +111,12 @@ struct pbs_mat {
   // sliced-ELL copy of the nonzeros for sell_pipe_kernel (sell.cuh; null: CSR order only)
   double* sell_v = nullptr;
   unsigned short* sell_c = nullptr;
-  long long* sell_off = nullptr;  // entry offset per 256-row block, nblk + 1
+  long long* sell_off = nullptr;
+  unsigned char* sell_len = nullptr;  // nonzeros per row, 256 per block
+  // value dictionary (<= 256 distinct values): u8 index per entry instead of sell_v
+  unsigned char* sell_vi = nullptr;
+  double* sell_dict = nullptr;
+  int sell_ndict = 0;
   int sell_lmax = 0;          // most levels (longest row) in one block
   long long sell_entries = 0;
   StencilView sv{};
@@ -308,7 +313,7 @@ static inline int pipe_slots_cap() {
   return v;
 }
 static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
-  static int v = env_int("PBS_SELL_SLOTS", 2, 2, kMaxStages);
+  static int v = env_int("PBS_SELL_SLOTS", 4, 2, kMaxStages);
   return v;
 }
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
@@ -398,12 +403,12 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
 // stages klev levels of the block (one chunk per block when its longest row
 // has at most kSellLevMax nonzeros: 7-point stencils).
 template <class Epi>
-static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, int* bslots, int* cstages, size_t* smem, int* ctas,
-                       int* klev) {
+static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, bool dict, int* bslots, int* cstages, size_t* smem,
+                       int* ctas, int* klev) {
   static int lev_cap = env_int("PBS_SELL_LEV", kSellLevMax, 1, kSellLevMax);
   int kl = lmax < lev_cap ? lmax : lev_cap;
   if (kl < 1) kl = 1;
-  const SellChunkLayout CL(kl);
+  const SellChunkLayout CL(kl, dict ? 1 : 8);
   const SellBlockLayout BL(W.total, Epi::kInStaged);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
@@ -437,7 +442,8 @@ static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, int* bslots, int* 
   *cstages = n + xc;
   *klev = kl;
   *smem = kPipeBarrierBytes + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
-  const void* k = c == 1 ? (const void*)sell_pipe_kernel<Epi, 1> : (const void*)sell_pipe_kernel<Epi, 2>;
+  const void* k = dict ? (c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, true> : (const void*)sell_pipe_kernel<Epi, 2, true>)
+                       : (c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, false> : (const void*)sell_pipe_kernel<Epi, 2, false>);
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -671,13 +677,14 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       grid = tpr_grid((const void*)csr_tpr_kernel<Epi, false>);
       csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
     }
-  } else if (!m->stencil && m->sell_v && (lo % kPipeRows) == 0) {
+  } else if (!m->stencil && (m->sell_v || m->sell_vi) && (lo % kPipeRows) == 0) {
     // sliced-ELL form (sell.cuh): row blocks counted from row 0, like the
     // window-local columns
-    SellView A{m->sell_v, m->sell_c, m->sell_off, lo, hi, m->n_cols};
+    SellView A{m->sell_v, m->sell_vi, m->sell_dict, m->sell_c, m->sell_len, m->sell_off, lo, hi, m->n_cols};
+    const bool dict = m->sell_vi != nullptr;
     int bslots, cstages, ctas, klev;
     size_t smem;
-    int rc = sell_config<Epi>(L.ctx, m->xwin, m->sell_lmax, &bslots, &cstages, &smem, &ctas, &klev);
+    int rc = sell_config<Epi>(L.ctx, m->xwin, m->sell_lmax, dict, &bslots, &cstages, &smem, &ctas, &klev);
     if (rc) {
       L.err = rc;
       return 0;
@@ -685,12 +692,14 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     const long long nb = (hi - lo + kPipeRows - 1) / kPipeRows;
     const long long cap = (long long)L.sms() * ctas;
     grid = L.cap_grid(nb < cap ? nb : cap);
-    if (ctas == 1)
-      launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, 1>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots,
-                 cstages, klev);
-    else
-      launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, 2>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots,
-                 cstages, klev);
+#define PBS_SELL(MB, D)                                                                                      \
+  launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, MB, D>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots, \
+             cstages, klev)
+    if (dict && ctas == 1) PBS_SELL(1, true);
+    else if (dict) PBS_SELL(2, true);
+    else if (ctas == 1) PBS_SELL(1, false);
+    else PBS_SELL(2, false);
+#undef PBS_SELL
     if (L.err) return 0;
   } else if (!m->stencil) {
     // window-local columns describe the 256-row blocks counted from row 0, so

@@ -10,8 +10,10 @@
 // At upload the operator's nonzeros are therefore also laid out per 256-row
 // block in level-major ("sliced ELL", slice = the row block) order: level k
 // of the block holds the k-th nonzero of each of its 256 rows — value and
-// window-local u16 column — padded with a sentinel column where a row is
-// shorter than the block's longest.  A block is L x 256 entries, contiguous,
+// window-local u16 column — padded (value 0, column 0) where a row is shorter
+// than the block's longest; a u8 length per row tells the consumer which
+// levels to add (a padded product is formed but never added, so signed
+// zeros and non-finite x stay exactly the reference's).  A block is L x 256 entries, contiguous,
 // so the producer still streams it with two 1-D bulk copies per chunk of
 // levels, and there is no row_ptr stream at all (8 B per row less per
 // product).  Consumer thread t reads entry k * 256 + t: consecutive lanes
@@ -19,6 +21,13 @@
 // is CTA-uniform, and the loop has no per-thread bounds.  Each row still sums
 // its products sequentially in ascending column order with rounded products
 // and rounded adds, so the result is bitwise kernels.py:95-100's.
+//
+// Value dictionary (DICT): when the operator holds at most 256 distinct
+// values (discretised constant-coefficient operators: 7 or 27), the value
+// stream is a u8 index per entry into a dictionary the CTA keeps in shared
+// memory — 3 bytes per nonzero instead of 10 from HBM, and chunk stages small
+// enough for a third block slot.  The f64 looked up is bit for bit the
+// uploaded value, so nothing changes in the arithmetic.
 //
 // Used for window-mode operators whose padding is small (stencil-like row
 // lengths: configs 1, 2, 4, 5); band mode, gathered x and ragged matrices
@@ -28,12 +37,16 @@
 
 namespace pbs {
 
-constexpr unsigned kSellPad = 0xffffu;  // sentinel column of a padding entry
+constexpr int kSellMaxLen = 255;        // longest row the u8 row lengths can hold
 constexpr int kSellLevMax = 8;          // levels per chunk stage, at most (20 KiB)
+constexpr int kSellDict = 256;          // dictionary entries (u8 value indices)
 
 struct SellView {
-  const double* sv;           // values, level-major per row block
-  const unsigned short* sc;   // window-local columns (kSellPad: padding)
+  const double* sv;           // values, level-major per row block (null with a dictionary)
+  const unsigned char* svi;   // DICT: index of each value in dict
+  const double* dict;         // DICT: kSellDict distinct values
+  const unsigned short* sc;   // window-local columns (0 in padding entries)
+  const unsigned char* slen;  // nonzeros per row, 256 per row block (0 past the last row)
   const long long* soff;      // entry offset of each 256-row block (multiples of 256), nblk + 1
   long long row_lo, row_hi;   // row_lo is a multiple of 256
   long long n_cols;
@@ -44,30 +57,45 @@ struct SellHdr {
   int nr, levels, fused, pad;
 };
 
-// block slot: header, x windows, epilogue inputs
+// block slot: header, row lengths, x windows, epilogue inputs
 struct SellBlockLayout {
-  size_t xw, ein, bytes;
+  size_t len, xw, ein, bytes;
   __host__ __device__ SellBlockLayout(int xw_total, int kin) {
-    xw = 128;
+    len = 128;
+    xw = len + kPipeRows;
     ein = xw + align128(sizeof(double) * (xw_total > 0 ? xw_total : 2));
     bytes = ein + align128(sizeof(double) * kPipeRows * (kin > 0 ? kin : 1));
   }
 };
 
-// chunk stage: klev levels of values, then of columns
+// chunk stage: klev levels of values (vb bytes each: f64, or u8 dictionary
+// indices), then of columns
 struct SellChunkLayout {
   size_t ci, bytes;
-  __host__ __device__ SellChunkLayout(int klev) {
-    ci = sizeof(double) * kPipeRows * (size_t)klev;
+  __host__ __device__ SellChunkLayout(int klev, int vb) {
+    ci = (size_t)vb * kPipeRows * (size_t)klev;
     bytes = ci + sizeof(unsigned short) * kPipeRows * (size_t)klev;
   }
 };
 
+// acc + p when level k of the chunk is one of the row's (k < rem), as a
+// predicated rounded add (no select on the result)
+__device__ __forceinline__ double sell_add_if(double acc, double p, int k, int rem) {
+  asm("{\n\t.reg .pred q;\n\tsetp.lt.s32 q, %2, %3;\n\t@q add.rn.f64 %0, %0, %1;\n\t}"
+      : "+d"(acc)
+      : "d"(p), "r"(k), "r"(rem));
+  return acc;
+}
+
 // N levels of one row, G staged products in flight: columns, values and x
-// loads are issued ahead of the rounded product / rounded add chain
-template <int N, int G>
-__device__ __forceinline__ double sell_levels(const double* __restrict__ vs, const unsigned short* __restrict__ cs,
-                                              const double* __restrict__ xw, double acc) {
+// loads are issued ahead of the rounded product / rounded add chain; rem =
+// the row's nonzeros left at this chunk's first level
+template <int N, int G, bool DICT>
+__device__ __forceinline__ double sell_levels(const void* __restrict__ vsv, const unsigned short* __restrict__ cs,
+                                              const double* __restrict__ xw, const double* __restrict__ dict,
+                                              double acc, int rem) {
+  const double* vs = reinterpret_cast<const double*>(vsv);
+  const unsigned char* vi = reinterpret_cast<const unsigned char*>(vsv);
 #pragma unroll
   for (int k0 = 0; k0 < N; k0 += G) {
     unsigned c[G];
@@ -77,30 +105,29 @@ __device__ __forceinline__ double sell_levels(const double* __restrict__ vs, con
       if (k0 + u < N) c[u] = cs[(k0 + u) * kPipeRows];
 #pragma unroll
     for (int u = 0; u < G; ++u)
-      if (k0 + u < N) v[u] = vs[(k0 + u) * kPipeRows];
+      if (k0 + u < N) v[u] = DICT ? dict[vi[(k0 + u) * kPipeRows]] : vs[(k0 + u) * kPipeRows];
 #pragma unroll
     for (int u = 0; u < G; ++u)
-      if (k0 + u < N) xv[u] = c[u] != kSellPad ? xw[c[u]] : 0.0;
+      if (k0 + u < N) xv[u] = xw[c[u]];
 #pragma unroll
     for (int u = 0; u < G; ++u)
-      if (k0 + u < N)
-        if (c[u] != kSellPad) acc = add(acc, mul(v[u], xv[u]));
+      if (k0 + u < N) acc = sell_add_if(acc, mul(v[u], xv[u]), k0 + u, rem);
   }
   return acc;
 }
 
-template <int G>
-__device__ __forceinline__ double sell_chunk(int nk, const double* vs, const unsigned short* cs, const double* xw,
-                                             double acc) {
+template <int G, bool DICT>
+__device__ __forceinline__ double sell_chunk(int nk, const void* vs, const unsigned short* cs, const double* xw,
+                                             const double* dict, double acc, int rem) {
   switch (nk) {  // CTA-uniform
-    case 8: return sell_levels<8, G>(vs, cs, xw, acc);
-    case 7: return sell_levels<7, G>(vs, cs, xw, acc);
-    case 6: return sell_levels<6, G>(vs, cs, xw, acc);
-    case 5: return sell_levels<5, G>(vs, cs, xw, acc);
-    case 4: return sell_levels<4, G>(vs, cs, xw, acc);
-    case 3: return sell_levels<3, G>(vs, cs, xw, acc);
-    case 2: return sell_levels<2, G>(vs, cs, xw, acc);
-    case 1: return sell_levels<1, G>(vs, cs, xw, acc);
+    case 8: return sell_levels<8, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 7: return sell_levels<7, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 6: return sell_levels<6, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 5: return sell_levels<5, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 4: return sell_levels<4, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 3: return sell_levels<3, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 2: return sell_levels<2, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 1: return sell_levels<1, G, DICT>(vs, cs, xw, dict, acc, rem);
     default: return acc;
   }
 }
@@ -109,18 +136,21 @@ __device__ __forceinline__ double sell_chunk(int nk, const double* vs, const uns
 // producer streams the first block's matrix chunks before griddep_wait; one
 // gate decision per CTA; consumers release the next grid once their rows are
 // written).  MINB: resident CTAs per SM the instantiation is compiled for.
-template <class Epi, int MINB = 2>
+template <class Epi, int MINB = 2, bool DICT = false>
 __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView A, const double* __restrict__ x,
                                                                     Epi epi, XWin W, int bslots, int cstages,
                                                                     int klev) {
   __shared__ int go;
+  __shared__ double dict_s[DICT ? kSellDict : 1];
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* cfull = reinterpret_cast<uint64_t*>(smem);
   uint64_t* cempty = cfull + kMaxStages;
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
   const SellBlockLayout BL(W.total, Epi::kInStaged);
-  const SellChunkLayout CL(klev);
+  const SellChunkLayout CL(klev, DICT ? 1 : 8);
+  // the dictionary belongs to the operator: read ahead of the grid dependency
+  if (DICT && threadIdx.x < kSellDict) dict_s[threadIdx.x] = __ldg(A.dict + threadIdx.x);
   unsigned char* blk0 = smem + kPipeBarrierBytes;
   unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -178,11 +208,11 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         unsigned char* st = chk0 + (size_t)cs * CL.bytes;
         const int nk = min(klev, levels - c * klev);
         const long long e0 = off + (long long)c * klev * kPipeRows;
-        const uint32_t bv = (uint32_t)(nk * kPipeRows * sizeof(double));
+        const uint32_t bv = (uint32_t)(nk * kPipeRows * (DICT ? 1 : sizeof(double)));
         const uint32_t bc = (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
         if (lane == 0) mbar_arrive_expect_tx(&cfull[cs], bv + bc);
         __syncwarp();
-        if (lane == 0) bulk_g2s(st, A.sv + e0, bv, &cfull[cs]);
+        if (lane == 0) bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
         if (lane == 1) bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
         if (++cs == cstages) {
           cs = 0;
@@ -203,7 +233,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
       }
       long long wlo[kMaxWin];
       uint32_t wbytes[kMaxWin];
-      uint32_t total = fuse_in ? Epi::kInStaged * bin : 0u;
+      uint32_t total = kPipeRows + (fuse_in ? Epi::kInStaged * bin : 0u);
 #pragma unroll
       for (int c = 0; c < kMaxWin; ++c) {
         wlo[c] = 0;
@@ -228,13 +258,12 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         bh->nr = nr;
         bh->levels = levels;
         bh->fused = fuse_in ? 1 : 0;
-        if (total)
-          mbar_arrive_expect_tx(&bfull[bs], total);
-        else
-          mbar_arrive(&bfull[bs]);
+        mbar_arrive_expect_tx(&bfull[bs], total);
       }
       __syncwarp();
-      if (lane >= 1 && lane <= W.nwin) {
+      if (lane == 0) {
+        bulk_g2s(bst + BL.len, A.slen + (gb0 + blk) * kPipeRows, kPipeRows, &bfull[bs]);
+      } else if (lane <= W.nwin) {
         int soff = 0;
 #pragma unroll
         for (int cc = 0; cc < kMaxWin; ++cc) {
@@ -282,14 +311,14 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
       for (int k = Epi::kInStaged; k < Epi::kIn; ++k) inr[k] = __ldg(e.in[k] + r0 + t);
     }
     const double* xw = reinterpret_cast<const double*>(bst + BL.xw);
+    const int len = reinterpret_cast<const unsigned char*>(bst + BL.len)[t];  // 0 past the last row
     double acc = 0.0;
     for (int l0 = 0; l0 < levels; l0 += klev) {
       mbar_wait(&cfull[cs], cph);
       const unsigned char* st = chk0 + (size_t)cs * CL.bytes;
       const int nk = min(klev, levels - l0);
-      // rows past the matrix end hold only padding entries
-      acc = sell_chunk<G>(nk, reinterpret_cast<const double*>(st) + t,
-                          reinterpret_cast<const unsigned short*>(st + CL.ci) + t, xw, acc);
+      acc = sell_chunk<G, DICT>(nk, st + (size_t)t * (DICT ? 1 : sizeof(double)),
+                                reinterpret_cast<const unsigned short*>(st + CL.ci) + t, xw, dict_s, acc, len - l0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&cempty[cs]);
       if (++cs == cstages) {
