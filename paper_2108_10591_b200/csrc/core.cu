@@ -616,6 +616,7 @@ static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
 static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
   free_sell(ctx, m);
   if (!m->wc || !m->xwin.nwin || m->xwin.band_s || !env_int("PBS_SELL", 1, 0, 1)) return PBS_OK;
+  if (m->n_rows > 0x7fff0000LL || m->n_cols > 0x7fff0000LL) return PBS_OK;  // the engine keeps row indices in 32 bits
   cudaStream_t s = ctx->stream;
   const long long nblk = (m->n_rows + kPipeRows - 1) / kPipeRows;
   int* lmax = nullptr;

@@ -313,7 +313,7 @@ static inline int pipe_slots_cap() {
   return v;
 }
 static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
-  static int v = env_int("PBS_SELL_SLOTS", 4, 2, kMaxStages);
+  static int v = env_int("PBS_SELL_SLOTS", 2, 2, kMaxStages);
   return v;
 }
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots

@@ -187,6 +187,35 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
     };
     bool opp_ready = false;
     if (nblk <= (int)blockIdx.x && !gate()) return;
+    // Every lane owns one copy stream of the block slot and works out its own
+    // source and size per block: lane 0 the row lengths, lanes 1..nwin the x
+    // windows, lanes 8.. the epilogue inputs.  (The whole warp used to compute
+    // all of it, and this warp's instruction stream, not HBM or the
+    // consumers, set the pace: ncu showed it never waiting on a free slot.)
+    const int role_win = lane >= 1 && lane <= W.nwin ? lane - 1 : -1;
+    const int role_in = lane >= 8 && lane < 8 + Epi::kInStaged ? lane - 8 : -1;
+    int wmin_l = 0, wmax_l = 0;
+    uint32_t dst_l = (uint32_t)BL.len;
+    const double* src_l = nullptr;
+    if (role_win >= 0) {
+      int so = 0;
+#pragma unroll
+      for (int cc = 0; cc < kMaxWin; ++cc) {
+        if (cc == role_win) {
+          wmin_l = W.wmin[cc];
+          wmax_l = W.wmax[cc];
+          dst_l = (uint32_t)(BL.xw + (size_t)so * sizeof(double));
+        }
+        so += cc < W.nwin ? W.cap[cc] : 0;
+      }
+      src_l = x;
+    } else if (role_in >= 0) {
+      dst_l = (uint32_t)(BL.ein + (size_t)role_in * kPipeRows * sizeof(double));
+#pragma unroll
+      for (int k = 0; k < Epi::kInStaged; ++k)
+        if (k == role_in) src_l = epi.in[k];
+    }
+    const int row_lo = (int)A.row_lo, row_hi = (int)A.row_hi, ncols = (int)A.n_cols;
     for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
       const int slot = q & 31;
       if (slot == 0) {  // entry offsets of blocks q .. q+31 of this CTA in one warp-wide load
@@ -198,11 +227,10 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
       }
       const long long off = __shfl_sync(0xffffffffu, pf_off, slot);
       const long long end = __shfl_sync(0xffffffffu, pf_end, slot);
-      const int levels = (int)((end - off) / kPipeRows);
+      const int levels = (int)((end - off) >> 8);
       const int nch = (levels + klev - 1) / klev;
-      const long long r0 = A.row_lo + (long long)blk * kPipeRows;
-      const int nr = (int)min((long long)kPipeRows, A.row_hi - r0);
-      const uint32_t bin = (uint32_t)(((nr + 1) & ~1) * sizeof(double));
+      const int r0 = row_lo + blk * kPipeRows;
+      const int nr = min(kPipeRows, row_hi - r0);
       auto issue_chunk = [&](int c) {
         mbar_wait(&cempty[cs], cph ^ 1);
         unsigned char* st = chk0 + (size_t)cs * CL.bytes;
@@ -210,10 +238,11 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         const long long e0 = off + (long long)c * klev * kPipeRows;
         const uint32_t bv = (uint32_t)(nk * kPipeRows * (DICT ? 1 : sizeof(double)));
         const uint32_t bc = (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
-        if (lane == 0) mbar_arrive_expect_tx(&cfull[cs], bv + bc);
-        __syncwarp();
-        if (lane == 0) bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
-        if (lane == 1) bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
+          bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
+          bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
+        }
         if (++cs == cstages) {
           cs = 0;
           cph ^= 1;
@@ -231,25 +260,26 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         if (!opp_ready) opp_ready = __shfl_sync(0xffffffffu, lane == 0 ? epi.ready() : false, 0);
         fuse_in = opp_ready;
       }
-      long long wlo[kMaxWin];
-      uint32_t wbytes[kMaxWin];
-      uint32_t total = kPipeRows + (fuse_in ? Epi::kInStaged * bin : 0u);
-#pragma unroll
-      for (int c = 0; c < kMaxWin; ++c) {
-        wlo[c] = 0;
-        wbytes[c] = 0;
-        if (c < W.nwin) {
-          long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
-          if (lo < 0) lo = 0;
-          if (hi > A.n_cols) hi = A.n_cols;
-          if (hi > lo) {
-            const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
-            wlo[c] = loa;
-            wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
-            total += wbytes[c];
-          }
+      // this lane's copy
+      const void* src = nullptr;
+      uint32_t bytes = 0;
+      if (lane == 0) {
+        src = A.slen + (gb0 + blk) * kPipeRows;
+        bytes = kPipeRows;
+      } else if (role_win >= 0) {
+        int lo = r0 + wmin_l, hi = r0 + nr + wmax_l;
+        if (lo < 0) lo = 0;
+        if (hi > ncols) hi = ncols;
+        if (hi > lo) {
+          const int loa = lo & ~1, hia = (hi + 1) & ~1;
+          src = src_l + loa;
+          bytes = (uint32_t)((hia - loa) * sizeof(double));
         }
+      } else if (role_in >= 0 && fuse_in) {
+        src = src_l + r0;
+        bytes = (uint32_t)(((nr + 1) & ~1) * sizeof(double));
       }
+      const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
       mbar_wait(&bempty[bs], bph ^ 1);
       unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
       if (lane == 0) {
@@ -261,20 +291,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         mbar_arrive_expect_tx(&bfull[bs], total);
       }
       __syncwarp();
-      if (lane == 0) {
-        bulk_g2s(bst + BL.len, A.slen + (gb0 + blk) * kPipeRows, kPipeRows, &bfull[bs]);
-      } else if (lane <= W.nwin) {
-        int soff = 0;
-#pragma unroll
-        for (int cc = 0; cc < kMaxWin; ++cc) {
-          if (cc == lane - 1 && wbytes[cc])
-            bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
-          soff += cc < W.nwin ? W.cap[cc] : 0;
-        }
-      } else if (fuse_in && lane >= 8 && lane < 8 + Epi::kInStaged) {
-        const int e = lane - 8;
-        bulk_g2s(bst + BL.ein + (size_t)e * kPipeRows * sizeof(double), epi.in[e] + r0, bin, &bfull[bs]);
-      }
+      if (bytes) bulk_g2s(bst + dst_l, src, bytes, &bfull[bs]);
       if (++bs == bslots) {
         bs = 0;
         bph ^= 1;

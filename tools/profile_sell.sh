@@ -9,3 +9,4 @@ ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page details --csv > $O/${TAG}_k12_k3_detail
 ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page raw --csv > $O/${TAG}_k12_k3_raw.csv 2>&1
 ncu -i /tmp/${TAG}_k12_k3.ncu-rep --page source --csv --print-source sass > /tmp/${TAG}_k12_k3_source.csv 2>/dev/null
 python tools/ncu_hot_sass.py /tmp/${TAG}_k12_k3_source.csv 60 > $O/${TAG}_k12_k3_hot_sass.txt 2>&1
+gzip -c /tmp/${TAG}_k12_k3_source.csv > $O/${TAG}_k12_k3_source.csv.gz
