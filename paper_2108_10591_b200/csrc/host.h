@@ -693,7 +693,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     const long long cap = (long long)L.sms() * ctas;
     grid = L.cap_grid(nb < cap ? nb : cap);
 #define PBS_SELL(MB, D)                                                                                      \
-  launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, MB, D>, grid, kPipeThreads, smem, A, x, epi, m->xwin, bslots, \
+  launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, MB, D>, grid, kSellThreads, smem, A, x, epi, m->xwin, bslots, \
              cstages, klev)
     if (dict && ctas == 1) PBS_SELL(1, true);
     else if (dict) PBS_SELL(2, true);

@@ -40,6 +40,7 @@ namespace pbs {
 constexpr int kSellMaxLen = 255;        // longest row the u8 row lengths can hold
 constexpr int kSellLevMax = 8;          // levels per chunk stage, at most (20 KiB)
 constexpr int kSellDict = 256;          // dictionary entries (u8 value indices)
+constexpr int kSellThreads = kPipeRows + 64;  // + two producer warps (block slots, matrix stream)
 
 struct SellView {
   const double* sv;           // values, level-major per row block (null with a dictionary)
@@ -137,7 +138,7 @@ __device__ __forceinline__ double sell_chunk(int nk, const void* vs, const unsig
 // gate decision per CTA; consumers release the next grid once their rows are
 // written).  MINB: resident CTAs per SM the instantiation is compiled for.
 template <class Epi, int MINB = 2, bool DICT = false>
-__global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView A, const double* __restrict__ x,
+__global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView A, const double* __restrict__ x,
                                                                     Epi epi, XWin W, int bslots, int cstages,
                                                                     int klev) {
   __shared__ int go;
@@ -170,28 +171,75 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
   const int nblk = (int)((nrows + kPipeRows - 1) / kPipeRows);
   const long long gb0 = A.row_lo / kPipeRows;  // first block, counted from row 0
 
-  if (warp == kConsumerWarps) {
-    // ----------------------------------------------------------- producer
-    int cs = 0, bs = 0;
-    uint32_t cph = 0, bph = 0;
+  if (warp == kConsumerWarps + 1) {
+    // ------------------------------------------- producer of the matrix stream
+    // The block's levels, klev per chunk stage.  Nothing here depends on the
+    // previous kernel, so the first chunks are in flight before the gate.
+    int cs = 0;
+    uint32_t cph = 0;
     long long pf_off = 0, pf_end = 0;
     bool gated = false;
     int issued = 0;  // chunk stages filled before the gate
     auto gate = [&]() -> bool {
       gated = true;
       griddep_wait();
-      cta_sync2<kPipeThreads>();  // thread 0 (a consumer) has taken the gate decision
+      cta_sync2<kSellThreads>();  // thread 0 (a consumer) has taken the gate decision
       if (go) return true;
       for (int s2 = 0; s2 < issued; ++s2) mbar_wait(&cfull[s2], 0);  // let the early copies land
       return false;
     };
-    bool opp_ready = false;
-    if (nblk <= (int)blockIdx.x && !gate()) return;
-    // Every lane owns one copy stream of the block slot and works out its own
+    for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
+      const int slot = q & 31;
+      if (slot == 0) {  // entry offsets of blocks q .. q+31 of this CTA in one warp-wide load
+        const long long b2 = (long long)blk + (long long)lane * gridDim.x;
+        if (b2 < nblk) {
+          pf_off = __ldg(A.soff + gb0 + b2);
+          pf_end = __ldg(A.soff + gb0 + b2 + 1);
+        }
+      }
+      const long long off = __shfl_sync(0xffffffffu, pf_off, slot);
+      const long long end = __shfl_sync(0xffffffffu, pf_end, slot);
+      const int levels = (int)((end - off) >> 8);
+      for (int l0 = 0; l0 < levels; l0 += klev) {
+        if (!gated && issued == cstages && !gate()) return;  // the next stage needs the consumers
+        mbar_wait(&cempty[cs], cph ^ 1);
+        if (lane == 0) {
+          unsigned char* st = chk0 + (size_t)cs * CL.bytes;
+          const int nk = min(klev, levels - l0);
+          const long long e0 = off + (long long)l0 * kPipeRows;
+          const uint32_t bv = (uint32_t)(nk * kPipeRows * (DICT ? 1 : sizeof(double)));
+          const uint32_t bc = (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
+          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
+          bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
+          bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
+        }
+        if (!gated) ++issued;
+        if (++cs == cstages) {
+          cs = 0;
+          cph ^= 1;
+        }
+      }
+      if (!gated && !gate()) return;  // first block's chunks are in flight
+    }
+    if (!gated) gate();
+    return;
+  }
+
+  if (warp == kConsumerWarps) {
+    // --------------------------------------------- producer of the block slots
+    // Every lane owns one copy stream of the slot and works out its own
     // source and size per block: lane 0 the row lengths, lanes 1..nwin the x
-    // windows, lanes 8.. the epilogue inputs.  (The whole warp used to compute
-    // all of it, and this warp's instruction stream, not HBM or the
-    // consumers, set the pace: ncu showed it never waiting on a free slot.)
+    // windows, lanes 8.. the epilogue inputs.  (One warp computing all of it,
+    // and the matrix stream too, set the kernel's pace: ncu showed the
+    // producer never waiting on a free slot while the consumers waited on
+    // data at half the HBM rate.)
+    int bs = 0;
+    uint32_t bph = 0;
+    long long pf_off = 0, pf_end = 0;
+    griddep_wait();
+    cta_sync2<kSellThreads>();
+    if (!go) return;
+    bool opp_ready = false;
     const int role_win = lane >= 1 && lane <= W.nwin ? lane - 1 : -1;
     const int role_in = lane >= 8 && lane < 8 + Epi::kInStaged ? lane - 8 : -1;
     int wmin_l = 0, wmax_l = 0;
@@ -218,7 +266,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
     const int row_lo = (int)A.row_lo, row_hi = (int)A.row_hi, ncols = (int)A.n_cols;
     for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
       const int slot = q & 31;
-      if (slot == 0) {  // entry offsets of blocks q .. q+31 of this CTA in one warp-wide load
+      if (slot == 0) {
         const long long b2 = (long long)blk + (long long)lane * gridDim.x;
         if (b2 < nblk) {
           pf_off = __ldg(A.soff + gb0 + b2);
@@ -228,33 +276,8 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
       const long long off = __shfl_sync(0xffffffffu, pf_off, slot);
       const long long end = __shfl_sync(0xffffffffu, pf_end, slot);
       const int levels = (int)((end - off) >> 8);
-      const int nch = (levels + klev - 1) / klev;
       const int r0 = row_lo + blk * kPipeRows;
       const int nr = min(kPipeRows, row_hi - r0);
-      auto issue_chunk = [&](int c) {
-        mbar_wait(&cempty[cs], cph ^ 1);
-        unsigned char* st = chk0 + (size_t)cs * CL.bytes;
-        const int nk = min(klev, levels - c * klev);
-        const long long e0 = off + (long long)c * klev * kPipeRows;
-        const uint32_t bv = (uint32_t)(nk * kPipeRows * (DICT ? 1 : sizeof(double)));
-        const uint32_t bc = (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
-        if (lane == 0) {
-          mbar_arrive_expect_tx(&cfull[cs], bv + bc);
-          bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
-          bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
-        }
-        if (++cs == cstages) {
-          cs = 0;
-          cph ^= 1;
-        }
-      };
-      int cfirst = 0;
-      if (!gated) {
-        cfirst = nch < cstages ? nch : cstages;
-        for (int c = 0; c < cfirst; ++c) issue_chunk(c);
-        issued = cfirst;
-        if (!gate()) return;
-      }
       bool fuse_in = true;
       if constexpr (EpiOpp<Epi>::value) {  // polled until seen once (it never goes back)
         if (!opp_ready) opp_ready = __shfl_sync(0xffffffffu, lane == 0 ? epi.ready() : false, 0);
@@ -296,7 +319,6 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
         bs = 0;
         bph ^= 1;
       }
-      for (int c = cfirst; c < nch; ++c) issue_chunk(c);
     }
     return;
   }
@@ -307,7 +329,7 @@ __global__ void __launch_bounds__(kPipeThreads, MINB) sell_pipe_kernel(SellView 
     go = epi.active();  // one gate decision per CTA
     if (!go && blockIdx.x == 0) epi.on_skip();
   }
-  cta_sync2<kPipeThreads>();
+  cta_sync2<kSellThreads>();
   if (!go) return;
   Epi e = epi;
   e.init();
