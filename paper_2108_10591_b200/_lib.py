@@ -38,7 +38,7 @@ EXPORTS = (
     "pbs_k_lincomb", "pbs_dot_batch_dev", "pbs_nccl_unique_id", "pbs_dist_init", "pbs_dist_destroy",
     "pbs_mat_set_partition", "pbs_stencil_to_csr", "pbs_dist_set_sm_limit", "pbs_dist_export",
     "pbs_dist_connect", "pbs_dist_connect_local", "pbs_solve_group", "pbs_spmv_group", "pbs_stencil_slab",
-    "pbs_csr_update",
+    "pbs_csr_update", "pbs_mat_layout",
 )
 TRANSPORTS = {"p2p": 0, "nccl": 1}
 DIST_BLOB_BYTES = 256
@@ -118,6 +118,7 @@ def load(build_if_missing: bool = True):
             "pbs_stencil_create": ([p, i32, i64, i32, p, p, pp], C.c_int),
             "pbs_mat_free": ([p], C.c_int),
             "pbs_mat_info": ([p, p, p, p, p], C.c_int),
+            "pbs_mat_layout": ([p, p], C.c_int),
             "pbs_spmv_dev": ([p, p, p, C.POINTER(i64)], C.c_int),
             "pbs_solve": ([p, i32, p, p, C.POINTER(Config), p, p, p, p, C.POINTER(Result)], C.c_int),
             "pbs_solve_dev": ([p, i32, p, p, C.POINTER(Config), p, p, p, p, C.POINTER(Result)], C.c_int),

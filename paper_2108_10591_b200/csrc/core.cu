@@ -1203,6 +1203,29 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   return PBS_OK;
 }
 
+PBS_EXPORT int pbs_mat_layout(pbs_mat* m, int64_t out[8]) {
+  if (!m || !out) return set_err(m ? m->ctx : nullptr, PBS_ERR_INVALID, "NULL argument");
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  out[6] = m->xwin.nwin;
+  out[7] = m->xwin.nwin ? m->xwin.total : m->xwin.band_s;
+  if (m->stencil) {
+    out[0] = 10;
+  } else if (m->sell_vi || m->sell_v) {
+    out[0] = m->sell_vi ? 4 : 3;
+    out[1] = m->sell_entries;
+    out[2] = m->sell_vi ? 3 : 10;
+    out[3] = 1;
+    out[4] = m->sell_ndict;
+    out[5] = m->sell_lmax;
+  } else {
+    out[0] = m->wc ? (m->xwin.band_s ? 2 : 1) : 0;
+    out[1] = m->nnz;
+    out[2] = m->wc ? 10 : 12;
+    out[3] = 8;
+  }
+  return PBS_OK;
+}
+
 PBS_EXPORT int pbs_mat_info(pbs_mat* m, int64_t* n_rows, int64_t* n_cols, int64_t* nnz, int32_t* is_stencil) {
   if (!m) return set_err(nullptr, PBS_ERR_INVALID, "mat is NULL");
   if (n_rows) *n_rows = m->n_rows;

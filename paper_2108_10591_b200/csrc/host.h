@@ -648,7 +648,8 @@ static void launch_pdl(Launcher& L, int engine, void (*kernel)(KArgs...), int gr
 // PBS_PLAIN_TPR=0 keeps the staged engine.
 template <class Epi>
 static bool csr_plain_tpr(const pbs_mat* m) {
-  static int on = env_int("PBS_PLAIN_TPR", 1, 0, 1);
+  static int on = env_int("PBS_PLAIN_TPR", 1, 0, 2);  // 2: even when the sliced-ELL form exists (A/B)
+  if (on == 1 && (m->sell_v || m->sell_vi)) return false;  // 3 or 10 B per entry, no row_ptr: streams less
   return on && (std::is_same<Epi, EpiStore>::value || std::is_same<Epi, EpiResid>::value) &&
          m->nnz <= 8 * m->n_rows;
 }

@@ -113,6 +113,18 @@ class DeviceMatrix:
                                             C.byref(bad)), self.ctx.handle)
         return bad.value
 
+    LAYOUTS = {0: "csr-gather", 1: "csr-window", 2: "csr-band", 3: "sell", 4: "sell-dict", 10: "stencil"}
+
+    def layout(self) -> dict:
+        """What the SpMV engines stream for this operator (pbs_mat_layout): the
+        layout name, entries and bytes per product, dictionary size."""
+        out = (C.c_int64 * 8)()
+        _lib.check(_lib.load().pbs_mat_layout(self.handle, out), self.ctx.handle)
+        return {"layout": self.LAYOUTS.get(int(out[0]), str(int(out[0]))), "entries": int(out[1]),
+                "bytes_per_entry": int(out[2]), "bytes_per_row": int(out[3]), "dict_entries": int(out[4]),
+                "max_row": int(out[5]), "x_windows": int(out[6]), "x_staged": int(out[7]),
+                "matrix_bytes": int(out[1]) * int(out[2]) + int(out[3]) * self.n_rows}
+
     def free(self):
         if self.handle:
             _lib.load().pbs_mat_free(self.handle)
