@@ -214,12 +214,13 @@ int pbs_mat_info(pbs_mat* mat, int64_t* n_rows, int64_t* n_cols, int64_t* nnz,
  * this is what bench.py's byte accounting and the layout tests read).
  * out[0] layout: 0 CSR order, int32 col_idx, x gathered; 1 CSR order, u16
  *        window-local columns; 2 CSR order, band mode; 3 sliced ELL, f64
- *        values; 4 sliced ELL, u8 dictionary values; 10 matrix-free stencil
+ *        values; 4 sliced ELL, u8 dictionary values; 5 sliced ELL, u8 (value,
+ *        relative column) pair dictionary; 10 matrix-free stencil
  * out[1] entries streamed per product (nonzeros + padding)
  * out[2] bytes per entry (value + column)
  * out[3] bytes per row besides (8: int64 row_ptr; 1: u8 row length)
- * out[4] dictionary entries in use (layout 4)
- * out[5] longest row of a 256-row block (layouts 3, 4)
+ * out[4] dictionary entries in use (layouts 4, 5)
+ * out[5] longest row of a 256-row block (layouts 3, 4, 5)
  * out[6] x windows per row block, out[7] staged x elements per row block */
 int pbs_mat_layout(pbs_mat* mat, int64_t out[8]);
 

@@ -97,6 +97,11 @@ def load(build_if_missing: bool = True):
     with _lock:
         if _lib is not None:
             return _lib
+        # The multi-GPU schedule runs compute, halo and reduction streams per
+        # partition; with the default 8 hardware queues streams alias and a
+        # flag wait on one holds back a kernel on another.  Only effective
+        # when set before the process creates its CUDA context.
+        os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
         path = lib_path()
         if not os.path.exists(path):
             if not build_if_missing:

@@ -53,6 +53,7 @@ MatSig mat_sig(const pbs_mat* m) {
   g.sell_len = m->sell_len;
   g.sell_vi = m->sell_vi;
   g.sell_dict = m->sell_dict;
+  g.sell_mode = m->sell_mode;
   g.sell_lmax = m->sell_lmax;
   memcpy(&g.xwin, &m->xwin, sizeof(XWin));
   memcpy(&g.sv, &m->sv, sizeof(StencilView));
@@ -593,6 +594,102 @@ __global__ void sell_fill_kernel(const long long* rp, const double* v, const uns
   }
 }
 
+// ---- pair dictionary: the distinct (value, staged column - row slot) pairs,
+// keyed (value-dictionary index << 32 | relative column) in a second hash set;
+// kPairPadKey is the padding entry's pair (value 0, relative column 0).
+constexpr unsigned long long kPairPadKey = 0xffffffff00000000ULL;
+
+__device__ __forceinline__ void pair_insert(unsigned long long key, unsigned long long* table, int* ctl) {
+  unsigned h = dict_hash(key);
+  for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
+    unsigned long long cur = *(volatile unsigned long long*)(table + h);
+    if (cur == key) return;
+    if (cur == kDictEmpty) {
+      cur = atomicCAS(table + h, kDictEmpty, key);
+      if (cur == kDictEmpty) {
+        if (atomicAdd(ctl, 1) >= kSellDict) ctl[1] = 1;
+        return;
+      }
+      if (cur == key) return;
+    }
+  }
+}
+
+__global__ void pair_insert_kernel(const long long* rp, const double* v, const unsigned short* wc, long long n_rows,
+                                   long long nblk, const long long* soff, const unsigned long long* vtable,
+                                   const unsigned char* vslot_idx, unsigned long long* table, int* ctl) {
+  for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+    if (*(volatile int*)(ctl + 1)) return;
+    const long long r = b * kPipeRows + threadIdx.x;
+    long long s = 0;
+    int len = 0;
+    if (r < n_rows) {
+      s = rp[r];
+      len = (int)(rp[r + 1] - s);
+    }
+    const int L = (int)((soff[b + 1] - soff[b]) / kPipeRows);
+    unsigned long long last = kDictEmpty;
+    for (int k = 0; k < len; ++k) {
+      const unsigned vi = dict_lookup(vtable, vslot_idx, v[s + k]);
+      const int rel = (int)wc[s + k] - (int)threadIdx.x;
+      const unsigned long long key = ((unsigned long long)vi << 32) | (unsigned)rel;
+      if (key != last) pair_insert(key, table, ctl);
+      last = key;
+    }
+    if (len < L) pair_insert(kPairPadKey, table, ctl);
+  }
+}
+
+__global__ void pair_compact_kernel(const unsigned long long* table, const double* vdict, SellPair* pairs,
+                                    unsigned char* slot_idx) {
+  int n = 0;
+  for (int h = 0; h < kDictSlots; ++h) {
+    const unsigned long long key = table[h];
+    if (key != kDictEmpty && n < kSellDict) {
+      SellPair p;
+      p.v = key == kPairPadKey ? 0.0 : vdict[(unsigned)(key >> 32)];
+      p.rel = key == kPairPadKey ? 0 : (int)(unsigned)key;
+      p.pad = 0;
+      pairs[n] = p;
+      slot_idx[h] = (unsigned char)n++;
+    }
+  }
+  for (; n < kSellDict; ++n) pairs[n] = SellPair{0.0, 0, 0};
+}
+
+__global__ void sell_fill_pair_kernel(const long long* rp, const double* v, const unsigned short* wc, long long n_rows,
+                                      long long nblk, const long long* soff, const unsigned long long* vtable,
+                                      const unsigned char* vslot_idx, const unsigned long long* table,
+                                      const unsigned char* slot_idx, unsigned char* spi, unsigned char* slen) {
+  for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
+    const long long r = b * kPipeRows + threadIdx.x;
+    long long s = 0;
+    int len = 0;
+    if (r < n_rows) {
+      s = rp[r];
+      len = (int)(rp[r + 1] - s);
+    }
+    const long long off = soff[b];
+    const int L = (int)((soff[b + 1] - off) / kPipeRows);
+    for (int k = 0; k < L; ++k) {
+      unsigned long long key = kPairPadKey;
+      if (k < len) {
+        const unsigned vi = dict_lookup(vtable, vslot_idx, v[s + k]);
+        key = ((unsigned long long)vi << 32) | (unsigned)((int)wc[s + k] - (int)threadIdx.x);
+      }
+      unsigned h = dict_hash(key);
+      unsigned char idx = 0;
+      for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1))
+        if (__ldg(table + h) == key) {
+          idx = __ldg(slot_idx + h);
+          break;
+        }
+      spi[off + (long long)k * kPipeRows + threadIdx.x] = idx;
+    }
+    slen[b * kPipeRows + threadIdx.x] = (unsigned char)len;
+  }
+}
+
 static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
   pool_free(ctx, m->sell_v);
   pool_free(ctx, m->sell_c);
@@ -604,6 +701,7 @@ static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
   m->sell_vi = nullptr;
   m->sell_dict = nullptr;
   m->sell_ndict = 0;
+  m->sell_mode = 0;
   m->sell_v = nullptr;
   m->sell_c = nullptr;
   m->sell_off = nullptr;
@@ -661,19 +759,59 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
     pool_free(ctx, ctl);
   }
   const bool dict = hctl[1] == 0 && hctl[0] <= kSellDict;
+  const int grid = (int)std::min<long long>(nblk, ctx->sms * 8);
+  CK(pool_alloc(ctx, &m->sell_len, (size_t)nblk * kPipeRows));
+  bool pairs = false;
   if (dict) {
-    CK(pool_alloc(ctx, &m->sell_dict, sizeof(double) * kSellDict));
+    CK(pool_alloc(ctx, &m->sell_dict, sizeof(SellPair) * kSellDict));  // doubles, or pairs
     CK(pool_alloc(ctx, &m->sell_vi, (size_t)entries));
     dict_compact_kernel<<<1, 1, 0, s>>>(table, m->sell_dict, slot_idx);
     m->sell_ndict = hctl[0];
+    // pair dictionary (PBS_SELL_PAIR=0: keep the u16 column stream)
+    if (env_int("PBS_SELL_PAIR", 1, 0, 1)) {
+      unsigned long long* ptable = nullptr;
+      unsigned char* pslot = nullptr;
+      SellPair* pdict = nullptr;
+      int* ctl = nullptr;
+      int pctl[2] = {0, 1};
+      CK(pool_alloc(ctx, &ptable, sizeof(unsigned long long) * kDictSlots));
+      CK(pool_alloc(ctx, &pslot, kDictSlots));
+      CK(pool_alloc(ctx, &pdict, sizeof(SellPair) * kSellDict));
+      CK(pool_alloc(ctx, &ctl, sizeof(int) * 2));
+      std::vector<unsigned long long> empty(kDictSlots, kDictEmpty);
+      CK(cudaMemcpyAsync(ptable, empty.data(), sizeof(unsigned long long) * kDictSlots, cudaMemcpyHostToDevice, s));
+      CK(cudaMemsetAsync(pslot, 0, kDictSlots, s));
+      CK(cudaMemsetAsync(ctl, 0, sizeof(int) * 2, s));
+      pair_insert_kernel<<<grid, kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk, m->sell_off, table, slot_idx,
+                                                    ptable, ctl);
+      CK(cudaMemcpyAsync(pctl, ctl, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      pool_free(ctx, ctl);
+      pairs = pctl[1] == 0 && pctl[0] <= kSellDict;
+      if (pairs) {
+        pair_compact_kernel<<<1, 1, 0, s>>>(ptable, m->sell_dict, pdict, pslot);
+        sell_fill_pair_kernel<<<grid, kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk, m->sell_off, table,
+                                                         slot_idx, ptable, pslot, m->sell_vi, m->sell_len);
+        pool_free(ctx, m->sell_dict);
+        m->sell_dict = reinterpret_cast<double*>(pdict);
+        m->sell_ndict = pctl[0];
+        m->sell_mode = kSellPairs;
+      } else {
+        pool_free(ctx, pdict);
+      }
+      pool_free(ctx, ptable);
+      pool_free(ctx, pslot);
+    }
+    if (!pairs) m->sell_mode = kSellDictV;
   } else {
     CK(pool_alloc(ctx, &m->sell_v, sizeof(double) * entries));
+    m->sell_mode = kSellF64;
   }
-  CK(pool_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
-  CK(pool_alloc(ctx, &m->sell_len, (size_t)nblk * kPipeRows));
-  sell_fill_kernel<<<(int)std::min<long long>(nblk, ctx->sms * 8), kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk,
-                                                                                     m->sell_off, m->sell_v, m->sell_c, m->sell_len,
-                                                                                     dict ? table : nullptr, slot_idx, m->sell_vi);
+  if (!pairs) {
+    CK(pool_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
+    sell_fill_kernel<<<grid, kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk, m->sell_off, m->sell_v, m->sell_c,
+                                                m->sell_len, dict ? table : nullptr, slot_idx, m->sell_vi);
+  }
   CK(cudaGetLastError());
   pool_free(ctx, table);
   pool_free(ctx, slot_idx);
@@ -1211,9 +1349,9 @@ PBS_EXPORT int pbs_mat_layout(pbs_mat* m, int64_t out[8]) {
   if (m->stencil) {
     out[0] = 10;
   } else if (m->sell_vi || m->sell_v) {
-    out[0] = m->sell_vi ? 4 : 3;
+    out[0] = m->sell_mode == kSellPairs ? 5 : (m->sell_vi ? 4 : 3);
     out[1] = m->sell_entries;
-    out[2] = m->sell_vi ? 3 : 10;
+    out[2] = m->sell_mode == kSellPairs ? 1 : (m->sell_vi ? 3 : 10);
     out[3] = 1;
     out[4] = m->sell_ndict;
     out[5] = m->sell_lmax;

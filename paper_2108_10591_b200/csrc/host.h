@@ -76,6 +76,7 @@ struct MatSig {
   long long stencil;
   const void *rp, *ci, *v, *wc;
   const void *sell_v, *sell_c, *sell_off, *sell_len, *sell_vi, *sell_dict;
+  long long sell_mode;
   long long sell_lmax;
   XWin xwin;
   StencilView sv;
@@ -117,6 +118,7 @@ struct pbs_mat {
   unsigned char* sell_vi = nullptr;
   double* sell_dict = nullptr;
   int sell_ndict = 0;
+  int sell_mode = 0;  // kSellF64 / kSellDictV / kSellPairs (sell_dict then holds SellPairs, sell_c is null)
   int sell_lmax = 0;          // most levels (longest row) in one block
   long long sell_entries = 0;
   StencilView sv{};
@@ -313,7 +315,7 @@ static inline int pipe_slots_cap() {
   return v;
 }
 static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
-  static int v = env_int("PBS_SELL_SLOTS", 2, 2, kMaxStages);
+  static int v = env_int("PBS_SELL_SLOTS", 3, 2, kMaxStages);
   return v;
 }
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
@@ -403,12 +405,14 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
 // stages klev levels of the block (one chunk per block when its longest row
 // has at most kSellLevMax nonzeros: 7-point stencils).
 template <class Epi>
-static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, bool dict, int* bslots, int* cstages, size_t* smem,
+static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, int mode, int* bslots, int* cstages, size_t* smem,
                        int* ctas, int* klev) {
   static int lev_cap = env_int("PBS_SELL_LEV", kSellLevMax, 1, kSellLevMax);
-  int kl = lmax < lev_cap ? lmax : lev_cap;
+  static int lev_cap_pair = env_int("PBS_SELL_LEV_PAIR", kSellLevMaxPair, 1, kSellLevMaxPair);
+  const int cap = mode == kSellPairs ? lev_cap_pair : lev_cap;
+  int kl = lmax < cap ? lmax : cap;
   if (kl < 1) kl = 1;
-  const SellChunkLayout CL(kl, dict ? 1 : 8);
+  const SellChunkLayout CL(kl, mode);
   const SellBlockLayout BL(W.total, Epi::kInStaged);
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
@@ -418,8 +422,10 @@ static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, bool dict, int* bs
   int n = 0, c = 0, xc = 0;
   size_t best = 0;
   for (int cc = pipe_ctas_per_sm(); cc >= 1; --cc) {
-    size_t budget = (size_t)per_sm / cc - 1024 - 2048;
-    if (budget > (size_t)optin - 2048) budget = (size_t)optin - 2048;
+    // less the 1 KiB the runtime reserves per CTA and the kernel's static smem (the dictionary)
+    const size_t fixed = 1024 + 512 + (mode == kSellPairs ? 4096 : 2048);
+    size_t budget = (size_t)per_sm / cc - fixed;
+    if (budget > (size_t)optin - fixed) budget = (size_t)optin - fixed;
     if (budget <= kPipeBarrierBytes) continue;
     budget -= kPipeBarrierBytes;
     int nn = (int)(budget / (BL.bytes + CL.bytes));
@@ -442,8 +448,13 @@ static int sell_config(pbs_ctx* ctx, const XWin& W, int lmax, bool dict, int* bs
   *cstages = n + xc;
   *klev = kl;
   *smem = kPipeBarrierBytes + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
-  const void* k = dict ? (c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, true> : (const void*)sell_pipe_kernel<Epi, 2, true>)
-                       : (c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, false> : (const void*)sell_pipe_kernel<Epi, 2, false>);
+  const void* k;
+  if (mode == kSellPairs)
+    k = c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, kSellPairs> : (const void*)sell_pipe_kernel<Epi, 2, kSellPairs>;
+  else if (mode == kSellDictV)
+    k = c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, kSellDictV> : (const void*)sell_pipe_kernel<Epi, 2, kSellDictV>;
+  else
+    k = c == 1 ? (const void*)sell_pipe_kernel<Epi, 1, kSellF64> : (const void*)sell_pipe_kernel<Epi, 2, kSellF64>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -681,11 +692,11 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
   } else if (!m->stencil && (m->sell_v || m->sell_vi) && (lo % kPipeRows) == 0) {
     // sliced-ELL form (sell.cuh): row blocks counted from row 0, like the
     // window-local columns
-    SellView A{m->sell_v, m->sell_vi, m->sell_dict, m->sell_c, m->sell_len, m->sell_off, lo, hi, m->n_cols};
-    const bool dict = m->sell_vi != nullptr;
+    SellView A{m->sell_v, m->sell_vi, (const void*)m->sell_dict, m->sell_c, m->sell_len, m->sell_off, lo, hi, m->n_cols};
+    const int mode = m->sell_mode;
     int bslots, cstages, ctas, klev;
     size_t smem;
-    int rc = sell_config<Epi>(L.ctx, m->xwin, m->sell_lmax, dict, &bslots, &cstages, &smem, &ctas, &klev);
+    int rc = sell_config<Epi>(L.ctx, m->xwin, m->sell_lmax, mode, &bslots, &cstages, &smem, &ctas, &klev);
     if (rc) {
       L.err = rc;
       return 0;
@@ -696,10 +707,12 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
 #define PBS_SELL(MB, D)                                                                                      \
   launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, MB, D>, grid, kSellThreads, smem, A, x, epi, m->xwin, bslots, \
              cstages, klev)
-    if (dict && ctas == 1) PBS_SELL(1, true);
-    else if (dict) PBS_SELL(2, true);
-    else if (ctas == 1) PBS_SELL(1, false);
-    else PBS_SELL(2, false);
+    if (mode == kSellPairs && ctas == 1) PBS_SELL(1, kSellPairs);
+    else if (mode == kSellPairs) PBS_SELL(2, kSellPairs);
+    else if (mode == kSellDictV && ctas == 1) PBS_SELL(1, kSellDictV);
+    else if (mode == kSellDictV) PBS_SELL(2, kSellDictV);
+    else if (ctas == 1) PBS_SELL(1, kSellF64);
+    else PBS_SELL(2, kSellF64);
 #undef PBS_SELL
     if (L.err) return 0;
   } else if (!m->stencil) {

@@ -29,6 +29,12 @@
 // enough for a third block slot.  The f64 looked up is bit for bit the
 // uploaded value, so nothing changes in the arithmetic.
 //
+// Pair dictionary (MODE 2): when also the (value, column - row) pairs are
+// few — every interior row of a constant-coefficient stencil repeats the
+// same 7 or 27 — one u8 per entry indexes a dictionary of (value, staged
+// offset relative to the row's own slot position): 1 byte per nonzero, and
+// one 16-byte shared-memory load gives both the value and the x address.
+//
 // Used for window-mode operators whose padding is small (stencil-like row
 // lengths: configs 1, 2, 4, 5); band mode, gathered x and ragged matrices
 // stay on csr_pipe_kernel.
@@ -39,13 +45,24 @@ namespace pbs {
 
 constexpr int kSellMaxLen = 255;        // longest row the u8 row lengths can hold
 constexpr int kSellLevMax = 8;          // levels per chunk stage, at most (20 KiB)
+constexpr int kSellLevMaxPair = 32;     // pair dictionary: 256 B per level
 constexpr int kSellDict = 256;          // dictionary entries (u8 value indices)
 constexpr int kSellThreads = kPipeRows + 64;  // + two producer warps (block slots, matrix stream)
 
+// value stream of the layout: f64 values, u8 value-dictionary indices (+ the
+// u16 column stream either way), or u8 (value, relative column) pair indices
+enum { kSellF64 = 0, kSellDictV = 1, kSellPairs = 2 };
+
+struct SellPair {
+  double v;
+  int rel;  // staged x index of the entry minus the row's index in its block
+  int pad;
+};
+
 struct SellView {
   const double* sv;           // values, level-major per row block (null with a dictionary)
-  const unsigned char* svi;   // DICT: index of each value in dict
-  const double* dict;         // DICT: kSellDict distinct values
+  const unsigned char* svi;   // dictionary modes: index of each entry's value / pair
+  const void* dict;           // kSellDict doubles (kSellDictV) or SellPairs (kSellPairs)
   const unsigned short* sc;   // window-local columns (0 in padding entries)
   const unsigned char* slen;  // nonzeros per row, 256 per row block (0 past the last row)
   const long long* soff;      // entry offset of each 256-row block (multiples of 256), nblk + 1
@@ -73,9 +90,9 @@ struct SellBlockLayout {
 // indices), then of columns
 struct SellChunkLayout {
   size_t ci, bytes;
-  __host__ __device__ SellChunkLayout(int klev, int vb) {
-    ci = (size_t)vb * kPipeRows * (size_t)klev;
-    bytes = ci + sizeof(unsigned short) * kPipeRows * (size_t)klev;
+  __host__ __device__ SellChunkLayout(int klev, int mode) {
+    ci = (size_t)(mode == kSellF64 ? 8 : 1) * kPipeRows * (size_t)klev;
+    bytes = ci + (mode == kSellPairs ? 0 : sizeof(unsigned short) * kPipeRows * (size_t)klev);
   }
 };
 
@@ -91,25 +108,45 @@ __device__ __forceinline__ double sell_add_if(double acc, double p, int k, int r
 // N levels of one row, G staged products in flight: columns, values and x
 // loads are issued ahead of the rounded product / rounded add chain; rem =
 // the row's nonzeros left at this chunk's first level
-template <int N, int G, bool DICT>
+template <int N, int G, int MODE>
 __device__ __forceinline__ double sell_levels(const void* __restrict__ vsv, const unsigned short* __restrict__ cs,
-                                              const double* __restrict__ xw, const double* __restrict__ dict,
-                                              double acc, int rem) {
+                                              const double* __restrict__ xw, const void* __restrict__ dictv,
+                                              int t, double acc, int rem) {
   const double* vs = reinterpret_cast<const double*>(vsv);
   const unsigned char* vi = reinterpret_cast<const unsigned char*>(vsv);
+  const double* dict = reinterpret_cast<const double*>(dictv);
+  const int4* pairs = reinterpret_cast<const int4*>(dictv);
+  const double* xt = xw + t;
 #pragma unroll
   for (int k0 = 0; k0 < N; k0 += G) {
-    unsigned c[G];
     double v[G], xv[G];
+    if constexpr (MODE == kSellPairs) {
+      unsigned pi[G];
+      int4 e[G];
 #pragma unroll
-    for (int u = 0; u < G; ++u)
-      if (k0 + u < N) c[u] = cs[(k0 + u) * kPipeRows];
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) pi[u] = vi[(k0 + u) * kPipeRows];
 #pragma unroll
-    for (int u = 0; u < G; ++u)
-      if (k0 + u < N) v[u] = DICT ? dict[vi[(k0 + u) * kPipeRows]] : vs[(k0 + u) * kPipeRows];
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) e[u] = pairs[pi[u]];  // one 16-byte load: value and relative x index
 #pragma unroll
-    for (int u = 0; u < G; ++u)
-      if (k0 + u < N) xv[u] = xw[c[u]];
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) {
+          v[u] = __hiloint2double(e[u].y, e[u].x);
+          xv[u] = xt[e[u].z];
+        }
+    } else {
+      unsigned c[G];
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) c[u] = cs[(k0 + u) * kPipeRows];
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) v[u] = MODE == kSellDictV ? dict[vi[(k0 + u) * kPipeRows]] : vs[(k0 + u) * kPipeRows];
+#pragma unroll
+      for (int u = 0; u < G; ++u)
+        if (k0 + u < N) xv[u] = xw[c[u]];
+    }
 #pragma unroll
     for (int u = 0; u < G; ++u)
       if (k0 + u < N) acc = sell_add_if(acc, mul(v[u], xv[u]), k0 + u, rem);
@@ -117,19 +154,35 @@ __device__ __forceinline__ double sell_levels(const void* __restrict__ vsv, cons
   return acc;
 }
 
-template <int G, bool DICT>
-__device__ __forceinline__ double sell_chunk(int nk, const void* vs, const unsigned short* cs, const double* xw,
-                                             const double* dict, double acc, int rem) {
+// nk <= 8 levels starting at vs / cs (already offset to the thread's column)
+template <int G, int MODE>
+__device__ __forceinline__ double sell_chunk8(int nk, const unsigned char* vs, const unsigned short* cs,
+                                              const double* xw, const void* dict, int t, double acc, int rem) {
   switch (nk) {  // CTA-uniform
-    case 8: return sell_levels<8, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 7: return sell_levels<7, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 6: return sell_levels<6, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 5: return sell_levels<5, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 4: return sell_levels<4, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 3: return sell_levels<3, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 2: return sell_levels<2, G, DICT>(vs, cs, xw, dict, acc, rem);
-    case 1: return sell_levels<1, G, DICT>(vs, cs, xw, dict, acc, rem);
+    case 8: return sell_levels<8, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 7: return sell_levels<7, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 6: return sell_levels<6, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 5: return sell_levels<5, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 4: return sell_levels<4, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 3: return sell_levels<3, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 2: return sell_levels<2, G, MODE>(vs, cs, xw, dict, t, acc, rem);
+    case 1: return sell_levels<1, G, MODE>(vs, cs, xw, dict, t, acc, rem);
     default: return acc;
+  }
+}
+
+// a chunk stage of nk levels (up to klev: 8, or 32 with the pair dictionary)
+template <int G, int MODE>
+__device__ __forceinline__ double sell_chunk(int nk, const unsigned char* vs, const unsigned short* cs,
+                                             const double* xw, const void* dict, int t, double acc, int rem) {
+  constexpr size_t vb = MODE == kSellF64 ? sizeof(double) : 1;
+  if constexpr (MODE == kSellPairs) {
+    int k0 = 0;
+    for (; k0 + 8 <= nk; k0 += 8)
+      acc = sell_levels<8, G, MODE>(vs + (size_t)k0 * kPipeRows * vb, cs, xw, dict, t, acc, rem - k0);
+    return sell_chunk8<G, MODE>(nk - k0, vs + (size_t)k0 * kPipeRows * vb, cs, xw, dict, t, acc, rem - k0);
+  } else {
+    return sell_chunk8<G, MODE>(nk, vs, cs, xw, dict, t, acc, rem);
   }
 }
 
@@ -137,21 +190,29 @@ __device__ __forceinline__ double sell_chunk(int nk, const void* vs, const unsig
 // producer streams the first block's matrix chunks before griddep_wait; one
 // gate decision per CTA; consumers release the next grid once their rows are
 // written).  MINB: resident CTAs per SM the instantiation is compiled for.
-template <class Epi, int MINB = 2, bool DICT = false>
+template <class Epi, int MINB = 2, int MODE = kSellF64>
 __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView A, const double* __restrict__ x,
                                                                     Epi epi, XWin W, int bslots, int cstages,
                                                                     int klev) {
   __shared__ int go;
-  __shared__ double dict_s[DICT ? kSellDict : 1];
+  __shared__ __align__(16) double dict_s[MODE == kSellPairs ? 2 * kSellDict : (MODE == kSellDictV ? kSellDict : 2)];
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* cfull = reinterpret_cast<uint64_t*>(smem);
   uint64_t* cempty = cfull + kMaxStages;
   uint64_t* bfull = cempty + kMaxStages;
   uint64_t* bempty = bfull + kMaxStages;
   const SellBlockLayout BL(W.total, Epi::kInStaged);
-  const SellChunkLayout CL(klev, DICT ? 1 : 8);
+  const SellChunkLayout CL(klev, MODE);
   // the dictionary belongs to the operator: read ahead of the grid dependency
-  if (DICT && threadIdx.x < kSellDict) dict_s[threadIdx.x] = __ldg(A.dict + threadIdx.x);
+  if (MODE != kSellF64 && threadIdx.x < kSellDict) {
+    const double* dg = reinterpret_cast<const double*>(A.dict);
+    if (MODE == kSellPairs) {
+      dict_s[2 * threadIdx.x] = __ldg(dg + 2 * threadIdx.x);
+      dict_s[2 * threadIdx.x + 1] = __ldg(dg + 2 * threadIdx.x + 1);
+    } else {
+      dict_s[threadIdx.x] = __ldg(dg + threadIdx.x);
+    }
+  }
   unsigned char* blk0 = smem + kPipeBarrierBytes;
   unsigned char* chk0 = blk0 + (size_t)bslots * BL.bytes;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -207,11 +268,11 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
           unsigned char* st = chk0 + (size_t)cs * CL.bytes;
           const int nk = min(klev, levels - l0);
           const long long e0 = off + (long long)l0 * kPipeRows;
-          const uint32_t bv = (uint32_t)(nk * kPipeRows * (DICT ? 1 : sizeof(double)));
-          const uint32_t bc = (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
+          const uint32_t bv = (uint32_t)(nk * kPipeRows * (MODE == kSellF64 ? sizeof(double) : 1));
+          const uint32_t bc = MODE == kSellPairs ? 0u : (uint32_t)(nk * kPipeRows * sizeof(unsigned short));
           mbar_arrive_expect_tx(&cfull[cs], bv + bc);
-          bulk_g2s(st, DICT ? (const void*)(A.svi + e0) : (const void*)(A.sv + e0), bv, &cfull[cs]);
-          bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
+          bulk_g2s(st, MODE == kSellF64 ? (const void*)(A.sv + e0) : (const void*)(A.svi + e0), bv, &cfull[cs]);
+          if (MODE != kSellPairs) bulk_g2s(st + CL.ci, A.sc + e0, bc, &cfull[cs]);
         }
         if (!gated) ++issued;
         if (++cs == cstages) {
@@ -356,8 +417,8 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
       mbar_wait(&cfull[cs], cph);
       const unsigned char* st = chk0 + (size_t)cs * CL.bytes;
       const int nk = min(klev, levels - l0);
-      acc = sell_chunk<G, DICT>(nk, st + (size_t)t * (DICT ? 1 : sizeof(double)),
-                                reinterpret_cast<const unsigned short*>(st + CL.ci) + t, xw, dict_s, acc, len - l0);
+      acc = sell_chunk<G, MODE>(nk, st + (size_t)t * (MODE == kSellF64 ? sizeof(double) : 1),
+                                reinterpret_cast<const unsigned short*>(st + CL.ci) + t, xw, dict_s, t, acc, len - l0);
       __syncwarp();
       if (lane == 0) mbar_arrive(&cempty[cs]);
       if (++cs == cstages) {

@@ -113,7 +113,7 @@ class DeviceMatrix:
                                             C.byref(bad)), self.ctx.handle)
         return bad.value
 
-    LAYOUTS = {0: "csr-gather", 1: "csr-window", 2: "csr-band", 3: "sell", 4: "sell-dict", 10: "stencil"}
+    LAYOUTS = {0: "csr-gather", 1: "csr-window", 2: "csr-band", 3: "sell", 4: "sell-dict", 5: "sell-pairs", 10: "stencil"}
 
     def layout(self) -> dict:
         """What the SpMV engines stream for this operator (pbs_mat_layout): the

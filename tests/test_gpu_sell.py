@@ -141,6 +141,44 @@ def test_sell_signed_zeros_empty_rows_and_nonfinite(pb):
     dm.free()
 
 
+@pytest.mark.parametrize("cfg,k", [("c2", 20), ("c4", 14), ("c1", 70)])
+def test_sell_pair_dictionary_on_stencil_csr(pb, cfg, k):
+    """A constant-coefficient stencil's CSR repeats the same (value, column -
+    row) pairs in every interior row: one u8 per nonzero.  Blocks whose x
+    windows are clamped at the matrix start hold other relative columns; the
+    row sums stay the reference's, bit for bit, signed zeros and non-finite x
+    included."""
+    from paper_2108_10591_b200 import problems
+
+    spec = problems.config_stencil(cfg, k=k)
+    rp, ci, v = problems.stencil_csr(spec)
+    n = spec.n
+    dm = _upload(rp, ci, v, PBS_PLAIN_TPR=0)
+    lay = dm.layout()
+    assert lay["layout"] == "sell-pairs", lay
+    assert lay["bytes_per_entry"] == 1 and spec.npts <= lay["dict_entries"] <= 256
+    rng = np.random.default_rng(k)
+    x = rng.standard_normal(n)
+    x[::5] = 0.0
+    x[2::9] = -0.0
+    assert np.array_equal(_bits(_spmv_dev(dm, x)), _bits(orc.spmv(rp, ci, v, x)))
+    xz = -np.zeros(n)
+    assert np.array_equal(_bits(_spmv_dev(dm, xz)), _bits(orc.spmv(rp, ci, v, xz)))
+    xi = x.copy()
+    xi[n // 3] = np.inf
+    refi = orc.spmv(rp, ci, v, xi)
+    first = int(np.flatnonzero(~np.isfinite(refi))[0])
+    got = _spmv_dev(dm, xi, expect_bad=first)
+    assert np.array_equal(np.isnan(got), np.isnan(refi))
+    ok = np.isfinite(refi)
+    assert np.array_equal(_bits(got[ok]), _bits(refi[ok]))
+    two = _upload(rp, ci, v, PBS_SELL_PAIR=0, PBS_PLAIN_TPR=0)
+    assert two.layout()["layout"] == "sell-dict"
+    assert np.array_equal(_bits(_spmv_dev(two, x)), _bits(orc.spmv(rp, ci, v, x)))
+    dm.free()
+    two.free()
+
+
 def test_sell_refused_for_ragged_rows(pb):
     """Row lengths uniform in [5, 30] (config 3's shape) would pad each block
     to its longest row: the layout is refused and CSR order kept."""
@@ -158,7 +196,7 @@ def test_sell_refused_for_ragged_rows(pb):
     forced.free()
 
 
-@pytest.mark.parametrize("env", [{}, {"PBS_SELL_DICT": 0}, {"PBS_SELL": 0}])
+@pytest.mark.parametrize("env", [{}, {"PBS_SELL_PAIR": 0}, {"PBS_SELL_DICT": 0}, {"PBS_SELL": 0}])
 def test_sell_solve_equals_csr_order_solve(pb, env):
     """The same system solved through each layout: identical histories in
     plan order (bitwise the reference's) and on the fast path."""
@@ -169,7 +207,8 @@ def test_sell_solve_equals_csr_order_solve(pb, env):
     b = orc.spmv(rp, ci, v, np.ones(spec.n))
     ref = orc.solve(rp, ci, v, b, tol=1e-10, max_iters=500, workers=3)
     dm = _upload(rp, ci, v, **env)
-    want = {(): "sell-dict", ("PBS_SELL_DICT",): "sell", ("PBS_SELL",): "csr-window"}[tuple(env)]
+    want = {(): "sell-pairs", ("PBS_SELL_PAIR",): "sell-dict", ("PBS_SELL_DICT",): "sell",
+            ("PBS_SELL",): "csr-window"}[tuple(env)]
     assert dm.layout()["layout"] == want
     out = pb.solve(dm, b, config=pb.SolverConfig(tol=1e-10, max_iters=500),
                    engine=pb.DeviceEngine(reduce="plan", workers=3))
