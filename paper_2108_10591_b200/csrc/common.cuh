@@ -198,6 +198,9 @@ __device__ __forceinline__ Ddbl two_sum(double a, double b) {
 
 // accumulate one product a*b into (p, s)
 __device__ __forceinline__ Ddbl dot2_step(Ddbl acc, double a, double b) {
+#ifdef PBS_PLAIN_DOT  // measurement-only build (tools/build_variants.py): what the compensation costs
+  return Ddbl{add(acc.hi, mul(a, b)), acc.lo};
+#endif
   const double h = mul(a, b);
   const double r = __fma_rn(a, b, -h);
   const Ddbl t = two_sum(acc.hi, h);

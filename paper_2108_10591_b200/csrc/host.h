@@ -318,6 +318,10 @@ static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
   static int v = env_int("PBS_SELL_SLOTS", 3, 2, kMaxStages);
   return v;
 }
+static inline int sell_prefetch() {  // L2 prefetch distance of the block slots' streams, in blocks (0: off)
+  static int v = env_int("PBS_SELL_PF", 2, 0, 8);
+  return v;
+}
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
   static int v = env_int("PBS_PIPE_XCHUNK", 0, 0, 4);
   return v;
@@ -706,7 +710,7 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     grid = L.cap_grid(nb < cap ? nb : cap);
 #define PBS_SELL(MB, D)                                                                                      \
   launch_pdl(L, kPdlCsrPipe, sell_pipe_kernel<Epi, MB, D>, grid, kSellThreads, smem, A, x, epi, m->xwin, bslots, \
-             cstages, klev)
+             cstages, klev, sell_prefetch())
     if (mode == kSellPairs && ctas == 1) PBS_SELL(1, kSellPairs);
     else if (mode == kSellPairs) PBS_SELL(2, kSellPairs);
     else if (mode == kSellDictV && ctas == 1) PBS_SELL(1, kSellDictV);

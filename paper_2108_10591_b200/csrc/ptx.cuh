@@ -47,6 +47,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// ask L2 for [src, src + bytes) (bytes a multiple of 16, src 16-byte aligned); no completion to wait for
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // Programmatic dependent launch.  wait: block until the grids this one depends
 // on have completed and their writes are visible (a no-op for a kernel
 // launched without the programmatic attribute).  launch_dependents: this CTA

@@ -186,6 +186,63 @@ __device__ __forceinline__ double sell_chunk(int nk, const unsigned char* vs, co
   }
 }
 
+// One lane's copy stream of a block slot: lane 0 the row lengths, lanes
+// 1..nwin the x windows, lanes 8.. the epilogue inputs.
+struct SellLaneStream {
+  int role_win, role_in;
+  int wmin, wmax;
+  uint32_t dst;       // offset in the block slot
+  const double* base;
+  template <class Epi>
+  __device__ void init(int lane, const XWin& W, const SellBlockLayout& BL, const Epi& epi, const double* x) {
+    role_win = lane >= 1 && lane <= W.nwin ? lane - 1 : -1;
+    role_in = lane >= 8 && lane < 8 + Epi::kInStaged ? lane - 8 : -1;
+    wmin = wmax = 0;
+    dst = (uint32_t)BL.len;
+    base = nullptr;
+    if (role_win >= 0) {
+      int so = 0;
+#pragma unroll
+      for (int cc = 0; cc < kMaxWin; ++cc) {
+        if (cc == role_win) {
+          wmin = W.wmin[cc];
+          wmax = W.wmax[cc];
+          dst = (uint32_t)(BL.xw + (size_t)so * sizeof(double));
+        }
+        so += cc < W.nwin ? W.cap[cc] : 0;
+      }
+      base = x;
+    } else if (role_in >= 0) {
+      dst = (uint32_t)(BL.ein + (size_t)role_in * kPipeRows * sizeof(double));
+#pragma unroll
+      for (int k = 0; k < Epi::kInStaged; ++k)
+        if (k == role_in) base = epi.in[k];
+    }
+  }
+  // source and size of this lane's copy for the block of rows [r0, r0 + nr)
+  __device__ __forceinline__ uint32_t stream(int lane, int r0, int nr, int ncols, const unsigned char* slen_blk,
+                                             bool inputs, const void** src) const {
+    if (lane == 0) {
+      *src = slen_blk;
+      return kPipeRows;
+    }
+    if (role_win >= 0) {
+      int lo = r0 + wmin, hi = r0 + nr + wmax;
+      if (lo < 0) lo = 0;
+      if (hi > ncols) hi = ncols;
+      if (hi <= lo) return 0;
+      const int loa = lo & ~1, hia = (hi + 1) & ~1;
+      *src = base + loa;
+      return (uint32_t)((hia - loa) * sizeof(double));
+    }
+    if (role_in >= 0 && inputs) {
+      *src = base + r0;
+      return (uint32_t)(((nr + 1) & ~1) * sizeof(double));
+    }
+    return 0;
+  }
+};
+
 // Same launch protocol as csr_pipe_kernel (programmatic dependent launch: the
 // producer streams the first block's matrix chunks before griddep_wait; one
 // gate decision per CTA; consumers release the next grid once their rows are
@@ -193,7 +250,7 @@ __device__ __forceinline__ double sell_chunk(int nk, const unsigned char* vs, co
 template <class Epi, int MINB = 2, int MODE = kSellF64>
 __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView A, const double* __restrict__ x,
                                                                     Epi epi, XWin W, int bslots, int cstages,
-                                                                    int klev) {
+                                                                    int klev, int pf) {
   __shared__ int go;
   __shared__ __align__(16) double dict_s[MODE == kSellPairs ? 2 * kSellDict : (MODE == kSellDictV ? kSellDict : 2)];
   extern __shared__ __align__(128) unsigned char smem[];
@@ -249,6 +306,8 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
       for (int s2 = 0; s2 < issued; ++s2) mbar_wait(&cfull[s2], 0);  // let the early copies land
       return false;
     };
+    SellLaneStream LS;
+    LS.init(lane, W, BL, epi, x);
     for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
       const int slot = q & 31;
       if (slot == 0) {  // entry offsets of blocks q .. q+31 of this CTA in one warp-wide load
@@ -281,6 +340,22 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
         }
       }
       if (!gated && !gate()) return;  // first block's chunks are in flight
+      // This warp has slack (one or two copies per block): it asks L2 for what
+      // the slot producer will copy for the block `pf` steps ahead, so that
+      // copy finds its lines in L2 instead of paying the DRAM latency inside
+      // the slot's turnaround.  (L2 is the coherence point: a line prefetched
+      // before its producer kernel's last write is updated in place.)
+      if (pf > 0) {
+        const long long bp = (long long)blk + (long long)pf * gridDim.x;
+        if (bp < nblk) {
+          const int r0p = (int)A.row_lo + (int)bp * kPipeRows;
+          const int nrp = min(kPipeRows, (int)A.row_hi - r0p);
+          const void* srcp = nullptr;
+          const uint32_t bp_bytes =
+              LS.stream(lane, r0p, nrp, (int)A.n_cols, A.slen + (gb0 + bp) * kPipeRows, true, &srcp);
+          if (bp_bytes) bulk_prefetch_l2(srcp, bp_bytes);
+        }
+      }
     }
     if (!gated) gate();
     return;
@@ -301,29 +376,8 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
     cta_sync2<kSellThreads>();
     if (!go) return;
     bool opp_ready = false;
-    const int role_win = lane >= 1 && lane <= W.nwin ? lane - 1 : -1;
-    const int role_in = lane >= 8 && lane < 8 + Epi::kInStaged ? lane - 8 : -1;
-    int wmin_l = 0, wmax_l = 0;
-    uint32_t dst_l = (uint32_t)BL.len;
-    const double* src_l = nullptr;
-    if (role_win >= 0) {
-      int so = 0;
-#pragma unroll
-      for (int cc = 0; cc < kMaxWin; ++cc) {
-        if (cc == role_win) {
-          wmin_l = W.wmin[cc];
-          wmax_l = W.wmax[cc];
-          dst_l = (uint32_t)(BL.xw + (size_t)so * sizeof(double));
-        }
-        so += cc < W.nwin ? W.cap[cc] : 0;
-      }
-      src_l = x;
-    } else if (role_in >= 0) {
-      dst_l = (uint32_t)(BL.ein + (size_t)role_in * kPipeRows * sizeof(double));
-#pragma unroll
-      for (int k = 0; k < Epi::kInStaged; ++k)
-        if (k == role_in) src_l = epi.in[k];
-    }
+    SellLaneStream LS;
+    LS.init(lane, W, BL, epi, x);
     const int row_lo = (int)A.row_lo, row_hi = (int)A.row_hi, ncols = (int)A.n_cols;
     for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
       const int slot = q & 31;
@@ -346,23 +400,7 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
       }
       // this lane's copy
       const void* src = nullptr;
-      uint32_t bytes = 0;
-      if (lane == 0) {
-        src = A.slen + (gb0 + blk) * kPipeRows;
-        bytes = kPipeRows;
-      } else if (role_win >= 0) {
-        int lo = r0 + wmin_l, hi = r0 + nr + wmax_l;
-        if (lo < 0) lo = 0;
-        if (hi > ncols) hi = ncols;
-        if (hi > lo) {
-          const int loa = lo & ~1, hia = (hi + 1) & ~1;
-          src = src_l + loa;
-          bytes = (uint32_t)((hia - loa) * sizeof(double));
-        }
-      } else if (role_in >= 0 && fuse_in) {
-        src = src_l + r0;
-        bytes = (uint32_t)(((nr + 1) & ~1) * sizeof(double));
-      }
+      const uint32_t bytes = LS.stream(lane, r0, nr, ncols, A.slen + (gb0 + blk) * kPipeRows, fuse_in, &src);
       const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
       mbar_wait(&bempty[bs], bph ^ 1);
       unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
@@ -375,7 +413,7 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
         mbar_arrive_expect_tx(&bfull[bs], total);
       }
       __syncwarp();
-      if (bytes) bulk_g2s(bst + dst_l, src, bytes, &bfull[bs]);
+      if (bytes) bulk_g2s(bst + LS.dst, src, bytes, &bfull[bs]);
       if (++bs == bslots) {
         bs = 0;
         bph ^= 1;

@@ -1188,60 +1188,77 @@ __global__ void __launch_bounds__(kPipeThreads, PBS_SPIPE_MINB) stencil_pipe_ker
   const long long nrows = S.row_hi - S.row_lo;
   const long long nblk = (nrows + kPipeRows - 1) / kPipeRows;
   if (warp == kConsumerWarps) {
+    // Every lane owns one copy stream of the slot and works out its own source
+    // and size per block (lanes 1..nwin the x windows, lanes 8.. the epilogue
+    // inputs); lane 0 writes the header.  One warp computing every window in
+    // every lane was the critical path of the staged engines (sell.cuh).
     int bs = 0;
     uint32_t bph = 0;
+    const BlockLayout BLp(W.total, Epi::kInStaged);
+    const int role_win = lane >= 1 && lane <= W.nwin ? lane - 1 : -1;
+    const int role_in = lane >= 8 && lane < 8 + Epi::kInStaged ? lane - 8 : -1;
+    long long wmin_l = 0, wmax_l = 0;
+    uint32_t dst_l = 0;
+    const double* src_l = nullptr;
+    if (role_win >= 0) {
+      int so = 0;
+#pragma unroll
+      for (int cc = 0; cc < kMaxWin; ++cc) {
+        if (cc == role_win) {
+          wmin_l = W.wmin[cc];
+          wmax_l = W.wmax[cc];
+          dst_l = (uint32_t)(BLp.xw + (size_t)so * sizeof(double));
+        }
+        so += cc < W.nwin ? W.cap[cc] : 0;
+      }
+      src_l = x;
+    } else if (role_in >= 0) {
+      dst_l = (uint32_t)(BLp.ein + (size_t)role_in * (kPipeRows + 2) * sizeof(double));
+#pragma unroll
+      for (int k = 0; k < Epi::kInStaged; ++k)
+        if (k == role_in) src_l = epi.in[k];
+    }
     for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
       const long long r0 = S.row_lo + blk * kPipeRows;
       const long long r0a = r0 & ~1LL;
       const int nr = (int)min((long long)kPipeRows, S.row_hi - r0);
       const int dr = (int)(r0 - r0a);
-      const uint32_t bin = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
-      long long wlo[kMaxWin];
-      uint32_t wbytes[kMaxWin];
-      uint32_t total = Epi::kInStaged * bin;
-#pragma unroll
-      for (int c = 0; c < kMaxWin; ++c) {
-        wlo[c] = 0x7fffffff;
-        wbytes[c] = 0;
-        if (c < W.nwin) {
-          long long lo = r0 + W.wmin[c], hi = r0 + nr - 1 + W.wmax[c] + 1;
-          if (lo < S.xlo) lo = S.xlo;
-          if (hi > S.xhi) hi = S.xhi;
-          if (hi > lo) {
-            const long long loa = lo & ~1LL, hia = (hi + 1) & ~1LL;
-            wlo[c] = loa;
-            wbytes[c] = (uint32_t)((hia - loa) * sizeof(double));
-            total += wbytes[c];
-          } else {
-            wlo[c] = lo & ~1LL;
-          }
+      const void* src = nullptr;
+      uint32_t bytes = 0;
+      long long ws_l = 0x7fffffff;  // first staged column of this lane's window
+      if (role_win >= 0) {
+        long long lo = r0 + wmin_l, hi = r0 + nr + wmax_l;
+        if (lo < S.xlo) lo = S.xlo;
+        if (hi > S.xhi) hi = S.xhi;
+        ws_l = lo & ~1LL;
+        if (hi > lo) {
+          const long long hia = (hi + 1) & ~1LL;
+          src = src_l + ws_l;
+          bytes = (uint32_t)((hia - ws_l) * sizeof(double));
         }
+      } else if (role_in >= 0) {
+        src = src_l + r0a;
+        bytes = (uint32_t)(((nr + dr + 1) & ~1) * sizeof(double));
       }
+      const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
       mbar_wait(&bempty[bs], bph ^ 1);
-      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
+      unsigned char* bst = blk0 + (size_t)bs * BLp.bytes;
+      BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
+      if (role_win >= 0) bh->ws[role_win] = ws_l;
       if (lane == 0) {
-        BlockHdr* bh = reinterpret_cast<BlockHdr*>(bst);
         bh->r0 = r0;
         bh->nr = nr;
         bh->dr = dr;
-#pragma unroll
-        for (int c = 0; c < kMaxWin; ++c) bh->ws[c] = wlo[c];
-        mbar_arrive_expect_tx(&bfull[bs], total);
       }
       __syncwarp();
-      if (lane >= 1 && lane <= W.nwin) {
-        int soff = 0;
-#pragma unroll
-        for (int cc = 0; cc < kMaxWin; ++cc) {
-          if (cc == lane - 1 && wbytes[cc])
-            bulk_g2s(bst + BL.xw + (size_t)soff * sizeof(double), x + wlo[cc], wbytes[cc], &bfull[bs]);
-          soff += cc < W.nwin ? W.cap[cc] : 0;
-        }
-      } else if (lane >= 8 && lane < 8 + Epi::kInStaged) {
-        const int e = lane - 8;
-        bulk_g2s(bst + BL.ein + (size_t)e * (kPipeRows + 2) * sizeof(double), epi.in[e] + r0a, bin, &bfull[bs]);
+      if (lane == 0) {
+        if (total)
+          mbar_arrive_expect_tx(&bfull[bs], total);
+        else
+          mbar_arrive(&bfull[bs]);  // unreachable with kIn > 0 or windows
       }
-      if (total == 0 && lane == 0) mbar_arrive(&bfull[bs]);  // unreachable with kIn > 0 or windows
+      __syncwarp();
+      if (bytes) bulk_g2s(bst + dst_l, src, bytes, &bfull[bs]);
       if (++bs == bslots) {
         bs = 0;
         bph ^= 1;

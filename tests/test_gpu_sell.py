@@ -94,7 +94,12 @@ def test_sell_spmv_bitwise(pb, n, length, ndistinct, want):
     dm = _upload(rp, ci, v, PBS_PLAIN_TPR=0)
     lay = dm.layout()
     assert lay["layout"] == want, lay
-    assert lay["entries"] >= rp[-1] and lay["entries"] % 256 == 0
+    lens_ = np.diff(rp)
+    nblk = (n + 255) // 256
+    padded = np.zeros(nblk * 256, dtype=np.int64)
+    padded[:n] = lens_
+    assert lay["entries"] == int(256 * padded.reshape(nblk, 256).max(axis=1).sum())  # each block padded to its longest row
+    assert lay["max_row"] == int(lens_.max())
     if want == "sell-dict":
         assert lay["dict_entries"] == ndistinct
     assert np.array_equal(_bits(_spmv_dev(dm, x)), _bits(ref))

@@ -21,22 +21,36 @@ OUT = os.path.join(B.HERE, "variants")
 def one(spec):
     name, _, defs = spec.partition("=")
     out = os.path.join(OUT, f"libpbsafe_{name}.so")
-    cmd = [B.nvcc(), *B.flags(), *[d for d in defs.split(",") if d], "-o", out, *B.SOURCES]
-    p = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(B.ROOT, "build", "variants", name)
+    os.makedirs(objdir, exist_ok=True)
+    extra = [d for d in defs.split(",") if d]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        return obj, subprocess.run([B.nvcc(), *B.flags(), *extra, "-c", "-o", obj, src], capture_output=True, text=True)
+
+    with ThreadPoolExecutor(len(B.SOURCES)) as ex:
+        res = list(ex.map(compile_one, B.SOURCES))
+    for obj, p in res:
+        if p.returncode:
+            return name, "FAILED\n" + p.stderr[-2000:]
+    p = subprocess.run([B.nvcc(), "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler", "-fPIC",
+                        "-o", out, *[obj for obj, _ in res]], capture_output=True, text=True)
     if p.returncode:
         return name, "FAILED\n" + p.stderr[-2000:]
     lines, cur = [], None
-    for ln in p.stderr.splitlines():
-        if "Compiling entry function" in ln and "csr_pipe" in ln:
-            cur = subprocess.run(["c++filt", ln.split("'")[1]], capture_output=True, text=True).stdout.strip()[:48]
+    for ln in "".join(pp.stderr for _, pp in res).splitlines():
+        if "Compiling entry function" in ln and ("csr_pipe" in ln or "sell_pipe" in ln):
+            cur = subprocess.run(["c++filt", ln.split("'")[1]], capture_output=True, text=True).stdout.strip()[:60]
         elif cur and "spill" in ln:
-            lines.append(f"  {cur:48s} {ln.split('info    :')[-1].strip()}")
+            if " 0 bytes spill stores" not in ln:
+                lines.append(f"  {cur:60s} {ln.split('info    :')[-1].strip()}")
             cur = None
     return name, out + "\n" + "\n".join(lines)
 
 
 if __name__ == "__main__":
     os.makedirs(OUT, exist_ok=True)
-    with ThreadPoolExecutor(4) as ex:
+    with ThreadPoolExecutor(1) as ex:
         for name, info in ex.map(one, sys.argv[1:]):
             print(name, info)
