@@ -318,8 +318,12 @@ static inline int sell_slots_cap() {  // block slots of the sliced-ELL engine
   static int v = env_int("PBS_SELL_SLOTS", 3, 2, kMaxStages);
   return v;
 }
-static inline int sell_prefetch() {  // L2 prefetch distance of the block slots' streams, in blocks (0: off)
-  static int v = env_int("PBS_SELL_PF", 2, 0, 8);
+// L2 prefetch distance of the block slots' streams, in blocks.  Off: asking L2
+// for the next blocks' lines ahead of their copies loses on configs 2 and 4
+// (9726 -> 9470 / 9210 / 8746 it/s at distance 1 / 2 / 4; the copies already
+// keep HBM busy and the prefetches only add requests, profiles/r2/sweeps_sell.md)
+static inline int sell_prefetch() {
+  static int v = env_int("PBS_SELL_PF", 0, 0, 8);
   return v;
 }
 static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
