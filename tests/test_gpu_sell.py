@@ -110,6 +110,54 @@ def test_sell_spmv_bitwise(pb, n, length, ndistinct, want):
     csr.free()
 
 
+@pytest.mark.parametrize("seed", range(12))
+def test_sell_random_shapes_bitwise(pb, seed):
+    """Seeded sweep over shapes the layout must handle: n around block
+    multiples, row lengths from empty to several chunks of levels, narrow and
+    wide bands, few / many distinct values, and constant-offset (stencil-like)
+    columns that take the pair dictionary.  Whatever layout the upload picks,
+    the row sums are the oracle's bit for bit."""
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.choice([1, 255, 256, 257, 700, 4096, 5000, 12345]))
+    base = int(rng.integers(1, 40))
+    lens = np.clip(base + rng.integers(-2, 1, n), 0, None)
+    if seed % 3 == 0:
+        lens[rng.integers(0, n, max(1, n // 50))] = 0
+    width = int(rng.choice([base // 2 + 2, 60, 400]))
+    nd = int(rng.choice([1, 3, 27, 256, 300, 0]))
+    pool = rng.standard_normal(max(nd, 1))
+    values = (lambda m: pool[rng.integers(0, nd, m)]) if nd else (lambda m: rng.standard_normal(m))
+    if seed % 4 == 1:
+        # constant offsets per level: every row holds the same (value, offset) pairs
+        offs = np.sort(rng.choice(np.arange(-width, width + 1), size=min(base, 2 * width + 1), replace=False))
+        vals = pool[np.arange(offs.size) % max(nd, 1)] if nd else rng.standard_normal(offs.size)
+        rows, cols, vv = [], [], []
+        for i in range(n):
+            ok = (i + offs >= 0) & (i + offs < n)
+            rows.append(np.full(int(ok.sum()), i))
+            cols.append(i + offs[ok])
+            vv.append(vals[ok])
+        ci = np.concatenate(cols).astype(np.int64)
+        rp = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(rp, np.concatenate(rows).astype(np.int64) + 1, 1)
+        rp = np.cumsum(rp)
+        v = np.concatenate(vv)
+    else:
+        rp, ci, v = _banded(n, lens, width, rng, values)
+    if rp[-1] == 0:
+        pytest.skip("empty matrix")
+    x = rng.standard_normal(n)
+    x[rng.integers(0, n, max(1, n // 10))] = 0.0
+    ref = orc.spmv(rp, ci, v, x)
+    dm = _upload(rp, ci, v)
+    lay = dm.layout()
+    got = _spmv_dev(dm, x)
+    assert np.array_equal(_bits(got), _bits(ref)), (seed, lay)
+    if seed % 4 == 1 and lay["layout"].startswith("sell"):
+        assert lay["layout"] == "sell-pairs", lay
+    dm.free()
+
+
 def test_sell_signed_zeros_empty_rows_and_nonfinite(pb):
     """Padding entries are formed but never added: a row summing to -0.0
     keeps its sign, an empty row gives +0.0, and inf / NaN in x reach exactly
