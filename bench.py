@@ -354,13 +354,16 @@ def run_single(args):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e_it = 0
+    step_ms = []
     for _ in range(args.steps):
+        ts = time.perf_counter()
         out = call()
+        step_ms.append(round((time.perf_counter() - ts) * 1e3, 2))
         e_it += out.iterations
     dt = time.perf_counter() - t0
     e2e = {"value": e_it / dt, "unit": "it/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": int(8 * n + out.iterations * (8 + 1 + 32)), "ms_per_step": dt / args.steps * 1e3,
-           "note": note}
+           "step_ms": step_ms, "note": note}
 
     cpu = None
     if not args.no_cpu and cfg_name == "c2":

@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpbsafe.so")
 # one translation unit per part of the library, compiled in parallel
 SOURCES = [os.path.join(CSRC, f) for f in ("core.cu", "solve.cu", "prod.cu", "pstab.cu", "dist.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("host.h", "common.cuh", "spmv.cuh", "vec.cuh", "finalize.cuh", "zmarch.cuh",
+DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("host.h", "common.cuh", "spmv.cuh", "sell.cuh", "vec.cuh", "finalize.cuh", "zmarch.cuh",
                                                   "ptx.cuh")] + [
     os.path.join(ROOT, "include", "pbsafe.h")]
 OBJDIR = os.path.join(ROOT, "build", "pbsafe")

@@ -6,6 +6,36 @@
 
 #include "host.h"
 
+// PBS_UPLOAD_TIMING=<ms>: print the host-side phase times of an upload that
+// takes longer than <ms> (stall hunting; off by default)
+#include <chrono>
+struct UploadTimer {
+  std::chrono::steady_clock::time_point t0, last;
+  std::string log;
+  double limit = -1;
+  void start() {
+    static const char* e = getenv("PBS_UPLOAD_TIMING");
+    limit = e ? atof(e) : -1;
+    if (limit < 0) return;
+    t0 = last = std::chrono::steady_clock::now();
+    log.clear();
+  }
+  void mark(const char* what) {
+    if (limit < 0) return;
+    auto now = std::chrono::steady_clock::now();
+    char buf[96];
+    snprintf(buf, sizeof(buf), " %s %.2f", what, std::chrono::duration<double, std::milli>(now - last).count());
+    log += buf;
+    last = now;
+  }
+  void stop() {
+    if (limit < 0) return;
+    const double tot = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (tot > limit) fprintf(stderr, "[pbs upload %.1f ms]%s\n", tot, log.c_str());
+  }
+};
+static UploadTimer g_upt;
+
 std::string g_last_error;
 
 void free_graphs(Workspace* ws) {
@@ -72,9 +102,16 @@ int ensure_ws(pbs_mat* m, long long hist_slots) {
   Workspace* ws = m->ws;
   if (!ws && ctx->ws_cache && !m->part.dist) {
     const MatSig g = mat_sig(m);
-    if (memcmp(&g, &ctx->ws_sig, sizeof(MatSig)) == 0) {
-      ws = m->ws = ctx->ws_cache;  // same operator layout: its graphs stay valid
+    if (ctx->ws_cache->n == m->n_rows) {
+      // The vectors, state block, host mirror and events only depend on n:
+      // adopt them.  The graphs bake the operator's pointers and layout in,
+      // so they survive only an identical signature (the pool usually hands
+      // a same-shape upload the same addresses, but not always — and
+      // rebuilding the whole workspace, with its page-locked mirror, costs
+      // 50-700 ms where re-capturing the graphs costs a few).
+      ws = m->ws = ctx->ws_cache;
       ctx->ws_cache = nullptr;
+      if (memcmp(&g, &ctx->ws_sig, sizeof(MatSig)) != 0) free_graphs(ws);
     } else {
       drop_ws_cache(ctx);
     }
@@ -360,6 +397,7 @@ PBS_EXPORT int pbs_destroy(pbs_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
   drop_ws_cache(ctx);
+  buf_flush(ctx);
   cudaFree(ctx->scratch);
   cudaFree(ctx->partials);
   cudaFree(ctx->tmp_state);
@@ -691,12 +729,12 @@ __global__ void sell_fill_pair_kernel(const long long* rp, const double* v, cons
 }
 
 static void free_sell(pbs_ctx* ctx, pbs_mat* m) {
-  pool_free(ctx, m->sell_v);
-  pool_free(ctx, m->sell_c);
-  pool_free(ctx, m->sell_off);
-  pool_free(ctx, m->sell_len);
-  pool_free(ctx, m->sell_vi);
-  pool_free(ctx, m->sell_dict);
+  buf_free(ctx, m->sell_v);
+  buf_free(ctx, m->sell_c);
+  buf_free(ctx, m->sell_off);
+  buf_free(ctx, m->sell_len);
+  buf_free(ctx, m->sell_vi);
+  buf_free(ctx, m->sell_dict);
   m->sell_len = nullptr;
   m->sell_vi = nullptr;
   m->sell_dict = nullptr;
@@ -718,23 +756,24 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
   cudaStream_t s = ctx->stream;
   const long long nblk = (m->n_rows + kPipeRows - 1) / kPipeRows;
   int* lmax = nullptr;
-  CK(pool_alloc(ctx, &m->sell_off, sizeof(long long) * (nblk + 1)));
-  CK(pool_alloc(ctx, &lmax, sizeof(int)));
+  CK(buf_alloc(ctx, &m->sell_off, sizeof(long long) * (nblk + 1)));
+  CK(buf_alloc(ctx, &lmax, sizeof(int)));
   CK(cudaMemsetAsync(lmax, 0, sizeof(int), s));
   sell_levels_kernel<<<(int)std::min<long long>(nblk, ctx->sms * 8), kPipeRows, 0, s>>>(m->rp, m->n_rows, nblk, m->sell_off,
                                                                                        lmax);
   size_t tmp_bytes = 0;
   cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, m->sell_off, m->sell_off, nblk + 1, s);
   void* tmp = nullptr;
-  CK(pool_alloc(ctx, &tmp, tmp_bytes));
+  CK(buf_alloc(ctx, &tmp, tmp_bytes));
   cub::DeviceScan::InclusiveSum(tmp, tmp_bytes, m->sell_off, m->sell_off, nblk + 1, s);
-  pool_free(ctx, tmp);
+  buf_free(ctx, tmp);
   long long entries = 0;
   int hl = 0;
   CK(cudaMemcpyAsync(&entries, m->sell_off + nblk, sizeof(entries), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&hl, lmax, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  pool_free(ctx, lmax);
+  g_upt.mark("levels");
+  buf_free(ctx, lmax);
   const long long pad_pct = env_int("PBS_SELL_PAD", 12, 0, 1000);
   if (entries <= 0 || hl > kSellMaxLen || entries > m->nnz + m->nnz * pad_pct / 100 + 64 * kPipeRows) {
     free_sell(ctx, m);
@@ -746,9 +785,9 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
   int hctl[2] = {0, 1};
   if (env_int("PBS_SELL_DICT", 1, 0, 1)) {
     int* ctl = nullptr;
-    CK(pool_alloc(ctx, &table, sizeof(unsigned long long) * kDictSlots));
-    CK(pool_alloc(ctx, &slot_idx, kDictSlots));
-    CK(pool_alloc(ctx, &ctl, sizeof(int) * 2));
+    CK(buf_alloc(ctx, &table, sizeof(unsigned long long) * kDictSlots));
+    CK(buf_alloc(ctx, &slot_idx, kDictSlots));
+    CK(buf_alloc(ctx, &ctl, sizeof(int) * 2));
     std::vector<unsigned long long> empty(kDictSlots, kDictEmpty);
     CK(cudaMemcpyAsync(table, empty.data(), sizeof(unsigned long long) * kDictSlots, cudaMemcpyHostToDevice, s));
     CK(cudaMemsetAsync(slot_idx, 0, kDictSlots, s));
@@ -756,15 +795,16 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
     dict_insert_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->v, m->nnz, table, ctl);
     CK(cudaMemcpyAsync(hctl, ctl, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));  // (also keeps `empty` alive until its copy has run)
-    pool_free(ctx, ctl);
+    g_upt.mark("dict");
+    buf_free(ctx, ctl);
   }
   const bool dict = hctl[1] == 0 && hctl[0] <= kSellDict;
   const int grid = (int)std::min<long long>(nblk, ctx->sms * 8);
-  CK(pool_alloc(ctx, &m->sell_len, (size_t)nblk * kPipeRows));
+  CK(buf_alloc(ctx, &m->sell_len, (size_t)nblk * kPipeRows));
   bool pairs = false;
   if (dict) {
-    CK(pool_alloc(ctx, &m->sell_dict, sizeof(SellPair) * kSellDict));  // doubles, or pairs
-    CK(pool_alloc(ctx, &m->sell_vi, (size_t)entries));
+    CK(buf_alloc(ctx, &m->sell_dict, sizeof(double) * kSellDict));
+    CK(buf_alloc(ctx, &m->sell_vi, (size_t)entries));
     dict_compact_kernel<<<1, 1, 0, s>>>(table, m->sell_dict, slot_idx);
     m->sell_ndict = hctl[0];
     // pair dictionary (PBS_SELL_PAIR=0: keep the u16 column stream)
@@ -774,10 +814,10 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
       SellPair* pdict = nullptr;
       int* ctl = nullptr;
       int pctl[2] = {0, 1};
-      CK(pool_alloc(ctx, &ptable, sizeof(unsigned long long) * kDictSlots));
-      CK(pool_alloc(ctx, &pslot, kDictSlots));
-      CK(pool_alloc(ctx, &pdict, sizeof(SellPair) * kSellDict));
-      CK(pool_alloc(ctx, &ctl, sizeof(int) * 2));
+      CK(buf_alloc(ctx, &ptable, sizeof(unsigned long long) * kDictSlots));
+      CK(buf_alloc(ctx, &pslot, kDictSlots));
+      CK(buf_alloc(ctx, &pdict, sizeof(SellPair) * kSellDict));
+      CK(buf_alloc(ctx, &ctl, sizeof(int) * 2));
       std::vector<unsigned long long> empty(kDictSlots, kDictEmpty);
       CK(cudaMemcpyAsync(ptable, empty.data(), sizeof(unsigned long long) * kDictSlots, cudaMemcpyHostToDevice, s));
       CK(cudaMemsetAsync(pslot, 0, kDictSlots, s));
@@ -786,35 +826,37 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
                                                     ptable, ctl);
       CK(cudaMemcpyAsync(pctl, ctl, sizeof(int) * 2, cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      pool_free(ctx, ctl);
+      g_upt.mark("pairs");
+      buf_free(ctx, ctl);
       pairs = pctl[1] == 0 && pctl[0] <= kSellDict;
       if (pairs) {
         pair_compact_kernel<<<1, 1, 0, s>>>(ptable, m->sell_dict, pdict, pslot);
         sell_fill_pair_kernel<<<grid, kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk, m->sell_off, table,
                                                          slot_idx, ptable, pslot, m->sell_vi, m->sell_len);
-        pool_free(ctx, m->sell_dict);
+        buf_free(ctx, m->sell_dict);
         m->sell_dict = reinterpret_cast<double*>(pdict);
         m->sell_ndict = pctl[0];
         m->sell_mode = kSellPairs;
       } else {
-        pool_free(ctx, pdict);
+        buf_free(ctx, pdict);
       }
-      pool_free(ctx, ptable);
-      pool_free(ctx, pslot);
+      buf_free(ctx, ptable);
+      buf_free(ctx, pslot);
     }
     if (!pairs) m->sell_mode = kSellDictV;
   } else {
-    CK(pool_alloc(ctx, &m->sell_v, sizeof(double) * entries));
+    CK(buf_alloc(ctx, &m->sell_v, sizeof(double) * entries));
     m->sell_mode = kSellF64;
   }
   if (!pairs) {
-    CK(pool_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
+    CK(buf_alloc(ctx, &m->sell_c, sizeof(unsigned short) * entries));
     sell_fill_kernel<<<grid, kPipeRows, 0, s>>>(m->rp, m->v, m->wc, m->n_rows, nblk, m->sell_off, m->sell_v, m->sell_c,
                                                 m->sell_len, dict ? table : nullptr, slot_idx, m->sell_vi);
   }
   CK(cudaGetLastError());
-  pool_free(ctx, table);
-  pool_free(ctx, slot_idx);
+  g_upt.mark("fill-launch");
+  buf_free(ctx, table);
+  buf_free(ctx, slot_idx);
   m->sell_lmax = hl;
   m->sell_entries = entries;
   return PBS_OK;
@@ -829,14 +871,14 @@ static int build_window_cols(pbs_ctx* ctx, pbs_mat* m) {
 
 static int build_window_cols_only(pbs_ctx* ctx, pbs_mat* m) {
   if (m->wc) {
-    pool_free(ctx, m->wc);
+    buf_free(ctx, m->wc);
     m->wc = nullptr;
   }
   if ((!m->xwin.nwin && !m->xwin.band_s) || m->nnz == 0 || m->xwin.total > 65535) return PBS_OK;
   cudaStream_t s = ctx->stream;
   int* bad = nullptr;
-  CK(pool_alloc(ctx, &m->wc, sizeof(unsigned short) * (m->nnz + 16)));
-  CK(pool_alloc(ctx, &bad, sizeof(int)));
+  CK(buf_alloc(ctx, &m->wc, sizeof(unsigned short) * (m->nnz + 16)));
+  CK(buf_alloc(ctx, &bad, sizeof(int)));
   CK(cudaMemsetAsync(m->wc + m->nnz, 0, sizeof(unsigned short) * 16, s));
   CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
   window_cols_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->rp, m->ci, m->n_rows, m->n_cols, m->xwin, m->wc, bad);
@@ -844,9 +886,10 @@ static int build_window_cols_only(pbs_ctx* ctx, pbs_mat* m) {
   CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   CK(cudaGetLastError());
-  pool_free(ctx, bad);
+  g_upt.mark("wcols");
+  buf_free(ctx, bad);
   if (hbad || env_int("PBS_NO_WINDOW_COLS", 0, 0, 1)) {  // 1: keep col_idx (A/B sweeps)
-    pool_free(ctx, m->wc);
+    buf_free(ctx, m->wc);
     m->wc = nullptr;
   }
   return PBS_OK;
@@ -856,16 +899,16 @@ static int build_window_cols_only(pbs_ctx* ctx, pbs_mat* m) {
 int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   m->xwin = XWin{};
   if (!m->stencil) {  // rebuilt below when the new pattern windows
-    pool_free(ctx, m->wc);
+    buf_free(ctx, m->wc);
     m->wc = nullptr;
     free_sell(ctx, m);
   }
   if (m->n_rows == 0 || m->nnz == 0 || m->n_cols > 0x7fffffffLL) return PBS_OK;
   cudaStream_t s = ctx->stream;
   int *bmin = nullptr, *bmax = nullptr, *wide = nullptr;
-  CK(pool_alloc(ctx, &bmin, sizeof(int) * 2 * kBins));
-  CK(pool_alloc(ctx, &bmax, sizeof(int) * 2 * kBins));
-  CK(pool_alloc(ctx, &wide, sizeof(int)));
+  CK(buf_alloc(ctx, &bmin, sizeof(int) * 2 * kBins));
+  CK(buf_alloc(ctx, &bmax, sizeof(int) * 2 * kBins));
+  CK(buf_alloc(ctx, &wide, sizeof(int)));
   std::vector<int> hmin(2 * kBins, 0x7fffffff), hmax(2 * kBins, (int)0x80000000);
   CK(cudaMemcpyAsync(bmin, hmin.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(bmax, hmax.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
@@ -876,9 +919,10 @@ int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   CK(cudaMemcpyAsync(hmax.data(), bmax, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
-  pool_free(ctx, bmin);
-  pool_free(ctx, bmax);
-  pool_free(ctx, wide);
+  g_upt.mark("bins");
+  buf_free(ctx, bmin);
+  buf_free(ctx, bmax);
+  buf_free(ctx, wide);
   if (hwide) return PBS_OK;
   std::vector<std::pair<int, int>> cl;  // [min, max] offsets
   for (int b = 0; b < 2 * kBins; ++b) {
@@ -949,8 +993,8 @@ static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const
       const long long chunk = 1LL << 24;
       long long* tmp = nullptr;
       int* bad = nullptr;
-      CK(pool_alloc(ctx, &tmp, sizeof(long long) * (nnz < chunk ? nnz : chunk)));
-      CK(pool_alloc(ctx, &bad, sizeof(int)));
+      CK(buf_alloc(ctx, &tmp, sizeof(long long) * (nnz < chunk ? nnz : chunk)));
+      CK(buf_alloc(ctx, &bad, sizeof(int)));
       CK(cudaMemsetAsync(bad, 0, sizeof(int), s));
       for (long long off = 0; off < nnz; off += chunk) {
         long long len = nnz - off < chunk ? nnz - off : chunk;
@@ -961,12 +1005,13 @@ static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const
       int hbad = 0;
       CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
-      pool_free(ctx, tmp);
-      pool_free(ctx, bad);
+      buf_free(ctx, tmp);
+      buf_free(ctx, bad);
       if (hbad) return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
     }
   }
   CK(cudaStreamSynchronize(s));
+  g_upt.mark("h2d+narrow");
   m->blk_nnz_max = 0;
   for (long long r0 = 0; r0 < n_rows; r0 += kPipeRows) {
     const long long r1 = r0 + kPipeRows < n_rows ? r0 + kPipeRows : n_rows;
@@ -986,7 +1031,13 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
   if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz)
     return set_err(ctx, PBS_ERR_INVALID, "row_ptr endpoints inconsistent with nnz arrays");
   CK(cudaSetDevice(ctx->device));
+  g_upt.start();
   if (ctx->ws_cache && ctx->ws_cache->n != n_rows) drop_ws_cache(ctx);  // cannot match: release it now
+  if (ctx->spare_rows != n_rows || ctx->spare_nnz != nnz) {  // another shape: its buffers are of no use
+    buf_flush(ctx);
+    ctx->spare_rows = n_rows;
+    ctx->spare_nnz = nnz;
+  }
   pbs_mat* m = new pbs_mat();
   m->ctx = ctx;
   m->n_rows = n_rows;
@@ -994,13 +1045,15 @@ PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int6
   m->nnz = nnz;
   cudaStream_t s = ctx->stream;
   // padding: the pipelined SpMV bulk-copies 16-byte-aligned windows
-  CK(pool_alloc(ctx, &m->rp, sizeof(long long) * (n_rows + 4)));
-  CK(pool_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
-  CK(pool_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
+  CK(buf_alloc(ctx, &m->rp, sizeof(long long) * (n_rows + 4)));
+  CK(buf_alloc(ctx, &m->ci, sizeof(int) * (nnz + 8)));
+  CK(buf_alloc(ctx, &m->v, sizeof(double) * (nnz + 4)));
   CK(cudaMemsetAsync(m->rp + n_rows + 1, 0, sizeof(long long) * 3, s));
   CK(cudaMemsetAsync(m->ci + nnz, 0, sizeof(int) * 8, s));
   CK(cudaMemsetAsync(m->v + nnz, 0, sizeof(double) * 4, s));
+  g_upt.mark("alloc");
   int rc = upload_arrays(ctx, m, row_ptr, col_idx, col_bytes, values);
+  g_upt.stop();
   if (rc) {
     pbs_mat_free(m);
     return rc;
@@ -1217,6 +1270,8 @@ PBS_EXPORT int pbs_stencil_to_csr(pbs_mat* st, pbs_mat** out) {
   cudaStream_t s = ctx->stream;
   const long long n = st->n_rows, nnz = st->nnz;
   if (nnz > 0x7fffffffffffLL) return set_err(ctx, PBS_ERR_INVALID, "too many nonzeros");
+  buf_flush(ctx);  // spares of an uploaded shape are of no use here
+  ctx->spare_rows = ctx->spare_nnz = -1;
   pbs_mat* m = new pbs_mat();
   m->ctx = ctx;
   m->n_rows = n;
@@ -1327,16 +1382,16 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   } else {
     free_ws(m->ws);
   }
-  pool_free(m->ctx, m->rp);
-  pool_free(m->ctx, m->ci);
-  pool_free(m->ctx, m->v);
-  pool_free(m->ctx, m->wc);
-  pool_free(m->ctx, m->sell_v);
-  pool_free(m->ctx, m->sell_c);
-  pool_free(m->ctx, m->sell_off);
-  pool_free(m->ctx, m->sell_len);
-  pool_free(m->ctx, m->sell_vi);
-  pool_free(m->ctx, m->sell_dict);
+  buf_free(m->ctx, m->rp);
+  buf_free(m->ctx, m->ci);
+  buf_free(m->ctx, m->v);
+  buf_free(m->ctx, m->wc);
+  buf_free(m->ctx, m->sell_v);
+  buf_free(m->ctx, m->sell_c);
+  buf_free(m->ctx, m->sell_off);
+  buf_free(m->ctx, m->sell_len);
+  buf_free(m->ctx, m->sell_vi);
+  buf_free(m->ctx, m->sell_dict);
   delete m;
   return PBS_OK;
 }

@@ -99,6 +99,16 @@ struct pbs_ctx {
   EventPool events;
   Workspace* ws_cache = nullptr;  // workspace of the last freed single-GPU operator
   MatSig ws_sig{};
+  // Buffers of the last uploaded CSR shape (operator arrays and upload
+  // temporaries), kept by exact size when freed and handed to the next upload
+  // of the same shape: a solve(CsrMatrix) per step then makes no allocation
+  // at all.  (Going back to the stream-ordered pool each time stalled an
+  // upload for 20-700 ms every few dozen calls, whenever the pool had split
+  // a cached block and had to map new memory.)
+  std::multimap<size_t, void*> spare;
+  std::map<void*, size_t> spare_sizes;  // live buffers that came from buf_alloc
+  size_t spare_bytes = 0;
+  long long spare_rows = -1, spare_nnz = -1;
 };
 
 struct pbs_mat {
@@ -153,6 +163,44 @@ static cudaError_t pool_alloc(pbs_ctx* ctx, T** p, size_t bytes) {
 }
 static inline void pool_free(pbs_ctx* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+constexpr size_t kSpareCapBytes = 6ULL << 30;  // buffers kept for the next same-shape upload, at most
+
+template <class T>
+static cudaError_t buf_alloc(pbs_ctx* ctx, T** p, size_t bytes) {
+  auto it = ctx->spare.lower_bound(bytes);  // the oldest spare of exactly this size
+  if (it != ctx->spare.end() && it->first == bytes) {
+    *p = (T*)it->second;
+    ctx->spare.erase(it);
+    ctx->spare_bytes -= bytes;
+    ctx->spare_sizes[(void*)*p] = bytes;
+    return cudaSuccess;
+  }
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, ctx->stream);
+  if (e == cudaSuccess) ctx->spare_sizes[(void*)*p] = bytes;
+  return e;
+}
+static inline void buf_free(pbs_ctx* ctx, void* p) {
+  if (!p) return;
+  auto it = ctx->spare_sizes.find(p);
+  if (it == ctx->spare_sizes.end()) {  // not from buf_alloc
+    cudaFreeAsync(p, ctx->stream);
+    return;
+  }
+  const size_t bytes = it->second;
+  ctx->spare_sizes.erase(it);
+  if (ctx->spare_bytes + bytes > kSpareCapBytes) {
+    cudaFreeAsync(p, ctx->stream);
+    return;
+  }
+  ctx->spare.emplace(bytes, p);  // after the older spares of this size
+  ctx->spare_bytes += bytes;
+}
+static inline void buf_flush(pbs_ctx* ctx) {
+  for (auto& kv : ctx->spare) cudaFreeAsync(kv.second, ctx->stream);
+  ctx->spare.clear();
+  ctx->spare_bytes = 0;
 }
 
 static inline int grid_for(pbs_ctx* ctx, const void* kernel, long long work_blocks, int cap_per_sm = 8,

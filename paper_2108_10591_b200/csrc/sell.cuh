@@ -372,14 +372,24 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
     int bs = 0;
     uint32_t bph = 0;
     long long pf_off = 0, pf_end = 0;
-    griddep_wait();
-    cta_sync2<kSellThreads>();
-    if (!go) return;
+    griddep_wait();  // the previous kernel's vectors are final from here on
+    // The first block's copies go out before the CTA's gate decision (thread
+    // 0's read of the solver state and the barrier behind it): if the gate
+    // says stop, they are left to land and the warp exits.
+    bool gated = false;
+    auto gate = [&](bool issued) -> bool {
+      gated = true;
+      cta_sync2<kSellThreads>();
+      if (go) return true;
+      if (issued) mbar_wait(&bfull[0], 0);
+      return false;
+    };
     bool opp_ready = false;
     SellLaneStream LS;
     LS.init(lane, W, BL, epi, x);
     const int row_lo = (int)A.row_lo, row_hi = (int)A.row_hi, ncols = (int)A.n_cols;
     for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
+      if (!gated && q == 1 && !gate(true)) return;
       const int slot = q & 31;
       if (slot == 0) {
         const long long b2 = (long long)blk + (long long)lane * gridDim.x;
@@ -419,6 +429,7 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
         bph ^= 1;
       }
     }
+    if (!gated) gate(nblk > (int)blockIdx.x);  // at most one block: the barrier is still owed
     return;
   }
 
