@@ -341,11 +341,11 @@ static inline int band_chunk_cap() {
   static int v = env_int("PBS_BAND_CHUNK", 3072, 256, kPipeChunkMax) & ~3;
   return v;
 }
-static inline int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr|tprlate: thread-per-row CSR engine
+static inline int csr_engine_tpr() {  // PBS_CSR_ENGINE=tpr: thread-per-row CSR engine for every product
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("PBS_CSR_ENGINE");
-    v = (e && std::string(e) == "tpr") ? 1 : ((e && std::string(e) == "tprlate") ? 2 : 0);
+    v = (e && std::string(e) == "tpr") ? 1 : 0;
   }
   return v;
 }
@@ -379,12 +379,9 @@ static inline int pipe_extra_chunks() {  // chunk stages beyond the block slots
   return v;
 }
 
-// PBS_PIPE_STAGE_IN: 1 (default) stage the epilogue inputs, 0 never (the
-// consumers load them; loses everywhere measured, profiles/sweeps/r1_c4_pipe.log)
-static inline int pipe_stage_in() {
-  static int v = env_int("PBS_PIPE_STAGE_IN", 1, 0, 1);
-  return v;
-}
+// The epilogue inputs are always staged by the producer: the build that let
+// the consumers load them instead lost everywhere measured
+// (profiles/sweeps/r1_c4_pipe.log) and is no longer compiled.
 
 // Ring sizing.  The engine is bound by the bytes each SM keeps in flight
 // (Little's law: ~45 KB/us per SM at full HBM rate times ~1-2 us of loaded
@@ -407,7 +404,7 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   int per_sm = 0, optin = 0;
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, ctx->device);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device);
-  const int si = Epi::kInStaged ? pipe_stage_in() : 1;
+  const int si = 1;
   const BlockLayout BL(W.total, si ? Epi::kInStaged : 0);
   // extra chunk stages pay when a block spans several chunks (the consumers
   // walk them in turn); with one chunk per block (7-point stencils, config 2:
@@ -445,8 +442,7 @@ static int pipe_config(pbs_ctx* ctx, const XWin& W, int colb, long long blk_nnz_
   *chunk = ch;
   *stage_in = si;
   *smem = kPipeBarrierBytes + (size_t)W.band_s * sizeof(double) + (size_t)n * BL.bytes + (size_t)(n + xc) * CL.bytes;
-  const void* k = si ? (c == 1 ? (const void*)csr_pipe_kernel<Epi, true, 1> : (const void*)csr_pipe_kernel<Epi, true>)
-                     : (const void*)csr_pipe_kernel<Epi, false>;
+  const void* k = c == 1 ? (const void*)csr_pipe_kernel<Epi, true, 1> : (const void*)csr_pipe_kernel<Epi, true>;
   auto it = ctx->occ.find(k);
   if (it == ctx->occ.end() || (size_t)it->second < *smem) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)*smem);
@@ -738,13 +734,8 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
       const int per_sm = L.leave_room && full > 1 ? full - 1 : full;
       return L.cap_grid(grid_for(L.ctx, k, nblk, per_sm, L.sms()));
     };
-    if (csr_engine_tpr() == 2) {
-      grid = tpr_grid((const void*)csr_tpr_kernel<Epi, true>);
-      csr_tpr_kernel<Epi, true><<<grid, kThreads, 0, L.s>>>(A, x, epi);
-    } else {
-      grid = tpr_grid((const void*)csr_tpr_kernel<Epi, false>);
-      csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
-    }
+    grid = tpr_grid((const void*)csr_tpr_kernel<Epi, false>);
+    csr_tpr_kernel<Epi, false><<<grid, kThreads, 0, L.s>>>(A, x, epi);
   } else if (!m->stencil && (m->sell_v || m->sell_vi) && (lo % kPipeRows) == 0) {
     // sliced-ELL form (sell.cuh): row blocks counted from row 0, like the
     // window-local columns
@@ -789,15 +780,13 @@ static int spmv_launch(Launcher& L, const double* x, Epi epi, long long lo, long
     grid = L.cap_grid(nblk < cap ? nblk : cap);
     // programmatic dependent launch: overlaps this CTA's prologue and first
     // matrix chunks with the previous kernel's drain
-    if (stage_in && ctas == 1)  // 1-CTA layout: the instantiation with more products in flight
+    (void)stage_in;
+    if (ctas == 1)  // 1-CTA layout: the instantiation with more products in flight
       launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, true, 1>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
                  cstages, chunk);
-    else if (stage_in)
+    else
       launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, true>, grid, kPipeThreads, smem, A, x, epi, W, bslots, cstages,
                  chunk);
-    else
-      launch_pdl(L, kPdlCsrPipe, csr_pipe_kernel<Epi, false>, grid, kPipeThreads, smem, A, x, epi, W, bslots,
-                 cstages, chunk);
     if (L.err) return 0;
   } else if (m->stencil &&
              stencil_zm_geom<Epi>(L.ctx, L.sms(), m, lo, hi,
