@@ -186,6 +186,18 @@ __device__ __forceinline__ double sell_chunk(int nk, const unsigned char* vs, co
   }
 }
 
+// Epi::kEarly: bit k set when staged input k is not written by the kernel
+// that precedes this epilogue's kernel in the schedules that launch it with
+// programmatic dependent launch, so its copy may precede griddep_wait.
+template <class Epi, class = void>
+struct EpiEarly {
+  static constexpr unsigned value = 0;
+};
+template <class Epi>
+struct EpiEarly<Epi, decltype((void)Epi::kEarly)> {
+  static constexpr unsigned value = Epi::kEarly;
+};
+
 // One lane's copy stream of a block slot: lane 0 the row lengths, lanes
 // 1..nwin the x windows, lanes 8.. the epilogue inputs.
 struct SellLaneStream {
@@ -372,26 +384,22 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
     int bs = 0;
     uint32_t bph = 0;
     long long pf_off = 0, pf_end = 0;
-    griddep_wait();  // the previous kernel's vectors are final from here on
-    // The first block's copies go out before the CTA's gate decision (thread
-    // 0's read of the solver state and the barrier behind it): if the gate
-    // says stop, they are left to land and the warp exits.
-    bool gated = false;
-    auto gate = [&](bool issued) -> bool {
-      gated = true;
-      cta_sync2<kSellThreads>();
-      if (go) return true;
-      if (issued) mbar_wait(&bfull[0], 0);
-      return false;
-    };
     bool opp_ready = false;
     SellLaneStream LS;
     LS.init(lane, W, BL, epi, x);
     const int row_lo = (int)A.row_lo, row_hi = (int)A.row_hi, ncols = (int)A.n_cols;
-    for (int blk = blockIdx.x, q = 0; blk < nblk; blk += gridDim.x, ++q) {
-      if (!gated && q == 1 && !gate(true)) return;
+    // Early streams: the row lengths (the operator's) and the epilogue inputs
+    // the previous kernel of the schedule does not write (Epi::kEarly).  For
+    // the first bslots blocks they go out before griddep_wait, while that
+    // kernel drains and runs its check tail; the x windows and the other
+    // inputs follow once it has completed.
+    constexpr unsigned kEarly = EpiOpp<Epi>::value ? 0u : EpiEarly<Epi>::value;
+    const bool lane_early = lane == 0 || (LS.role_in >= 0 && ((kEarly >> LS.role_in) & 1u));
+    // phase 0: every stream of the block; 1: header, expected bytes and the
+    // early streams; 2: the late streams of a block issued with phase 1
+    auto issue = [&](int blk, int q, int phase) {
       const int slot = q & 31;
-      if (slot == 0) {
+      if (slot == 0 && phase != 2) {  // entry offsets of blocks q .. q+31 of this CTA
         const long long b2 = (long long)blk + (long long)lane * gridDim.x;
         if (b2 < nblk) {
           pf_off = __ldg(A.soff + gb0 + b2);
@@ -408,28 +416,48 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
         if (!opp_ready) opp_ready = __shfl_sync(0xffffffffu, lane == 0 ? epi.ready() : false, 0);
         fuse_in = opp_ready;
       }
-      // this lane's copy
       const void* src = nullptr;
       const uint32_t bytes = LS.stream(lane, r0, nr, ncols, A.slen + (gb0 + blk) * kPipeRows, fuse_in, &src);
-      const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
-      mbar_wait(&bempty[bs], bph ^ 1);
-      unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
-      if (lane == 0) {
-        SellHdr* bh = reinterpret_cast<SellHdr*>(bst);
-        bh->r0 = r0;
-        bh->nr = nr;
-        bh->levels = levels;
-        bh->fused = fuse_in ? 1 : 0;
-        mbar_arrive_expect_tx(&bfull[bs], total);
+      const int sl = phase == 2 ? q : bs;  // phase 2 only runs for q < bslots
+      unsigned char* bst = blk0 + (size_t)sl * BL.bytes;
+      if (phase != 2) {
+        const uint32_t total = __reduce_add_sync(0xffffffffu, bytes);
+        mbar_wait(&bempty[bs], bph ^ 1);
+        if (lane == 0) {
+          SellHdr* bh = reinterpret_cast<SellHdr*>(bst);
+          bh->r0 = r0;
+          bh->nr = nr;
+          bh->levels = levels;
+          bh->fused = fuse_in ? 1 : 0;
+          mbar_arrive_expect_tx(&bfull[bs], total);
+        }
+        __syncwarp();
       }
-      __syncwarp();
-      if (bytes) bulk_g2s(bst + LS.dst, src, bytes, &bfull[bs]);
-      if (++bs == bslots) {
+      const bool mine = phase == 0 || ((phase == 1) == lane_early);
+      if (bytes && mine) bulk_g2s(bst + LS.dst, src, bytes, &bfull[sl]);
+      if (phase != 2 && ++bs == bslots) {
         bs = 0;
         bph ^= 1;
       }
+    };
+    int npre = 0;
+    if (kEarly)
+      for (int blk = blockIdx.x; blk < nblk && npre < bslots; blk += gridDim.x, ++npre) issue(blk, npre, 1);
+    griddep_wait();  // the previous kernel's vectors are final from here on
+    if (kEarly) {
+      for (int q = 0; q < npre; ++q) issue((int)blockIdx.x + q * (int)gridDim.x, q, 2);
+    } else if (nblk > (int)blockIdx.x) {
+      // the first block goes out before the CTA's gate decision (thread 0's
+      // read of the solver state and the barrier behind it)
+      issue(blockIdx.x, 0, 0);
+      npre = 1;
     }
-    if (!gated) gate(nblk > (int)blockIdx.x);  // at most one block: the barrier is still owed
+    cta_sync2<kSellThreads>();
+    if (!go) {  // the gate says stop: let what was issued land
+      for (int q = 0; q < npre; ++q) mbar_wait(&bfull[q], 0);
+      return;
+    }
+    for (int blk = (int)blockIdx.x + npre * (int)gridDim.x, q = npre; blk < nblk; blk += gridDim.x, ++q) issue(blk, q, 0);
     return;
   }
 

@@ -278,6 +278,11 @@ template <bool DOTS>
 struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-local K2 updates)
   static constexpr int kIn = DOTS ? 12 : 11;
   static constexpr int kInStaged = 11;  // r0s (DOTS) is loaded by the consumer thread
+  // K12 with the dots is only launched by the fused steady iteration, after
+  // K3 (writes l g s), the setup's / a replacement iteration's s = A r, or a
+  // finalize kernel: r p u t y w z x are final before that kernel starts
+  // (sell.cuh: EpiEarly)
+  static constexpr unsigned kEarly = DOTS ? 0x737u : 0u;
   static constexpr int kWcBatch = DOTS ? PBS_WCB_K12D : 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = DOTS ? PBS_K12D_MINB : 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
@@ -440,6 +445,10 @@ template <unsigned M>
 struct EpiK3T {
   static constexpr int kIn = M == kAllDots ? 8 : (M ? 7 : 4);
   static constexpr int kInStaged = kIn;  // inputs the staged engines copy into smem
+  // K3 with the four s-dots follows K12 (writes As p u w t z y x r) in the
+  // fused iteration and plain (non-programmatic) kernels in the multi-GPU
+  // schedule: l g s r0s are final before its predecessor starts
+  static constexpr unsigned kEarly = M == kDotsK3 ? 0x4eu : 0u;
   static constexpr int kWcBatch = M == kAllDots ? 2 : PBS_WCB_K3S;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
