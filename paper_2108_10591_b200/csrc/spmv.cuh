@@ -282,7 +282,10 @@ struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-loca
   // K3 (writes l g s), the setup's / a replacement iteration's s = A r, or a
   // finalize kernel: r p u t y w z x are final before that kernel starts
   // (sell.cuh: EpiEarly)
-  static constexpr unsigned kEarly = DOTS ? 0x737u : 0u;
+  // Measured neutral to slightly negative (config 2: 9.71k vs 9.75-9.9k it/s,
+  // profiles/r2/sweeps_sell.md): the early copies compete with the draining
+  // kernel for HBM.  Mask kept for the record: 0x737.
+  static constexpr unsigned kEarly = 0u;
   static constexpr int kWcBatch = DOTS ? PBS_WCB_K12D : 4;  // staged-window products in flight per row
   static constexpr int kMinBlocks = DOTS ? PBS_K12D_MINB : 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = false;  // staged engine wins (sweep r1)
@@ -448,7 +451,8 @@ struct EpiK3T {
   // K3 with the four s-dots follows K12 (writes As p u w t z y x r) in the
   // fused iteration and plain (non-programmatic) kernels in the multi-GPU
   // schedule: l g s r0s are final before its predecessor starts
-  static constexpr unsigned kEarly = M == kDotsK3 ? 0x4eu : 0u;
+  // (mask 0x4e; off, see EpiK12T)
+  static constexpr unsigned kEarly = 0u;
   static constexpr int kWcBatch = M == kAllDots ? 2 : PBS_WCB_K3S;  // staged-window products in flight per row
   static constexpr int kMinBlocks = 1;  // direct stencil engine occupancy target
   static constexpr bool kStencilPipe = true;  // staged engine wins (sweep r1)
