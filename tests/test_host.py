@@ -236,7 +236,7 @@ def test_bench_reference_arm_contract():
 
 def test_sass_census_blackwell_async_copies():
     """The hot engines are Blackwell-native in SASS, not just built for sm_100a:
-    every staged CSR / stencil SpMV instantiation issues 1-D bulk async copies
+    every staged CSR / sliced-ELL / stencil SpMV instantiation issues 1-D bulk async copies
     (UBLKCP) and waits on mbarrier phases (SYNCS.PHASECHK), and the z-marching
     engine issues 3-D TMA tensor loads (UTMALDG)."""
     import subprocess
@@ -249,15 +249,19 @@ def test_sass_census_blackwell_async_copies():
     for chunk in re.split(r"\n\s*Function : ", sass)[1:]:
         name, body = chunk.split("\n", 1)
         funcs[name.strip()] = body
-    pipe = {n: b for n, b in funcs.items() if "csr_pipe_kernel" in n or "stencil_pipe_kernel" in n}
+    pipe = {n: b for n, b in funcs.items()
+            if "csr_pipe_kernel" in n or "stencil_pipe_kernel" in n or "sell_pipe_kernel" in n}
     zm = {n: b for n, b in funcs.items() if "stencil_zm_kernel" in n}
-    assert len(pipe) >= 20 and len(zm) >= 8, (len(pipe), len(zm))
+    sell = [n for n in pipe if "sell_pipe_kernel" in n]
+    assert len(pipe) >= 20 and len(zm) >= 8 and len(sell) >= 18, (len(pipe), len(zm), len(sell))
     for n, b in pipe.items():
         assert "UBLKCP" in b and "SYNCS.PHASECHK" in b, n
     for n, b in zm.items():
         assert "UTMALDG" in b and "SYNCS.PHASECHK" in b, n
     # the two kernels of the config-2 iteration and the config-4 matrix-free K12
-    hot = ("csr_pipe_kernelINS_7EpiK12TILb1EEE", "csr_pipe_kernelINS_6EpiK3TILj77EEE",
+    # (sliced-ELL K12 / K3 in the pair-dictionary mode, 2 CTAs per SM; the CSR-order pair; z-marching K12)
+    hot = ("sell_pipe_kernelINS_7EpiK12TILb1EEELi2ELi2E", "sell_pipe_kernelINS_6EpiK3TILj77EEELi2ELi2E",
+           "csr_pipe_kernelINS_7EpiK12TILb1EEE", "csr_pipe_kernelINS_6EpiK3TILj77EEE",
            "stencil_zm_kernelINS_7EpiK12TILb1EEELi27E")
     for h in hot:
         assert any(h in n for n in funcs), h
