@@ -241,16 +241,16 @@ def _raise_for(rc, res, ctx_handle):
 def _build_outcome(method, config, eng, res, x, rel, flags, coef, keep) -> SolveOutcome:
     k = int(res.n_records)
     history = []
+    # plain Python floats / ints once (tolist), not a numpy scalar per field
+    rel_l, flag_l, coef_l = rel[:k].tolist(), flags[:k].tolist(), coef[:k].tolist()
+    omega_form = method in ("bicgstab", "pbicgstab")  # CoefficientSet(alpha, beta, omega) (solvers.py:309)
     for i in range(k):
-        rec = IterationRecord(i, float(rel[i]), replaced=bool(flags[i] & _lib.HIST_REPLACED))
-        if flags[i] & _lib.HIST_HAS_COEF:
-            if method in ("bicgstab", "pbicgstab"):  # CoefficientSet(alpha, beta, omega) (solvers.py:309)
-                rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
-                                                  omega=float(coef[i, 2]))
-            else:
-                rec.coefficients = CoefficientSet(alpha=float(coef[i, 0]), beta=float(coef[i, 1]),
-                                                  zeta=float(coef[i, 2]), eta=float(coef[i, 3]))
-        history.append(rec)
+        f = flag_l[i]
+        cs = None
+        if f & _lib.HIST_HAS_COEF:
+            a, b_, z, e = coef_l[i]
+            cs = CoefficientSet(a, b_, None, None, z) if omega_form else CoefficientSet(a, b_, z, e)
+        history.append(IterationRecord(i, rel_l[i], None, bool(f & _lib.HIST_REPLACED), cs))
     status = _STATUS[res.status]
     iterations = int(res.iterations)
     stopped_in_loop = iterations < config.max_iters  # a loop check ended it
