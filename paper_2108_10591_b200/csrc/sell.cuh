@@ -9,31 +9,31 @@
 //
 // At upload the operator's nonzeros are therefore also laid out per 256-row
 // block in level-major ("sliced ELL", slice = the row block) order: level k
-// of the block holds the k-th nonzero of each of its 256 rows — value and
-// window-local u16 column — padded (value 0, column 0) where a row is shorter
-// than the block's longest; a u8 length per row tells the consumer which
-// levels to add (a padded product is formed but never added, so signed
-// zeros and non-finite x stay exactly the reference's).  A block is L x 256 entries, contiguous,
-// so the producer still streams it with two 1-D bulk copies per chunk of
-// levels, and there is no row_ptr stream at all (8 B per row less per
-// product).  Consumer thread t reads entry k * 256 + t: consecutive lanes
-// read consecutive shared-memory words (no bank conflicts), the level count
-// is CTA-uniform, and the loop has no per-thread bounds.  Each row still sums
-// its products sequentially in ascending column order with rounded products
-// and rounded adds, so the result is bitwise kernels.py:95-100's.
+// of the block holds the k-th nonzero of each of its 256 rows, padded where a
+// row is shorter than the block's longest.  A u8 length per row tells the
+// consumer which levels to add: a padded product is formed but never added,
+// so signed zeros and non-finite x stay exactly the reference's.  A block is
+// L x 256 entries, contiguous, so the matrix stream is one or two 1-D bulk
+// copies per chunk of levels, and there is no row_ptr stream (8 B per row
+// less per product).  Consumer thread t reads entry k * 256 + t: consecutive
+// lanes read consecutive shared-memory words, the level count is CTA-uniform,
+// and the loop has no per-thread bounds.  Each row still sums its products
+// sequentially in ascending column order with rounded products and rounded
+// adds: bitwise kernels.py:95-100's row sum.
 //
-// Value dictionary (DICT): when the operator holds at most 256 distinct
-// values (discretised constant-coefficient operators: 7 or 27), the value
-// stream is a u8 index per entry into a dictionary the CTA keeps in shared
-// memory — 3 bytes per nonzero instead of 10 from HBM, and chunk stages small
-// enough for a third block slot.  The f64 looked up is bit for bit the
-// uploaded value, so nothing changes in the arithmetic.
+// Three value streams (SellView / kSell*), chosen at upload (core.cu):
+//   kSellF64    f64 value + u16 window-local column per entry (10 B).
+//   kSellDictV  at most 256 distinct f64 bit patterns in the operator
+//               (constant-coefficient discretisations: 7 or 27): a u8 index
+//               into a dictionary the CTA keeps in shared memory + the u16
+//               column (3 B).  The f64 looked up is the uploaded bit pattern.
+//   kSellPairs  also at most 256 distinct (value, staged column - row slot)
+//               pairs (every interior row of a stencil repeats the same
+//               ones): one u8 per entry into a dictionary of 16-byte pairs
+//               (1 B); one LDS.128 gives the value and the x address.
 //
-// Pair dictionary (MODE 2): when also the (value, column - row) pairs are
-// few — every interior row of a constant-coefficient stencil repeats the
-// same 7 or 27 — one u8 per entry indexes a dictionary of (value, staged
-// offset relative to the row's own slot position): 1 byte per nonzero, and
-// one 16-byte shared-memory load gives both the value and the x address.
+// Two producer warps: one streams the matrix chunks (and runs ahead of the
+// grid dependency), one fills the block slots with one copy stream per lane.
 //
 // Used for window-mode operators whose padding is small (stencil-like row
 // lengths: configs 1, 2, 4, 5); band mode, gathered x and ragged matrices
