@@ -398,11 +398,6 @@ PBS_EXPORT int pbs_destroy(pbs_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   drop_ws_cache(ctx);
   buf_flush(ctx);
-  if (ctx->copy_stream) {
-    cudaStreamDestroy(ctx->copy_stream);
-    cudaEventDestroy(ctx->ev_alloc);
-    cudaEventDestroy(ctx->ev_values);
-  }
   cudaFree(ctx->scratch);
   cudaFree(ctx->partials);
   cudaFree(ctx->tmp_state);
@@ -784,10 +779,6 @@ static int build_sell(pbs_ctx* ctx, pbs_mat* m) {
     free_sell(ctx, m);
     return PBS_OK;
   }
-  if (ctx->values_pending) {  // upload_arrays: the values arrive on the copy stream
-    CK(cudaStreamWaitEvent(s, ctx->ev_values, 0));
-    ctx->values_pending = false;
-  }
   // value dictionary (PBS_SELL_DICT=0: keep the f64 value stream)
   unsigned long long* table = nullptr;
   unsigned char* slot_idx = nullptr;
@@ -992,24 +983,11 @@ static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const
                          const double* values) {
   const long long n_rows = m->n_rows, n_cols = m->n_cols, nnz = m->nnz;
   cudaStream_t s = ctx->stream;
-  // The values travel on a second stream, after the indices on the copy
-  // engine: the x windows, window-local columns and sliced-ELL levels need
-  // only row_ptr and col_idx, so those kernels (and the host decisions
-  // between them) run while the values are still in flight; the value
-  // dictionary, the fill and everything later on `s` wait for ev_values.
-  if (!ctx->copy_stream) {
-    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-    CK(cudaEventCreateWithFlags(&ctx->ev_alloc, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ctx->ev_values, cudaEventDisableTiming));
-  }
   CK(cudaMemcpyAsync(m->rp, row_ptr, sizeof(long long) * (n_rows + 1), cudaMemcpyHostToDevice, s));
   if (nnz > 0) {
-    CK(cudaEventRecord(ctx->ev_alloc, s));  // m->v is allocated (and its tail cleared) in s's order
-    CK(cudaStreamWaitEvent(ctx->copy_stream, ctx->ev_alloc, 0));
+    CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, s));
     if (col_bytes == 4) {
       CK(cudaMemcpyAsync(m->ci, col_idx, sizeof(int) * nnz, cudaMemcpyHostToDevice, s));
-      CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->copy_stream));
-      CK(cudaEventRecord(ctx->ev_values, ctx->copy_stream));
     } else {
       // stage int64 indices in chunks and narrow on the device
       const long long chunk = 1LL << 24;
@@ -1024,20 +1002,15 @@ static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const
                            cudaMemcpyHostToDevice, s));
         cvt_i64_i32_kernel<<<ctx->sms * 4, 256, 0, s>>>(tmp, m->ci + off, len, bad, n_cols);
       }
-      CK(cudaMemcpyAsync(m->v, values, sizeof(double) * nnz, cudaMemcpyHostToDevice, ctx->copy_stream));
-      CK(cudaEventRecord(ctx->ev_values, ctx->copy_stream));
       int hbad = 0;
       CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       buf_free(ctx, tmp);
       buf_free(ctx, bad);
-      if (hbad) {
-        cudaStreamSynchronize(ctx->copy_stream);
-        return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
-      }
+      if (hbad) return set_err(ctx, PBS_ERR_INVALID, "column index out of range");
     }
   }
-  CK(cudaStreamSynchronize(s));  // row_ptr and col_idx are on the device; the values may not be yet
+  CK(cudaStreamSynchronize(s));
   g_upt.mark("h2d+narrow");
   m->blk_nnz_max = 0;
   for (long long r0 = 0; r0 < n_rows; r0 += kPipeRows) {
@@ -1045,13 +1018,7 @@ static int upload_arrays(pbs_ctx* ctx, pbs_mat* m, const int64_t* row_ptr, const
     const long long bn = row_ptr[r1] - row_ptr[r0];
     if (bn > m->blk_nnz_max) m->blk_nnz_max = bn;
   }
-  ctx->values_pending = nnz > 0;
-  int rc = compute_xwin(ctx, m);
-  if (ctx->values_pending) {  // no layout step needed the values: order the rest of `s` behind them here
-    cudaStreamWaitEvent(s, ctx->ev_values, 0);
-    ctx->values_pending = false;
-  }
-  return rc;
+  return compute_xwin(ctx, m);
 }
 
 PBS_EXPORT int pbs_csr_upload(pbs_ctx* ctx, int64_t n_rows, int64_t n_cols, int64_t nnz,
@@ -1408,7 +1375,6 @@ PBS_EXPORT int pbs_mat_free(pbs_mat* m) {
   if (!m) return PBS_OK;
   cudaSetDevice(m->ctx->device);
   cudaStreamSynchronize(m->ctx->stream);
-  if (m->ctx->copy_stream) cudaStreamSynchronize(m->ctx->copy_stream);  // an upload that failed half way
   if (m->ws && !m->part.dist) {
     drop_ws_cache(m->ctx);
     m->ctx->ws_cache = m->ws;

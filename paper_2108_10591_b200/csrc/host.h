@@ -105,10 +105,6 @@ struct pbs_ctx {
   // at all.  (Going back to the stream-ordered pool each time stalled an
   // upload for 20-700 ms every few dozen calls, whenever the pool had split
   // a cached block and had to map new memory.)
-  // upload: the values' H2D copy runs on its own stream beside the index-only layout kernels
-  cudaStream_t copy_stream = nullptr;
-  cudaEvent_t ev_alloc = nullptr, ev_values = nullptr;
-  bool values_pending = false;
   std::multimap<size_t, void*> spare;
   std::map<void*, size_t> spare_sizes;  // live buffers that came from buf_alloc
   size_t spare_bytes = 0;
