@@ -316,15 +316,15 @@ struct EpiK12T {  // K1 (As = A s) fused with block 1 of the iteration (row-loca
     const double rv = v[0], pv = v[1], uv = v[2], sv = v[3], tv = v[4], yv = v[5];
     const double lv = v[6], gv = v[7], wv = v[8], zv = v[9], xv = v[10];
     const double pn = asd(rv, beta, pv, uv);              // p = r + beta*(p - u)
-    const double o = lc2(1.0, sv, beta, tv);              // o = s + beta*t
+    const double o = add(sv, mul(beta, tv));               // o = s + beta*t   (1.0 * s is s: no product issued)
     const double un = lcn(zeta, o, eta, yv, beta, uv);    // u = zeta*o + eta*(y + beta*u)
-    const double q = lc2(1.0, asv, beta, lv);             // q = As + beta*l
+    const double q = add(asv, mul(beta, lv));              // q = As + beta*l
     const double wn = lcn(zeta, q, eta, gv, beta, wv);    // w = zeta*q + eta*(g + beta*w)
-    const double tn = lc2(1.0, o, -1.0, wn);              // t = o - w
+    const double tn = sub(o, wn);                          // t = o - w
     const double zn = lc3(zeta, rv, eta, zv, -alpha, un); // z = zeta*r + eta*z - alpha*u
     const double yn = lc3(zeta, sv, eta, yv, -alpha, wn); // y = zeta*s + eta*y - alpha*w
-    const double xn = lc3(1.0, xv, alpha, pn, 1.0, zn);   // x = x + alpha*p + z
-    const double rn = lc3(1.0, rv, -alpha, o, -1.0, yn);  // r = r - alpha*o - y
+    const double xn = add(add(xv, mul(alpha, pn)), zn);    // x = x + alpha*p + z
+    const double rn = sub(add(rv, mul(-alpha, o)), yn);    // r = r - alpha*o - y
     p[i] = pn;
     u[i] = un;
     w[i] = wn;
@@ -406,15 +406,15 @@ struct EpiK1opp {
     const double rv = v[0], pv = v[1], uv = v[2], sv = v[3], tv = v[4], yv = v[5];
     const double lv = v[6], gv = v[7], wv = v[8], zv = v[9], xv = v[10];
     const double pn = asd(rv, beta, pv, uv);              // p = r + beta*(p - u)
-    const double o = lc2(1.0, sv, beta, tv);              // o = s + beta*t
+    const double o = add(sv, mul(beta, tv));               // o = s + beta*t   (1.0 * s is s: no product issued)
     const double un = lcn(zeta, o, eta, yv, beta, uv);    // u = zeta*o + eta*(y + beta*u)
-    const double q = lc2(1.0, asv, beta, lv);             // q = As + beta*l
+    const double q = add(asv, mul(beta, lv));              // q = As + beta*l
     const double wn = lcn(zeta, q, eta, gv, beta, wv);    // w = zeta*q + eta*(g + beta*w)
-    const double tn = lc2(1.0, o, -1.0, wn);              // t = o - w
+    const double tn = sub(o, wn);                          // t = o - w
     const double zn = lc3(zeta, rv, eta, zv, -alpha, un); // z = zeta*r + eta*z - alpha*u
     const double yn = lc3(zeta, sv, eta, yv, -alpha, wn); // y = zeta*s + eta*y - alpha*w
-    const double xn = lc3(1.0, xv, alpha, pn, 1.0, zn);   // x = x + alpha*p + z
-    const double rn = lc3(1.0, rv, -alpha, o, -1.0, yn);  // r = r - alpha*o - y
+    const double xn = add(add(xv, mul(alpha, pn)), zn);    // x = x + alpha*p + z
+    const double rn = sub(add(rv, mul(-alpha, o)), yn);    // r = r - alpha*o - y
     p[i] = pn;
     u[i] = un;
     w[i] = wn;
@@ -483,10 +483,10 @@ struct EpiK3T {
   __device__ void row(long long i, double aw, const double* v) {
     if (!isfinite(aw)) report_nonfinite(st, tag, i);
     const double asv = v[0];
-    const double q = lc2(1.0, asv, beta, v[1]);               // q = As + beta*l
-    const double lv = lc2(1.0, q, -1.0, aw);                  // l = q - A w
+    const double q = add(asv, mul(beta, v[1]));               // q = As + beta*l  (1.0 * As is As)
+    const double lv = sub(q, aw);                              // l = q - A w
     const double gv = lc3(zeta, asv, eta, v[2], -alpha, aw);  // g = zeta As + eta g - alpha Aw
-    const double sv = lc3(1.0, v[3], -alpha, q, -1.0, gv);    // s = s - alpha q - g
+    const double sv = sub(add(v[3], mul(-alpha, q)), gv);      // s = s - alpha q - g
     l[i] = lv;
     g[i] = gv;
     s[i] = sv;
