@@ -381,7 +381,8 @@ def run_single(args):
                    "operator": args.operator, "iterations_per_solve": avg_it, "time_to_tol_ms": total_ms / args.steps,
                    "parallelism": "single GPU", "device_layout": lay,
                    "iterations_reference": ITER_REF.get(cfg_name),
-                   "l2": "inputs larger than L2 (operator + 18 workspace vectors >> 126 MB)", "graphs": True},
+                   "l2": (f"inputs larger than L2: {(18 * 8 * n + m_eng) / 1e6:.0f} MB of workspace vectors and "
+                          "operator per iteration against 126 MB, no flush between steps"), "graphs": True},
         "roofline": {"bound": "hbm", "achieved": dom["GBps"], "peak": peak, "unit": "GB/s", "frac": dom["frac"],
                      "traffic": traffic, "kernel": dom["name"], "alg_bytes_per_launch": dom["alg_bytes"],
                      "engine_bytes_per_launch": dom["engine_bytes"], "engine_frac": dom["engine_frac"],
