@@ -474,7 +474,10 @@ __global__ void __launch_bounds__(kSellThreads, MINB) sell_pipe_kernel(SellView 
   const int t = threadIdx.x;
   int cs = 0, bs = 0;
   uint32_t cph = 0, bph = 0;
-  constexpr int G = MINB == 1 ? 8 : 4;
+#ifndef PBS_SELL_G  // staged products in flight per row at 2 CTAs/SM (-D override for sweeps)
+#define PBS_SELL_G 4
+#endif
+  constexpr int G = MINB == 1 ? 8 : PBS_SELL_G;
   for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
     mbar_wait(&bfull[bs], bph);
     const unsigned char* bst = blk0 + (size_t)bs * BL.bytes;
