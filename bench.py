@@ -317,7 +317,12 @@ def run_single(args):
     tr_path = os.path.join(ROOT, "profiles", "dram_bytes.json")  # the committed ncu --set full capture
     if os.path.exists(tr_path) and cfg_name == "c2" and not stencil:
         try:
-            traffic = json.load(open(tr_path)).get(dom_key, {}).get("dram_bytes_per_launch")
+            tr = json.load(open(tr_path))
+            traffic = tr.get(dom_key, {}).get("dram_bytes_per_launch")
+            for kname, kd in kernels.items():  # ncu's DRAM bytes per launch over this run's launch time
+                if tr.get(kname, {}).get("dram_bytes_per_launch"):
+                    kd["traffic"] = tr[kname]["dram_bytes_per_launch"]
+                    kd["traffic_frac"] = kd["traffic"] / (kd["avg_us"] * 1e-6) / 1e9 / peak
         except Exception:
             traffic = None
 
