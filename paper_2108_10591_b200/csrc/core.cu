@@ -556,16 +556,25 @@ __device__ __forceinline__ unsigned dict_hash(unsigned long long b) {
 // ctl[0]: distinct values seen, ctl[1]: gave up (too many, or the reserved pattern)
 __global__ void dict_insert_kernel(const double* v, long long nnz, unsigned long long* table, int* ctl) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  unsigned long long last = kDictEmpty;
+  // the thread's last eight distinct patterns: an operator with a handful of
+  // values never goes back to the table after its first few nonzeros
+  unsigned long long seen[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) seen[k] = kDictEmpty;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < nnz; i += stride) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(v[i]);
-    if (b == last) continue;
-    last = b;
-    if (*(volatile int*)(ctl + 1)) return;
-    if (b == kDictEmpty) {
+    if (b == kDictEmpty) {  // the free-slot marker itself: no dictionary for this operator
       ctl[1] = 1;
       return;
     }
+    bool hit = false;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) hit |= b == seen[k];
+    if (hit) continue;
+#pragma unroll
+    for (int k = 7; k > 0; --k) seen[k] = seen[k - 1];
+    seen[0] = b;
+    if (*(volatile int*)(ctl + 1)) return;
     unsigned h = dict_hash(b);
     for (int probe = 0; probe < kDictSlots; ++probe, h = (h + 1) & (kDictSlots - 1)) {
       unsigned long long cur = *(volatile unsigned long long*)(table + h);
@@ -656,6 +665,9 @@ __device__ __forceinline__ void pair_insert(unsigned long long key, unsigned lon
 __global__ void pair_insert_kernel(const long long* rp, const double* v, const unsigned short* wc, long long n_rows,
                                    long long nblk, const long long* soff, const unsigned long long* vtable,
                                    const unsigned char* vslot_idx, unsigned long long* table, int* ctl) {
+  unsigned long long seen[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) seen[q] = kDictEmpty;  // no key has this pattern (value index < 256 or the pad key)
   for (long long b = blockIdx.x; b < nblk; b += gridDim.x) {
     if (*(volatile int*)(ctl + 1)) return;
     const long long r = b * kPipeRows + threadIdx.x;
@@ -666,13 +678,18 @@ __global__ void pair_insert_kernel(const long long* rp, const double* v, const u
       len = (int)(rp[r + 1] - s);
     }
     const int L = (int)((soff[b + 1] - soff[b]) / kPipeRows);
-    unsigned long long last = kDictEmpty;
     for (int k = 0; k < len; ++k) {
       const unsigned vi = dict_lookup(vtable, vslot_idx, v[s + k]);
       const int rel = (int)wc[s + k] - (int)threadIdx.x;
       const unsigned long long key = ((unsigned long long)vi << 32) | (unsigned)rel;
-      if (key != last) pair_insert(key, table, ctl);
-      last = key;
+      bool hit = false;  // the thread's last eight distinct pairs (a stencil row repeats the previous row's)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) hit |= key == seen[q];
+      if (hit) continue;
+#pragma unroll
+      for (int q = 7; q > 0; --q) seen[q] = seen[q - 1];
+      seen[0] = key;
+      pair_insert(key, table, ctl);
     }
     if (len < L) pair_insert(kPairPadKey, table, ctl);
   }

@@ -232,6 +232,27 @@ def test_sell_pair_dictionary_on_stencil_csr(pb, cfg, k):
     two.free()
 
 
+def test_sell_dictionary_refuses_its_own_marker(pb):
+    """The value hash set marks free slots with one NaN bit pattern; an
+    operator that holds exactly that pattern gets no dictionary (f64 value
+    stream) and its products keep the reference's NaN placement."""
+    rng = np.random.default_rng(11)
+    n = 2000
+    pool = np.array([1.0, -0.5, 2.0, np.float64(np.uint64(0x7ff8dead00000001).view(np.float64))])
+    rp, ci, v = _banded(n, np.full(n, 9), 30, rng, lambda m: pool[np.arange(m) % 3])
+    v[123] = pool[3]  # one entry with the marker pattern
+    dm = _upload(rp, ci, v, PBS_PLAIN_TPR=0)
+    assert dm.layout()["layout"] == "sell", dm.layout()
+    x = rng.standard_normal(n)
+    ref = orc.spmv(rp, ci, v, x)
+    bad = int(np.flatnonzero(~np.isfinite(ref))[0])
+    got = _spmv_dev(dm, x, expect_bad=bad)
+    assert np.array_equal(np.isnan(got), np.isnan(ref))
+    ok = np.isfinite(ref)
+    assert np.array_equal(_bits(got[ok]), _bits(ref[ok]))
+    dm.free()
+
+
 def test_sell_refused_for_ragged_rows(pb):
     """Row lengths uniform in [5, 30] (config 3's shape) would pad each block
     to its longest row: the layout is refused and CSR order kept."""
