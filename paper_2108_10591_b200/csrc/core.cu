@@ -2,6 +2,7 @@
 // matrix-free stencils, stencil -> CSR on the device), workspaces, the
 // kernel-table entry points and the single-GPU C-ABI declared in
 // include/pbsafe.h.
+#include <array>
 #include <cub/device/device_scan.cuh>
 
 #include "host.h"
@@ -429,6 +430,11 @@ __global__ void cvt_i64_i32_kernel(const long long* in, int* out, long long n, i
   }
 }
 
+constexpr int kBinsOut = 1024;  // occupied offset bins read back, at most
+
+__global__ void bins_init_kernel(int* bmin, int* bmax, int* occ, int* wide);
+__global__ void bins_compact_kernel(const int* bmin, const int* bmax, int* occ);
+
 // Offset histogram for the x windows: bin = floor((col - row) / 256); per bin
 // the min / max offset seen (warp-aggregated atomics); |bin| >= kBins -> wide.
 constexpr int kBins = 65536;
@@ -464,6 +470,30 @@ __global__ void offset_bins_kernel(const long long* rp, const int* ci, long long
     }
   }
   (void)r_first;
+}
+
+__global__ void bins_init_kernel(int* bmin, int* bmax, int* occ, int* wide) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < 2 * kBins) {
+    bmin[b] = 0x7fffffff;
+    bmax[b] = (int)0x80000000;
+  }
+  if (b == 0) {
+    occ[0] = 0;
+    *wide = 0;
+  }
+}
+
+// occupied bins -> (bin, min, max) triples in occ[1..] (any order; occ[0] counts them all)
+__global__ void bins_compact_kernel(const int* bmin, const int* bmax, int* occ) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= 2 * kBins || bmin[b] > bmax[b]) return;
+  const int k = atomicAdd(occ, 1);
+  if (k < kBinsOut) {
+    occ[1 + 3 * k] = b;
+    occ[2 + 3 * k] = bmin[b];
+    occ[3 + 3 * k] = bmax[b];
+  }
 }
 
 // Window-local column of every nonzero: the staged offset of x[col] in its
@@ -926,28 +956,34 @@ int compute_xwin(pbs_ctx* ctx, pbs_mat* m) {
   CK(buf_alloc(ctx, &bmin, sizeof(int) * 2 * kBins));
   CK(buf_alloc(ctx, &bmax, sizeof(int) * 2 * kBins));
   CK(buf_alloc(ctx, &wide, sizeof(int)));
-  std::vector<int> hmin(2 * kBins, 0x7fffffff), hmax(2 * kBins, (int)0x80000000);
-  CK(cudaMemcpyAsync(bmin, hmin.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(bmax, hmax.data(), sizeof(int) * 2 * kBins, cudaMemcpyHostToDevice, s));
-  CK(cudaMemsetAsync(wide, 0, sizeof(int), s));
+  // The two 512 KB bin arrays stay on the device: they are initialised there,
+  // and only the occupied bins (a handful for any matrix that windows) come
+  // back, as (bin, min, max) triples.
+  int* occ = nullptr;  // [0] count, then kBinsOut triples
+  CK(buf_alloc(ctx, &occ, sizeof(int) * (1 + 3 * kBinsOut)));
+  bins_init_kernel<<<(2 * kBins + 255) / 256, 256, 0, s>>>(bmin, bmax, occ, wide);
   offset_bins_kernel<<<ctx->sms * 8, 256, 0, s>>>(m->rp, m->ci, m->n_rows, bmin, bmax, wide);
+  bins_compact_kernel<<<(2 * kBins + 255) / 256, 256, 0, s>>>(bmin, bmax, occ);
   int hwide = 0;
-  CK(cudaMemcpyAsync(hmin.data(), bmin, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(hmax.data(), bmax, sizeof(int) * 2 * kBins, cudaMemcpyDeviceToHost, s));
+  std::vector<int> hocc(1 + 3 * kBinsOut);
+  CK(cudaMemcpyAsync(hocc.data(), occ, sizeof(int) * (1 + 3 * kBinsOut), cudaMemcpyDeviceToHost, s));
   CK(cudaMemcpyAsync(&hwide, wide, sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   g_upt.mark("bins");
   buf_free(ctx, bmin);
   buf_free(ctx, bmax);
   buf_free(ctx, wide);
-  if (hwide) return PBS_OK;
+  buf_free(ctx, occ);
+  if (hwide || hocc[0] > kBinsOut) return PBS_OK;  // offsets in more bins than any window set covers: gather x
+  std::vector<std::array<int, 3>> bins(hocc[0]);
+  for (int k = 0; k < hocc[0]; ++k) bins[k] = {hocc[1 + 3 * k], hocc[2 + 3 * k], hocc[3 + 3 * k]};
+  std::sort(bins.begin(), bins.end());  // ascending bin
   std::vector<std::pair<int, int>> cl;  // [min, max] offsets
-  for (int b = 0; b < 2 * kBins; ++b) {
-    if (hmin[b] > hmax[b]) continue;
-    if (!cl.empty() && (long long)hmin[b] - cl.back().second <= kPipeRows + 4)
-      cl.back().second = hmax[b] > cl.back().second ? hmax[b] : cl.back().second;
+  for (const auto& b : bins) {
+    if (!cl.empty() && (long long)b[1] - cl.back().second <= kPipeRows + 4)
+      cl.back().second = b[2] > cl.back().second ? b[2] : cl.back().second;
     else
-      cl.push_back({hmin[b], hmax[b]});
+      cl.push_back({b[1], b[2]});
   }
   while (cl.size() > (size_t)kMaxWin) {  // merge across the smallest gap
     size_t best = 0;
