@@ -253,6 +253,25 @@ def test_sell_dictionary_refuses_its_own_marker(pb):
     dm.free()
 
 
+def test_wide_random_matrix_gathers_x(pb):
+    """Columns anywhere in the row: offsets occupy thousands of 256-wide bins
+    (more than the upload reads back), no x window or band fits, and the CSR
+    engine gathers x from L2 — still the reference's sums."""
+    rng = np.random.default_rng(5)
+    n = 400_000
+    k = 6
+    ci = np.sort(rng.integers(0, n, (n, k)), axis=1)
+    ci[:, 0] = np.minimum(ci[:, 0], np.arange(n))  # keep rows sorted and mostly distinct
+    ci = np.sort(ci, axis=1).reshape(-1).astype(np.int64)
+    rp = np.arange(0, n * k + 1, k, dtype=np.int64)
+    v = rng.uniform(-1, 1, n * k)
+    dm = _upload(rp, ci, v)
+    assert dm.layout()["layout"] == "csr-gather", dm.layout()
+    x = rng.standard_normal(n)
+    assert np.array_equal(_bits(_spmv_dev(dm, x)), _bits(orc.spmv(rp, ci, v, x)))
+    dm.free()
+
+
 def test_sell_refused_for_ragged_rows(pb):
     """Row lengths uniform in [5, 30] (config 3's shape) would pad each block
     to its longest row: the layout is refused and CSR order kept."""
