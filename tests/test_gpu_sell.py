@@ -253,6 +253,32 @@ def test_sell_dictionary_refuses_its_own_marker(pb):
     dm.free()
 
 
+def test_sell_pairs_rows_longer_than_one_chunk(pb):
+    """45 constant offsets per row: the pair dictionary applies (45 pairs plus
+    the clamped first block's) and a block's levels span two 32-level chunks."""
+    rng = np.random.default_rng(45)
+    n = 3000
+    offs = np.sort(rng.choice(np.arange(-70, 71), size=45, replace=False))
+    vals = rng.standard_normal(45)
+    rows, cols, vv = [], [], []
+    for i in range(n):
+        ok = (i + offs >= 0) & (i + offs < n)
+        rows.append(np.full(int(ok.sum()), i))
+        cols.append(i + offs[ok])
+        vv.append(vals[ok])
+    ci = np.concatenate(cols).astype(np.int64)
+    rp = np.zeros(n + 1, dtype=np.int64)
+    np.add.at(rp, np.concatenate(rows).astype(np.int64) + 1, 1)
+    rp = np.cumsum(rp)
+    v = np.concatenate(vv)
+    dm = _upload(rp, ci, v, PBS_SELL_PAD=50)
+    lay = dm.layout()
+    assert lay["layout"] == "sell-pairs" and lay["max_row"] == 45, lay
+    x = rng.standard_normal(n)
+    assert np.array_equal(_bits(_spmv_dev(dm, x)), _bits(orc.spmv(rp, ci, v, x)))
+    dm.free()
+
+
 def test_wide_random_matrix_gathers_x(pb):
     """Columns anywhere in the row: offsets occupy thousands of 256-wide bins
     (more than the upload reads back), no x window or band fits, and the CSR
